@@ -1,0 +1,205 @@
+/*
+ * moeb200.h -- C ABI of libmoeb200.so, the B200-native MoE-offloading decode engine.
+ *
+ * Every entry point is `extern "C"`, takes plain pointers and sizes (no torch or
+ * CUDA runtime types in the signatures: streams are passed as `void*` holding a
+ * cudaStream_t, 0 = the legacy default stream) and returns a moe_status.
+ * On failure, moe_last_error() returns a thread-local message.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/moesim):
+ *   moe_replay_policy          <- kernels.replay_policy            kernels.py:60-147
+ *   moe_replay_policy_layers   <- simulate.simulate's layer loop   simulate.py:167-174
+ *   moe_policy_step            <- policies.policy_step             policies.py:140-228
+ *   moe_gate_topk_f64          <- toymoe._gate_topk / gate_select  toymoe.py:99-126
+ *   moe_toy_forward_f64        <- toymoe._forward / forward_token  toymoe.py:129-146
+ *   moe_engine_*               <- toymoe.run_model decode loop     toymoe.py:159-190
+ *                                 + per-layer cache (simulate.py:140-184) live on device
+ * Status codes map onto the reference exception taxonomy (errors.py:8-31):
+ *   MOE_INVALID_CONFIG -> ConfigError, MOE_NONFINITE -> FloatingPointError
+ *   (toymoe.py:109-110).
+ */
+#ifndef MOEB200_H
+#define MOEB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_ABI_VERSION 1
+
+typedef int32_t moe_status;
+enum {
+  MOE_OK = 0,
+  MOE_INVALID_CONFIG = 1, /* ConfigError */
+  MOE_NONFINITE = 2,      /* FloatingPointError("gate logits are not finite") */
+  MOE_CUDA_ERROR = 3,
+  MOE_OOM = 4,
+};
+
+/* Policy codes shared with the reference (kernels.py:53-57, simulate.py:23). */
+enum { MOE_P_LRU = 0, MOE_P_LFU = 1, MOE_P_LFU_AGED = 2, MOE_P_OPT = 3 };
+
+/* Expert bodies. TOY_TANH is the reference's expert (toymoe.py:143-145),
+ * SWIGLU the Mixtral-shaped north-star expert (w2 . (silu(w1 h) * w3 h)). */
+enum { MOE_EXPERT_TOY_TANH_F32 = 0, MOE_EXPERT_SWIGLU_BF16 = 1 };
+
+/* Speculative prefetch issue point. */
+enum {
+  MOE_PREFETCH_OFF = 0,
+  MOE_PREFETCH_EARLY = 1 /* gate_{l+1}(h'_l): post-mixing state of layer l */
+};
+
+const char* moe_last_error(void);
+int32_t moe_abi_version(void);
+/* Number of CUDA kernels this library has launched in this process (all entry points). */
+uint64_t moe_kernel_launches(void);
+
+/* ---- cache policy: offline replay (K7) ------------------------------------------- */
+
+/* Replay one layer's activation stream through a policy, on the GPU.
+ * acts_dev: (T, K) int64, C-contiguous, rows ascending distinct ids in [0, E).
+ * resident_before_dev / evicted_dev: (T, E) uint8 outputs (device).
+ * decay_factor / decay_period are only read for MOE_P_LFU_AGED (pass 1.0 / 1 otherwise).
+ * Bit-exact with kernels.replay_policy (kernels.py:60-147). E <= 256, K <= C. */
+moe_status moe_replay_policy(const int64_t* acts_dev, int64_t T, int32_t K, int32_t E,
+                             int32_t C, int32_t policy, double decay_factor,
+                             int64_t decay_period, uint8_t* resident_before_dev,
+                             uint8_t* evicted_dev, void* stream);
+
+/* L independent layers in one launch: acts (L, T, K), outputs (L, T, E). */
+moe_status moe_replay_policy_layers(const int64_t* acts_dev, int32_t L, int64_t T, int32_t K,
+                                    int32_t E, int32_t C, int32_t policy, double decay_factor,
+                                    int64_t decay_period, uint8_t* resident_before_dev,
+                                    uint8_t* evicted_dev, void* stream);
+
+/* ---- cache policy: one step with explicit state (policies.policy_step) ------------ */
+
+/* State arrays (device, length E, updated in place):
+ *   resident u8, last_touch i64 (larger = more recent; ties break to the lower id),
+ *   freq f64.  *step is the step counter (host value, used for lfu-aged decay).
+ * act_dev: n_act int64 ids.  For MOE_P_OPT, future_ids_dev / future_offsets_dev describe
+ * the remaining stream as a ragged array (n_future sets; offsets has n_future+1 entries).
+ * Outputs (device, length E): resident_before u8, evicted u8.
+ * The caller validates n_act <= C (policies.py:153-156). */
+moe_status moe_policy_step(uint8_t* resident_dev, int64_t* last_touch_dev, double* freq_dev,
+                           int64_t step, int32_t E, int32_t C, int32_t policy,
+                           double decay_factor, int64_t decay_period, const int64_t* act_dev,
+                           int32_t n_act, const int64_t* future_ids_dev,
+                           const int64_t* future_offsets_dev, int64_t n_future,
+                           uint8_t* resident_before_dev, uint8_t* evicted_dev, void* stream);
+
+/* ---- gate (K1) on arbitrary gates, fp64 (toymoe.gate_select / speculate_next) ------ */
+
+/* h_dev (d,), w_dev (d, E) in the reference layout (toymoe.py:50), bias_dev (E,) or NULL.
+ * Outputs: order_dev (k,) int64 prob-desc with ties to the lower id, probs_dev (E,) f64.
+ * Returns MOE_NONFINITE if any logit is non-finite. */
+moe_status moe_gate_topk_f64(const double* h_dev, const double* w_dev, const double* bias_dev,
+                             int32_t d, int32_t E, int32_t k, int64_t* order_dev,
+                             double* probs_dev, void* stream);
+
+/* One toy layer step, fp64 (toymoe._forward, toymoe.py:138-146):
+ * h = x + alpha * (x @ M); gate; out = h + sum_{e in sel, prob-desc} p_e * tanh(h @ W1_e) @ W2_e.
+ * mixing (d, d), gate_w (d, E), gate_b (E,) or NULL, w1/w2 (E, d, d), all reference layout. */
+moe_status moe_toy_forward_f64(const double* x_dev, const double* mixing_dev,
+                               const double* gate_w_dev, const double* gate_b_dev,
+                               const double* w1_dev, const double* w2_dev, int32_t d, int32_t E,
+                               int32_t k, double alpha, double* out_dev, int64_t* selected_dev,
+                               double* probs_dev, void* stream);
+
+/* ---- the offload decode engine ------------------------------------------------------ */
+
+typedef struct moe_engine moe_engine;
+
+typedef struct {
+  int32_t num_layers;     /* L */
+  int32_t num_experts;    /* E (<= 32 for the live engine) */
+  int32_t top_k;          /* K */
+  int32_t hidden_dim;     /* d */
+  int32_t ffn_dim;        /* f (SwiGLU); ignored for the toy expert (f = d) */
+  int32_t expert_kind;    /* MOE_EXPERT_* */
+  int32_t cache_size;     /* C policy slots per layer (simulate.SimConfig.cache_size) */
+  int32_t policy;         /* MOE_P_LRU / MOE_P_LFU / MOE_P_LFU_AGED (OPT is offline-only) */
+  double decay_factor;    /* lfu-aged only */
+  int64_t decay_period;   /* lfu-aged only */
+  float mixing_scale;     /* alpha (toymoe.py:140) */
+  int32_t prefetch;       /* MOE_PREFETCH_* */
+  int32_t renormalize;    /* 0: reference routing (softmax over E, no renorm, toymoe.py:122-123)
+                             1: Mixtral routing (renormalise the top-k probabilities) */
+  int32_t record_speculation; /* record the reference-definition guess (toymoe.py:178-180) */
+  int32_t max_tokens;     /* capacity of the device step-record ring */
+  int64_t chunk_bytes;    /* transfer chunk size (prefetch cancellation granularity) */
+  int32_t prefetch_depth; /* max prefetch chunks in flight on the copy stream */
+  int32_t device;
+} moe_engine_config;
+
+typedef struct {
+  int64_t tokens;           /* decode tokens processed */
+  int64_t steps;            /* (token, layer) steps */
+  int64_t hits, misses;     /* policy hits / misses */
+  int64_t h2d_bytes;        /* bytes copied host->device for experts (demand + prefetch) */
+  int64_t demand_bytes;     /* of which demand misses (== misses * expert_bytes w/o prefetch) */
+  int64_t prefetch_bytes;   /* of which speculative prefetch chunks issued */
+  int64_t prefetch_issued;  /* experts prefetched (guess not resident) */
+  int64_t prefetch_used;    /* prefetched experts adopted by a demand miss */
+  int64_t prefetch_wasted_bytes; /* bytes of prefetch chunks for guesses that were wrong */
+  int64_t expert_bytes;     /* bytes of one expert block */
+  double copy_busy_ms;      /* copy-stream busy time for demand transfers (events) */
+} moe_stats;
+
+moe_status moe_engine_create(const moe_engine_config* cfg, moe_engine** out);
+moe_status moe_engine_destroy(moe_engine* eng);
+
+/* Dense per-layer weights from host memory, reference layout (toymoe.py:74-83):
+ * mixing (d, d) as `x @ M`, gate_w (d, E), gate_b (E,). dtype: f32. */
+moe_status moe_engine_set_dense_f32(moe_engine* eng, int32_t layer, const float* mixing,
+                                    const float* gate_w, const float* gate_b);
+/* One toy expert from host memory, reference layout: w1, w2 (d, d) f32 (toymoe.py:82-83). */
+moe_status moe_engine_set_toy_expert_f32(moe_engine* eng, int32_t layer, int32_t expert,
+                                         const float* w1, const float* w2);
+/* Synthetic Mixtral-shaped weights from the counter-hash generator (moe_hash_weights). */
+moe_status moe_engine_init_random(moe_engine* eng, uint64_t seed);
+/* Host view of one expert block in the pinned store ([w1 | w3 | w2] bf16 or [W1t | W2t] f32). */
+moe_status moe_engine_expert_host_ptr(moe_engine* eng, int32_t layer, int32_t expert,
+                                      void** ptr, int64_t* bytes);
+/* Copy back the device-layout dense weights (for the oracle): mixing (d,d) in the device
+ * dtype's bytes, gate_w (E,d) f32, gate_b (E,) f32; host destinations. */
+moe_status moe_engine_dense_host(moe_engine* eng, int32_t layer, void* mixing, float* gate_w,
+                                 float* gate_b);
+
+/* Reset every per-layer cache to the cold state (policies.warm_state, policies.py:133-137). */
+moe_status moe_engine_reset(moe_engine* eng);
+
+/* Decode T tokens: h_in_dev (T, d) f32 device, h_out_dev (T, d) f32 device.
+ * Token t's step records go to ring position (tokens_done + t) % max_tokens. */
+moe_status moe_engine_decode(moe_engine* eng, const float* h_in_dev, int64_t T,
+                             float* h_out_dev, void* stream);
+
+/* Block until the engine's outstanding work is complete; reports MOE_NONFINITE if any
+ * gate produced non-finite logits since the last call. */
+moe_status moe_engine_sync(moe_engine* eng);
+
+/* Read the step records of tokens [t0, t0+T) (absolute token indices; must still be in
+ * the ring). Host outputs, any may be NULL:
+ *   acts (T, L, K) int64 sorted ascending; guessed (T, L-1, K) int64 sorted;
+ *   resident_before / evicted (T, L, E) uint8; probs (T, L, K) f32 in selection order. */
+moe_status moe_engine_records(moe_engine* eng, int64_t t0, int64_t T, int64_t* acts,
+                              int64_t* guessed, uint8_t* resident_before, uint8_t* evicted,
+                              float* probs);
+
+moe_status moe_engine_stats(moe_engine* eng, moe_stats* out);
+
+/* ---- synthetic weights (counter hash), shared with oracle/weights.c ---------------- */
+
+/* bf16 bits of element `index` of tensor `tensor_id` for seed `seed`, scaled to unit
+ * variance * std (uniform on [-sqrt(3), sqrt(3)) * std).  See DESIGN.md "Synthetic weights". */
+moe_status moe_hash_weights_bf16(uint64_t seed, uint64_t tensor_id, float std, int64_t n,
+                                 uint16_t* out_dev, void* stream);
+moe_status moe_hash_weights_f32(uint64_t seed, uint64_t tensor_id, float std, int64_t n,
+                                float* out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOEB200_H */

@@ -1,0 +1,212 @@
+"""ORACLE (test infrastructure only): numpy fp64 restatement of the reference model path.
+
+toy_*       restate moesim/toymoe.py line by line in numpy fp64 (the reference dtype):
+              draw order gate_w, gate_b, mixing, w1, w2, inputs ....... toymoe.py:73-83, 169
+              _softmax ................................................ toymoe.py:93-96
+              _gate_topk: z = h@W (+b), finite check, lexsort order ... toymoe.py:99-115
+              _forward: h = x + a*(x@M); out = h + sum p_e tanh(h@W1)@W2 toymoe.py:138-146
+              run_model loop with the guess before each layer >= 1 .... toymoe.py:175-185
+MixtralRef  the same _forward with the north-star SwiGLU expert, on the engine's synthetic
+            weights (counter hash, bf16-rounded, widened to fp64: "identical inputs").
+            layout="ref" keeps every matrix as (d_in, d_out) and computes `h @ W` like the
+            reference; layout="torch" is the tuned nn.Linear-layout fp32 variant (ii).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .native import hash_fill, replay_policy
+
+
+def softmax(z: np.ndarray) -> np.ndarray:
+    z = z - z.max()
+    ez = np.exp(z)
+    return ez / ez.sum()
+
+
+def gate_topk(h: np.ndarray, W: np.ndarray, b, k: int):
+    z = h @ W
+    if b is not None:
+        z = z + b
+    if not np.isfinite(z).all():
+        raise FloatingPointError("gate logits are not finite")
+    E = z.shape[0]
+    order = np.lexsort((np.arange(E), -z))[:k]
+    return order, softmax(z), z
+
+
+def toy_weights(L: int, E: int, d: int, skew: float, seed: int, tokens: int):
+    rng = np.random.default_rng(seed)
+    s = 1.0 / np.sqrt(d)
+    w = {
+        "gate_w": rng.standard_normal((L, d, E)) * s,
+        "gate_b": rng.standard_normal((L, E)) * skew,
+        "mixing": rng.standard_normal((L, d, d)),
+        "w1": rng.standard_normal((L, E, d, d)) * s,
+        "w2": rng.standard_normal((L, E, d, d)) * s,
+    }
+    w["inputs"] = rng.standard_normal((tokens, d))
+    return w
+
+
+def toy_forward(w: dict, x: np.ndarray, l: int, alpha: float, k: int):
+    h = x + alpha * (x @ w["mixing"][l])
+    sel, probs, z = gate_topk(h, w["gate_w"][l], w["gate_b"][l], k)
+    out = h.copy()
+    for e in sel:
+        out = out + probs[e] * (np.tanh(h @ w["w1"][l, e]) @ w["w2"][l, e])
+    return out, sel, probs, z
+
+
+def toy_run_model(L, E, K, d, alpha, skew, seed, T, weights=None, return_gaps=False):
+    """acts (T, L, K), guessed/actual (T, L-1, K); weights override for the
+    identical-inputs protocol.  With return_gaps, also the k-th/(k+1)-th logit gap per
+    (t, l) so near-ties can be reported."""
+    w = weights if weights is not None else toy_weights(L, E, d, skew, seed, T)
+    acts = np.zeros((T, L, K), np.int64)
+    guessed = np.zeros((T, max(L - 1, 0), K), np.int64)
+    gaps = np.full((T, L), np.inf)
+    for t in range(T):
+        h = w["inputs"][t]
+        for l in range(L):
+            if l >= 1:
+                g, _, _ = gate_topk(h, w["gate_w"][l], w["gate_b"][l], K)
+                guessed[t, l - 1] = np.sort(g)
+            h, sel, _, z = toy_forward(w, h, l, alpha, K)
+            acts[t, l] = np.sort(sel)
+            if K < E:
+                zs = np.sort(z)[::-1]
+                gaps[t, l] = zs[K - 1] - zs[K]
+    actual = acts[:, 1:, :].copy() if L >= 2 else np.zeros((T, 0, K), np.int64)
+    if L < 2 or T == 0:
+        guessed, actual = guessed[:0], actual[:0]
+    if return_gaps:
+        return acts, guessed, actual, gaps
+    return acts, guessed, actual
+
+
+def _tid(kind: int, layer: int = 0, expert: int = 0, matrix: int = 0) -> int:
+    return (kind << 40) | (layer << 16) | (expert << 4) | matrix
+
+
+def _std(n: int) -> float:
+    return float(np.float32(1.0 / math.sqrt(n)))
+
+
+class MixtralRef:
+    """CPU decode of the Mixtral-shaped engine path (SwiGLU experts) on identical inputs.
+
+    Weights are regenerated from the counter hash exactly as the engine's init_random:
+    mixing [d_out, d_in] bf16 std 1; gate_w [E, d] f32 std 1/sqrt(d); gate_b [E] f32 std 1;
+    w1, w3 [f, d] bf16 std 1/sqrt(d); w2 [d, f] bf16 std 1/sqrt(f).
+    """
+
+    def __init__(self, L, E, K, d, f, alpha, seed=42, layout="ref", threads=None,
+                 layers=None, renormalize=False):
+        self.L, self.E, self.K, self.d, self.f = L, E, K, d, f
+        self.alpha, self.seed, self.layout, self.threads = alpha, seed, layout, threads
+        self.renormalize = renormalize
+        self.dtype = np.float64 if layout == "ref" else np.float32
+        self.layers = list(range(L)) if layers is None else list(layers)
+        self._dense = {}
+        self._experts = {}
+
+    def _fill(self, tid, std, n):
+        if self.layout == "ref":
+            return hash_fill(self.seed, tid, std, n, "f64", self.threads)
+        return hash_fill(self.seed, tid, std, n, "f64", self.threads).astype(np.float32)
+
+    def dense(self, l):
+        if l not in self._dense:
+            d, E = self.d, self.E
+            M = self._fill(_tid(1, l), 1.0, d * d).reshape(d, d)             # [out, in]
+            gw = hash_fill(self.seed, _tid(2, l), _std(d), E * d, "f32", self.threads)
+            gb = hash_fill(self.seed, _tid(3, l), 1.0, E, "f32", self.threads)
+            gw = gw.astype(self.dtype).reshape(E, d)
+            gb = gb.astype(self.dtype)
+            if self.layout == "ref":   # x @ M_ref with M_ref = M_dev^T, W_ref = Wg_dev^T
+                M, gw = np.ascontiguousarray(M.T), np.ascontiguousarray(gw.T)
+            self._dense[l] = (M, gw, gb)
+        return self._dense[l]
+
+    def expert(self, l, e):
+        if (l, e) not in self._experts:
+            d, f = self.d, self.f
+            w1 = self._fill(_tid(4, l, e, 1), _std(d), f * d).reshape(f, d)
+            w3 = self._fill(_tid(4, l, e, 2), _std(d), f * d).reshape(f, d)
+            w2 = self._fill(_tid(4, l, e, 3), _std(f), f * d).reshape(d, f)
+            if self.layout == "ref":
+                w1, w3, w2 = (np.ascontiguousarray(w.T) for w in (w1, w3, w2))
+            self._experts[(l, e)] = (w1, w3, w2)
+        return self._experts[(l, e)]
+
+    def materialize(self, layers=None):
+        for l in (self.layers if layers is None else layers):
+            self.dense(l)
+            for e in range(self.E):
+                self.expert(l, e)
+
+    def forward(self, x: np.ndarray, l: int):
+        """One layer: returns (h_out, selected prob-desc, probs over E, logits)."""
+        M, gw, gb = self.dense(l)
+        x = x.astype(self.dtype)
+        if self.layout == "ref":
+            h = x + self.alpha * (x @ M)
+            z = h @ gw + gb
+        else:
+            h = x + np.float32(self.alpha) * (M @ x)
+            z = gw @ h + gb
+        if not np.isfinite(z).all():
+            raise FloatingPointError("gate logits are not finite")
+        sel = np.lexsort((np.arange(self.E), -z))[: self.K]
+        p = softmax(z)
+        weights = p[sel] / p[sel].sum() if self.renormalize else p[sel]
+        out = h.copy()
+        for e, pe in zip(sel, weights):
+            w1, w3, w2 = self.expert(l, e)
+            if self.layout == "ref":
+                a1, a3 = h @ w1, h @ w3
+                act = a1 / (1.0 + np.exp(-a1)) * a3
+                out = out + pe * (act @ w2)
+            else:
+                a1, a3 = w1 @ h, w3 @ h
+                act = a1 / (np.float32(1.0) + np.exp(-a1)) * a3
+                out = out + pe * (w2 @ act)
+        return out, sel, p, z
+
+    def guess(self, h: np.ndarray, l: int):
+        """Reference-definition guess for layer l from the previous layer's output."""
+        _, gw, gb = self.dense(l)
+        z = h.astype(self.dtype) @ gw + gb if self.layout == "ref" else gw @ h.astype(self.dtype) + gb
+        return np.sort(np.lexsort((np.arange(self.E), -z))[: self.K])
+
+    @staticmethod
+    def inputs(seed: int, T: int, d: int, t0: int = 0) -> np.ndarray:
+        """Token inputs: f32 std 1, tensor kind 5, one tensor per token."""
+        return np.stack([hash_fill(seed, _tid(5, t0 + t), 1.0, d, "f32") for t in range(T)])
+
+    def decode(self, X: np.ndarray):
+        """Run tokens through self.layers; returns (outputs, acts (T, n_layers, K))."""
+        T = X.shape[0]
+        acts = np.zeros((T, len(self.layers), self.K), np.int64)
+        outs = []
+        for t in range(T):
+            h = X[t].astype(self.dtype)
+            for i, l in enumerate(self.layers):
+                h, sel, _, _ = self.forward(h, l)
+                acts[t, i] = np.sort(sel)
+            outs.append(h)
+        return np.stack(outs) if outs else np.zeros((0, self.d)), acts
+
+
+def replay_layers(acts: np.ndarray, E: int, C: int, policy: int, df=1.0, dp=1):
+    """Per-layer replay of a (T, L, K) activation grid with the C oracle."""
+    T, L, K = acts.shape
+    rb = np.zeros((L, T, E), np.uint8)
+    ev = np.zeros((L, T, E), np.uint8)
+    for l in range(L):
+        rb[l], ev[l] = replay_policy(np.ascontiguousarray(acts[:, l, :]), E, C, policy, df, dp)
+    return rb, ev

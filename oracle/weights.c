@@ -1,0 +1,72 @@
+/*
+ * ORACLE -- test infrastructure only (see oracle/__init__.py).
+ *
+ * C restatement of the engine's synthetic-weight definition (DESIGN.md "Synthetic
+ * weights"), written from the spec, not shared with paper_2511_05814_b200/csrc:
+ *   key = sm(seed ^ sm(tensor_id)),  h = sm(key + i)   (sm = splitmix64 finaliser)
+ *   s   = (int)(h >> 40) - 2^23,  v = (float)s * (float)(sqrt(3) * std / 2^23)
+ *   bf16 = round-to-nearest-even(v)
+ * Compile with -ffp-contract=off (a single multiply, but keep the rule explicit).
+ * Multi-threaded fills let the CPU baseline materialise Mixtral-sized experts quickly.
+ */
+#include <stdint.h>
+#include <string.h>
+#include <pthread.h>
+
+static uint64_t sm(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static float scale_of(float std) { return (float)(1.7320508075688772 * (double)std / 8388608.0); }
+
+static inline float value_at(uint64_t key, uint64_t i, float c) {
+  int32_t s = (int32_t)(sm(key + i) >> 40) - (1 << 23);
+  return (float)s * c;
+}
+
+static inline uint16_t to_bf16(float v) {
+  uint32_t u;
+  memcpy(&u, &v, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+typedef struct { uint64_t key; float c; int64_t lo, hi; void* out; int kind; } job_t;
+
+static void* run(void* p) {
+  job_t* j = (job_t*)p;
+  for (int64_t i = j->lo; i < j->hi; ++i) {
+    float v = value_at(j->key, (uint64_t)i, j->c);
+    if (j->kind == 0) ((uint16_t*)j->out)[i] = to_bf16(v);
+    else if (j->kind == 1) ((float*)j->out)[i] = v;
+    else {  /* bf16-rounded, widened to double: the oracle's "identical inputs" */
+      uint32_t u = (uint32_t)to_bf16(v) << 16;
+      float f;
+      memcpy(&f, &u, 4);
+      ((double*)j->out)[i] = (double)f;
+    }
+  }
+  return NULL;
+}
+
+/* kind 0: bf16 bits, 1: f32, 2: bf16 widened to f64 */
+void oracle_hash_fill(uint64_t seed, uint64_t tensor_id, float std, int64_t n, int kind,
+                      void* out, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 64) threads = 64;
+  pthread_t th[64];
+  job_t jobs[64];
+  const uint64_t key = sm(seed ^ sm(tensor_id));
+  const float c = scale_of(std);
+  const int64_t per = (n + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    int64_t lo = t * per, hi = lo + per < n ? lo + per : n;
+    if (lo > hi) lo = hi;
+    jobs[t] = (job_t){key, c, lo, hi, out, kind};
+    pthread_create(&th[t], NULL, run, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+}

@@ -1,0 +1,98 @@
+// Shared plumbing for libmoeb200: status/error reporting, launch accounting, warp helpers.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdarg>
+#include <string>
+#include <atomic>
+
+#include "../../include/moeb200.h"
+
+namespace moe {
+
+// thread-local last error (moe_last_error)
+void set_error(const char* fmt, ...);
+std::atomic<uint64_t>& launch_counter();
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+#define MOE_CUDA(expr)                                                            \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      ::moe::set_error("%s failed at %s:%d: %s", #expr, __FILE__, __LINE__,       \
+                       cudaGetErrorString(_e));                                   \
+      return _e == cudaErrorMemoryAllocation ? MOE_OOM : MOE_CUDA_ERROR;          \
+    }                                                                             \
+  } while (0)
+
+// Check the launch that just happened and count it.
+#define MOE_LAUNCHED()                                                            \
+  do {                                                                            \
+    ::moe::launch_counter().fetch_add(1, std::memory_order_relaxed);              \
+    MOE_CUDA(cudaGetLastError());                                                 \
+  } while (0)
+
+#define MOE_REQUIRE(cond, ...)                                                    \
+  do {                                                                            \
+    if (!(cond)) {                                                                \
+      ::moe::set_error(__VA_ARGS__);                                              \
+      return MOE_INVALID_CONFIG;                                                  \
+    }                                                                             \
+  } while (0)
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t w = __shfl_xor_sync(FULL, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t w = __shfl_xor_sync(FULL, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// Order-preserving map of a finite float/double onto unsigned integers, with -0 == +0
+// (numpy's comparison semantics, which lexsort relies on in toymoe.py:114).
+__device__ __forceinline__ uint32_t ordered_bits(float f) {
+  if (f == 0.0f) f = 0.0f;
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ uint64_t ordered_bits(double f) {
+  if (f == 0.0) f = 0.0;
+  uint64_t u = static_cast<uint64_t>(__double_as_longlong(f));
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+}  // namespace moe

@@ -1,0 +1,743 @@
+// Host runtime of the offload decode engine: weights in pinned host DRAM, a fixed-size
+// per-layer expert cache in HBM, and a transfer thread that forwards the device's load
+// decisions to the copy engine.
+//
+// Per (token t, layer l), on the caller's compute stream:
+//   mix_kernel        h_in -> h' = h_in + alpha * M h_in                 (toymoe.py:140)
+//   gate_cache_kernel gate, softmax, top-k, guess, policy step, buffers  (toymoe.py:99-115,
+//                     178-180; kernels.py:89-145) -> step record + mailbox entry
+//   up/down (phase 0) experts that hit: run while the misses are in flight
+//   cuStreamWaitValue32(ready >= seq + 1)   (released by the copy stream after the misses land)
+//   up/down (phase 1) experts that missed
+// The transfer thread polls the mailbox (mapped pinned memory), issues cudaMemcpyAsync of
+// the missed expert blocks on the copy stream, then cuStreamWriteValue32(ready, seq + 1).
+#include "engine_kernels.cuh"
+#include "hash.cuh"
+
+#include <cuda.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace moe {
+
+moe_status launch_hash_bf16(uint64_t seed, uint64_t tid, float std, long long n, uint16_t* out,
+                            cudaStream_t s);
+moe_status launch_hash_f32(uint64_t seed, uint64_t tid, float std, long long n, float* out,
+                           cudaStream_t s);
+
+// ---- driver entry points (stream memory operations) ------------------------------------
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_waitValue32 p_waitValue32 = nullptr;
+static PFN_writeValue32 p_writeValue32 = nullptr;
+
+static moe_status load_driver_entry_points() {
+  static std::once_flag once;
+  static moe_status st = MOE_OK;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", reinterpret_cast<void**>(&p_waitValue32),
+                                cudaEnableDefault, &q1) != cudaSuccess ||
+        q1 != cudaDriverEntryPointSuccess ||
+        cudaGetDriverEntryPoint("cuStreamWriteValue32",
+                                reinterpret_cast<void**>(&p_writeValue32), cudaEnableDefault,
+                                &q2) != cudaSuccess ||
+        q2 != cudaDriverEntryPointSuccess) {
+      set_error("stream memory operations (cuStreamWaitValue32/WriteValue32) unavailable");
+      st = MOE_CUDA_ERROR;
+    }
+  });
+  return st;
+}
+
+// ---- pinned host store ------------------------------------------------------------------
+// Anonymous mapping with transparent huge pages, first-touched by all host threads in
+// parallel, then page-locked with cudaHostRegister (portable: usable from every context).
+struct PinnedStore {
+  char* base = nullptr;
+  size_t bytes = 0;
+  bool registered = false;
+  bool via_alloc = false;
+
+  moe_status allocate(size_t n) {
+    bytes = n;
+    const char* mode = getenv("MOE_PIN_MODE");
+    if (mode && strcmp(mode, "alloc") == 0) {
+      via_alloc = true;
+      MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&base), n, cudaHostAllocPortable));
+      return MOE_OK;
+    }
+    void* p = mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) {
+      set_error("mmap of %zu bytes for the expert store failed", n);
+      return MOE_OOM;
+    }
+    base = static_cast<char*>(p);
+    madvise(base, n, MADV_HUGEPAGE);
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t per = ((n + hw - 1) / hw + 4095) & ~size_t(4095);
+    std::vector<std::thread> th;
+    for (unsigned i = 0; i < hw; ++i)
+      th.emplace_back([this, i, per] {
+        const size_t lo = i * per, hi = std::min(bytes, lo + per);
+        for (size_t o = lo; o < hi; o += 4096) base[o] = 0;
+      });
+    for (auto& x : th) x.join();
+    MOE_CUDA(cudaHostRegister(base, n, cudaHostRegisterPortable));
+    registered = true;
+    return MOE_OK;
+  }
+  void release() {
+    if (!base) return;
+    if (via_alloc) {
+      cudaFreeHost(base);
+    } else {
+      if (registered) cudaHostUnregister(base);
+      munmap(base, bytes);
+    }
+    base = nullptr;
+  }
+};
+
+struct PrefetchJob {
+  int layer, buf, expert;
+  long long next_chunk, n_chunks;
+  bool cancelled, adopted;
+};
+
+}  // namespace moe
+
+using namespace moe;
+
+struct moe_engine {
+  moe_engine_config cfg{};
+  int d = 0, dpad = 0, f = 0, NB = 0, S = 0;
+  bool bf16 = false;
+  long long expert_bytes = 0;
+  int device = 0;
+
+  // device memory
+  char* pool = nullptr;          // [L][NB][expert_bytes]
+  void* mixing = nullptr;        // [L][dpad][dpad] (bf16 or f32), device layout
+  float* gate_w = nullptr;       // [L][E][dpad]
+  float* gate_b = nullptr;       // [L][E]
+  LayerState* states = nullptr;  // [L]
+  StepRecord* ring = nullptr;    // [max_tokens][L]
+  float *h_in = nullptr, *h_mid = nullptr, *y = nullptr, *act = nullptr;
+  float *x_pad = nullptr, *out_pad = nullptr;  // padded token staging when d % 8 != 0
+  unsigned int* ready_ctr = nullptr;
+  int* err = nullptr;
+  DeviceStats* dstats = nullptr;
+
+  // mapped pinned memory shared with the device
+  MailRecord* mail_h = nullptr;
+  MailRecord* mail_d = nullptr;
+  volatile long long* consumed_h = nullptr;
+  long long* consumed_d = nullptr;
+  volatile unsigned int* chunk_done_h = nullptr;
+  CUdeviceptr chunk_done_d = 0;
+
+  PinnedStore store;
+  cudaStream_t copy_stream = nullptr;
+
+  // transfer thread
+  std::thread worker;
+  std::atomic<bool> stop{false};
+  std::atomic<long long> next_mail{0};  // first mail seq not yet processed
+  long long tokens_done = 0;            // absolute tokens enqueued
+  std::deque<PrefetchJob> jobs;
+  unsigned int chunks_issued = 0;
+  std::mutex stats_mu;
+  moe_stats st{};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_events;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> free_events;
+  std::atomic<int> worker_error{0};
+  std::string worker_msg;
+};
+
+namespace {
+
+moe_status issue_copy(moe_engine* g, int layer, int buf, int expert, long long off, long long n) {
+  char* dst = g->pool + (static_cast<long long>(layer) * g->NB + buf) * g->expert_bytes + off;
+  const char* src =
+      g->store.base + (static_cast<long long>(layer) * g->cfg.num_experts + expert) * g->expert_bytes + off;
+  MOE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, g->copy_stream));
+  return MOE_OK;
+}
+
+std::pair<cudaEvent_t, cudaEvent_t> take_events(moe_engine* g) {
+  std::lock_guard<std::mutex> lk(g->stats_mu);
+  if (!g->free_events.empty()) {
+    auto e = g->free_events.back();
+    g->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  return {a, b};
+}
+
+// Process one mailbox entry: cancels, new prefetches, demand copies, release.
+moe_status handle_mail(moe_engine* g, const MailRecord& m) {
+  const long long chunk = g->cfg.chunk_bytes;
+  const long long nchunks = (g->expert_bytes + chunk - 1) / chunk;
+  // cancelled staging buffers of this step's layer: stop their remaining chunks
+  for (int i = 0; i < m.n_cancel; ++i)
+    for (auto& j : g->jobs)
+      if (!j.cancelled && !j.adopted && j.layer == m.layer && j.buf == m.cancel_buf[i]) {
+        j.cancelled = true;
+        std::lock_guard<std::mutex> lk(g->stats_mu);
+        g->st.prefetch_wasted_bytes += std::min(j.next_chunk * chunk, g->expert_bytes);
+      }
+  long long demand = 0;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (m.n_demand > 0) {
+    ev = take_events(g);
+    MOE_CUDA(cudaEventRecord(ev.first, g->copy_stream));
+  }
+  for (int i = 0; i < m.n_demand; ++i) {
+    const int e = m.demand_expert[i], b = m.demand_buf[i];
+    long long from = 0;
+    if (m.demand_adopt[i]) {
+      for (auto& j : g->jobs)
+        if (!j.cancelled && !j.adopted && j.layer == m.layer && j.buf == b && j.expert == e) {
+          j.adopted = true;
+          from = j.next_chunk;
+          break;
+        }
+      std::lock_guard<std::mutex> lk(g->stats_mu);
+      g->st.prefetch_used += 1;
+    }
+    for (long long c = from; c < nchunks; ++c) {
+      const long long off = c * chunk, n = std::min(chunk, g->expert_bytes - off);
+      moe_status s = issue_copy(g, m.layer, b, e, off, n);
+      if (s != MOE_OK) return s;
+      demand += n;
+    }
+  }
+  if (m.n_demand > 0) MOE_CUDA(cudaEventRecord(ev.second, g->copy_stream));
+  if (m.n_demand > 0 || m.need_ack) {
+    if (p_writeValue32(reinterpret_cast<CUstream>(g->copy_stream),
+                       reinterpret_cast<CUdeviceptr>(g->ready_ctr),
+                       static_cast<cuuint32_t>(m.seq + 1), 0) != CUDA_SUCCESS) {
+      set_error("cuStreamWriteValue32 failed");
+      return MOE_CUDA_ERROR;
+    }
+  }
+  // new prefetches for layer + 1 (issued chunk by chunk from the idle loop)
+  for (int i = 0; i < m.n_prefetch; ++i) {
+    g->jobs.push_back(PrefetchJob{m.layer + 1, m.prefetch_buf[i], m.prefetch_expert[i], 0,
+                                  nchunks, false, false});
+  }
+  std::lock_guard<std::mutex> lk(g->stats_mu);
+  g->st.demand_bytes += demand;
+  g->st.h2d_bytes += demand;
+  g->st.prefetch_issued += m.n_prefetch;
+  if (m.n_demand > 0) g->busy_events.push_back(ev);
+  return MOE_OK;
+}
+
+// Issue one chunk of the oldest live prefetch job if the in-flight budget allows.
+moe_status pump_prefetch(moe_engine* g, bool* did) {
+  *did = false;
+  while (!g->jobs.empty() &&
+         (g->jobs.front().cancelled || g->jobs.front().adopted ||
+          g->jobs.front().next_chunk >= g->jobs.front().n_chunks))
+    g->jobs.pop_front();
+  if (g->jobs.empty()) return MOE_OK;
+  const unsigned int done = *g->chunk_done_h;
+  if (g->chunks_issued - done >= static_cast<unsigned int>(g->cfg.prefetch_depth)) return MOE_OK;
+  PrefetchJob& j = g->jobs.front();
+  const long long chunk = g->cfg.chunk_bytes;
+  const long long off = j.next_chunk * chunk, n = std::min(chunk, g->expert_bytes - off);
+  moe_status s = issue_copy(g, j.layer, j.buf, j.expert, off, n);
+  if (s != MOE_OK) return s;
+  j.next_chunk += 1;
+  g->chunks_issued += 1;
+  if (p_writeValue32(reinterpret_cast<CUstream>(g->copy_stream), g->chunk_done_d,
+                     g->chunks_issued, 0) != CUDA_SUCCESS) {
+    set_error("cuStreamWriteValue32 failed");
+    return MOE_CUDA_ERROR;
+  }
+  std::lock_guard<std::mutex> lk(g->stats_mu);
+  g->st.prefetch_bytes += n;
+  g->st.h2d_bytes += n;
+  *did = true;
+  return MOE_OK;
+}
+
+void worker_main(moe_engine* g) {
+  cudaSetDevice(g->device);
+  long long idle = 0;
+  while (!g->stop.load(std::memory_order_relaxed)) {
+    const long long seq = g->next_mail.load(std::memory_order_relaxed);
+    MailRecord& m = g->mail_h[seq % kMailRing];
+    if (m.ready == seq + 1) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      MailRecord copy;
+      memcpy(&copy, const_cast<MailRecord*>(&m), sizeof(MailRecord));
+      moe_status s = handle_mail(g, copy);
+      if (s != MOE_OK) {
+        g->worker_msg = moe_last_error();
+        g->worker_error.store(s);
+        return;
+      }
+      g->next_mail.store(seq + 1, std::memory_order_release);
+      *g->consumed_h = seq + 1;
+      idle = 0;
+      continue;
+    }
+    bool did = false;
+    moe_status s = pump_prefetch(g, &did);
+    if (s != MOE_OK) {
+      g->worker_msg = moe_last_error();
+      g->worker_error.store(s);
+      return;
+    }
+    if (did) continue;
+    if (++idle > 200000) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+moe_status alloc_device(void** p, size_t n) {
+  MOE_CUDA(cudaMalloc(p, n));
+  MOE_CUDA(cudaMemset(*p, 0, n));
+  return MOE_OK;
+}
+
+#define TRY(x)                     \
+  do {                             \
+    moe_status _s = (x);           \
+    if (_s != MOE_OK) return _s;   \
+  } while (0)
+
+int round8(int x) { return (x + 7) / 8 * 8; }
+
+}  // namespace
+
+extern "C" {
+
+moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) {
+  MOE_REQUIRE(cfg_in && out, "null argument");
+  const moe_engine_config& c = *cfg_in;
+  MOE_REQUIRE(c.num_layers >= 1, "num_layers must be >= 1, got %d", c.num_layers);
+  MOE_REQUIRE(c.num_experts >= 1 && c.num_experts <= kMaxE,
+              "the live engine supports 1..%d experts per layer, got %d", kMaxE, c.num_experts);
+  MOE_REQUIRE(c.top_k >= 1 && c.top_k <= c.num_experts && c.top_k <= kMaxK,
+              "top_k must be in [1, min(E, %d)], got %d", kMaxK, c.top_k);
+  MOE_REQUIRE(c.cache_size >= c.top_k,
+              "top_k=%d experts per step cannot fit in cache_size=%d", c.top_k, c.cache_size);
+  MOE_REQUIRE(c.hidden_dim >= 1, "hidden_dim must be >= 1, got %d", c.hidden_dim);
+  MOE_REQUIRE(c.expert_kind == MOE_EXPERT_TOY_TANH_F32 || c.expert_kind == MOE_EXPERT_SWIGLU_BF16,
+              "unknown expert kind %d", c.expert_kind);
+  MOE_REQUIRE(c.policy == MOE_P_LRU || c.policy == MOE_P_LFU || c.policy == MOE_P_LFU_AGED,
+              "the live engine runs lru/lfu/lfu-aged; opt needs the future and is offline-only");
+  MOE_REQUIRE(c.policy != MOE_P_LFU_AGED || (c.decay_period >= 1 && c.decay_factor > 0.0 &&
+                                              c.decay_factor <= 1.0),
+              "bad lfu-aged parameters");
+  MOE_REQUIRE(c.mixing_scale >= 0.f, "mixing_scale must be >= 0");
+  MOE_REQUIRE(c.prefetch == MOE_PREFETCH_OFF || c.prefetch == MOE_PREFETCH_EARLY,
+              "unknown prefetch mode %d", c.prefetch);
+  MOE_REQUIRE(c.max_tokens >= 1, "max_tokens must be >= 1");
+  TRY(load_driver_entry_points());
+
+  auto* g = new moe_engine();
+  g->cfg = c;
+  if (g->cfg.chunk_bytes <= 0) g->cfg.chunk_bytes = 16ll << 20;
+  if (g->cfg.prefetch_depth <= 0) g->cfg.prefetch_depth = 2;
+  g->device = c.device;
+  g->d = c.hidden_dim;
+  g->bf16 = c.expert_kind == MOE_EXPERT_SWIGLU_BF16;
+  if (g->bf16) {
+    MOE_REQUIRE(c.hidden_dim % 8 == 0 && c.ffn_dim >= 8 && c.ffn_dim % 8 == 0,
+                "SwiGLU experts need hidden_dim and ffn_dim multiples of 8");
+    g->dpad = c.hidden_dim;
+    g->f = c.ffn_dim;
+    g->expert_bytes = 3ll * g->f * g->dpad * 2;
+  } else {
+    g->dpad = round8(c.hidden_dim);
+    g->f = g->dpad;
+    g->expert_bytes = 2ll * g->dpad * g->dpad * 4;
+  }
+  g->S = c.prefetch ? c.top_k : 0;
+  g->NB = c.cache_size + g->S;
+  MOE_REQUIRE(g->NB <= kMaxBuf, "cache_size + staging buffers must be <= %d", kMaxBuf);
+  const int L = c.num_layers, E = c.num_experts, K = c.top_k, D = g->dpad;
+  MOE_CUDA(cudaSetDevice(g->device));
+
+  const size_t msz = g->bf16 ? 2 : 4;
+  TRY(alloc_device(reinterpret_cast<void**>(&g->pool), static_cast<size_t>(L) * g->NB * g->expert_bytes));
+  TRY(alloc_device(&g->mixing, static_cast<size_t>(L) * D * D * msz));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->gate_w), sizeof(float) * L * E * D));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->gate_b), sizeof(float) * L * E));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->states), sizeof(LayerState) * L));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->ring), sizeof(StepRecord) * L * static_cast<size_t>(c.max_tokens)));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->h_in), sizeof(float) * D));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->h_mid), sizeof(float) * 2 * D));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->y), sizeof(float) * K * D));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->act), sizeof(float) * K * g->f));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->ready_ctr), sizeof(unsigned int)));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->err), sizeof(int)));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->dstats), sizeof(DeviceStats)));
+  if (D != g->d) {
+    TRY(alloc_device(reinterpret_cast<void**>(&g->x_pad), sizeof(float) * D));
+    TRY(alloc_device(reinterpret_cast<void**>(&g->out_pad), sizeof(float) * D));
+  }
+  MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->mail_h), sizeof(MailRecord) * kMailRing,
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(g->mail_h, 0, sizeof(MailRecord) * kMailRing);
+  MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g->mail_d), g->mail_h, 0));
+  long long* consumed = nullptr;
+  MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&consumed), sizeof(long long),
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  *consumed = 0;
+  g->consumed_h = consumed;
+  MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g->consumed_d), consumed, 0));
+  unsigned int* cd = nullptr;
+  MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cd), sizeof(unsigned int),
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  *cd = 0;
+  g->chunk_done_h = cd;
+  void* cdd = nullptr;
+  MOE_CUDA(cudaHostGetDevicePointer(&cdd, cd, 0));
+  g->chunk_done_d = reinterpret_cast<CUdeviceptr>(cdd);
+  MOE_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+
+  TRY(g->store.allocate(static_cast<size_t>(L) * E * g->expert_bytes));
+  reset_states_kernel<<<L, 64>>>(g->states, L, g->NB);
+  MOE_LAUNCHED();
+  MOE_CUDA(cudaDeviceSynchronize());
+  g->st.expert_bytes = g->expert_bytes;
+  g->worker = std::thread(worker_main, g);
+  *out = g;
+  return MOE_OK;
+}
+
+moe_status moe_engine_destroy(moe_engine* g) {
+  if (!g) return MOE_OK;
+  cudaSetDevice(g->device);
+  cudaDeviceSynchronize();
+  g->stop.store(true);
+  if (g->worker.joinable()) g->worker.join();
+  cudaStreamSynchronize(g->copy_stream);
+  for (auto& e : g->busy_events) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  for (auto& e : g->free_events) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  void* dev[] = {g->pool, g->mixing, g->gate_w, g->gate_b, g->states, g->ring, g->h_in,
+                 g->h_mid, g->y, g->act, g->ready_ctr, g->err, g->dstats, g->x_pad, g->out_pad};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (g->mail_h) cudaFreeHost(g->mail_h);
+  if (g->consumed_h) cudaFreeHost(const_cast<long long*>(g->consumed_h));
+  if (g->chunk_done_h) cudaFreeHost(const_cast<unsigned int*>(g->chunk_done_h));
+  if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
+  g->store.release();
+  delete g;
+  return MOE_OK;
+}
+
+moe_status moe_engine_set_dense_f32(moe_engine* g, int32_t layer, const float* mixing,
+                                    const float* gate_w, const float* gate_b) {
+  MOE_REQUIRE(g && layer >= 0 && layer < g->cfg.num_layers, "layer %d out of range", layer);
+  MOE_REQUIRE(!g->bf16, "set_dense_f32 is for the f32 (toy) engine");
+  MOE_CUDA(cudaSetDevice(g->device));
+  const int d = g->d, D = g->dpad, E = g->cfg.num_experts;
+  // device layout: M_dev[j][i] = M_ref[i][j]; W_dev[e][i] = W_ref[i][e]; zero padding
+  std::vector<float> mt(static_cast<size_t>(D) * D, 0.f), gw(static_cast<size_t>(E) * D, 0.f);
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) mt[static_cast<size_t>(j) * D + i] = mixing[static_cast<size_t>(i) * d + j];
+  for (int i = 0; i < d; ++i)
+    for (int e = 0; e < E; ++e) gw[static_cast<size_t>(e) * D + i] = gate_w[static_cast<size_t>(i) * E + e];
+  MOE_CUDA(cudaMemcpy(static_cast<float*>(g->mixing) + static_cast<size_t>(layer) * D * D, mt.data(),
+                      sizeof(float) * mt.size(), cudaMemcpyHostToDevice));
+  MOE_CUDA(cudaMemcpy(g->gate_w + static_cast<size_t>(layer) * E * D, gw.data(),
+                      sizeof(float) * gw.size(), cudaMemcpyHostToDevice));
+  std::vector<float> gb(E, 0.f);
+  if (gate_b)
+    for (int e = 0; e < E; ++e) gb[e] = gate_b[e];
+  MOE_CUDA(cudaMemcpy(g->gate_b + static_cast<size_t>(layer) * E, gb.data(), sizeof(float) * E,
+                      cudaMemcpyHostToDevice));
+  return MOE_OK;
+}
+
+moe_status moe_engine_set_toy_expert_f32(moe_engine* g, int32_t layer, int32_t expert,
+                                         const float* w1, const float* w2) {
+  MOE_REQUIRE(g && layer >= 0 && layer < g->cfg.num_layers, "layer %d out of range", layer);
+  MOE_REQUIRE(expert >= 0 && expert < g->cfg.num_experts, "expert %d out of range", expert);
+  MOE_REQUIRE(!g->bf16, "set_toy_expert_f32 is for the toy engine");
+  const int d = g->d, D = g->dpad;
+  float* blk = reinterpret_cast<float*>(
+      g->store.base + (static_cast<long long>(layer) * g->cfg.num_experts + expert) * g->expert_bytes);
+  memset(blk, 0, g->expert_bytes);
+  float* w1t = blk;
+  float* w2t = blk + static_cast<size_t>(D) * D;
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) {
+      w1t[static_cast<size_t>(j) * D + i] = w1[static_cast<size_t>(i) * d + j];
+      w2t[static_cast<size_t>(j) * D + i] = w2[static_cast<size_t>(i) * d + j];
+    }
+  return MOE_OK;
+}
+
+moe_status moe_engine_init_random(moe_engine* g, uint64_t seed) {
+  MOE_REQUIRE(g, "null engine");
+  MOE_REQUIRE(g->bf16, "init_random synthesises Mixtral-shaped (SwiGLU bf16) weights");
+  MOE_CUDA(cudaSetDevice(g->device));
+  const int L = g->cfg.num_layers, E = g->cfg.num_experts, d = g->d, f = g->f;
+  cudaStream_t s = g->copy_stream;
+  // std = float(1 / sqrt(n)) rounded once from double (the oracle uses the same rule)
+  const float sd = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+  const float sf = static_cast<float>(1.0 / std::sqrt(static_cast<double>(f)));
+  for (int l = 0; l < L; ++l) {
+    uint16_t* M = static_cast<uint16_t*>(g->mixing) + static_cast<size_t>(l) * d * d;
+    TRY(launch_hash_bf16(seed, tensor_id(kTMixing, l, 0, 0), 1.f, 1ll * d * d, M, s));
+    TRY(launch_hash_f32(seed, tensor_id(kTGateW, l, 0, 0), sd, 1ll * E * d,
+                        g->gate_w + static_cast<size_t>(l) * E * d, s));
+    TRY(launch_hash_f32(seed, tensor_id(kTGateB, l, 0, 0), 1.f, E,
+                        g->gate_b + static_cast<size_t>(l) * E, s));
+  }
+  // experts: generate into a free HBM buffer, then copy down into the pinned store
+  uint16_t* scratch = reinterpret_cast<uint16_t*>(g->pool);
+  const long long fd = 1ll * f * d;
+  for (int l = 0; l < L; ++l)
+    for (int e = 0; e < E; ++e) {
+      TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW1), sd, fd, scratch, s));
+      TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW3), sd, fd, scratch + fd, s));
+      TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW2), sf, fd, scratch + 2 * fd, s));
+      MOE_CUDA(cudaMemcpyAsync(g->store.base + (static_cast<long long>(l) * E + e) * g->expert_bytes,
+                               scratch, g->expert_bytes, cudaMemcpyDeviceToHost, s));
+    }
+  MOE_CUDA(cudaStreamSynchronize(s));
+  return MOE_OK;
+}
+
+moe_status moe_engine_expert_host_ptr(moe_engine* g, int32_t layer, int32_t expert, void** ptr,
+                                      int64_t* bytes) {
+  MOE_REQUIRE(g && layer >= 0 && layer < g->cfg.num_layers && expert >= 0 &&
+                  expert < g->cfg.num_experts,
+              "expert (%d, %d) out of range", layer, expert);
+  *ptr = g->store.base + (static_cast<long long>(layer) * g->cfg.num_experts + expert) * g->expert_bytes;
+  *bytes = g->expert_bytes;
+  return MOE_OK;
+}
+
+moe_status moe_engine_dense_host(moe_engine* g, int32_t layer, void* mixing, float* gate_w,
+                                 float* gate_b) {
+  MOE_REQUIRE(g && layer >= 0 && layer < g->cfg.num_layers, "layer %d out of range", layer);
+  MOE_CUDA(cudaSetDevice(g->device));
+  const int D = g->dpad, E = g->cfg.num_experts;
+  const size_t msz = g->bf16 ? 2 : 4;
+  if (mixing)
+    MOE_CUDA(cudaMemcpy(mixing, static_cast<char*>(g->mixing) + static_cast<size_t>(layer) * D * D * msz,
+                        static_cast<size_t>(D) * D * msz, cudaMemcpyDeviceToHost));
+  if (gate_w)
+    MOE_CUDA(cudaMemcpy(gate_w, g->gate_w + static_cast<size_t>(layer) * E * D,
+                        sizeof(float) * E * D, cudaMemcpyDeviceToHost));
+  if (gate_b)
+    MOE_CUDA(cudaMemcpy(gate_b, g->gate_b + static_cast<size_t>(layer) * E, sizeof(float) * E,
+                        cudaMemcpyDeviceToHost));
+  return MOE_OK;
+}
+
+moe_status moe_engine_reset(moe_engine* g) {
+  MOE_REQUIRE(g, "null engine");
+  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_CUDA(cudaDeviceSynchronize());
+  MOE_CUDA(cudaStreamSynchronize(g->copy_stream));
+  reset_states_kernel<<<g->cfg.num_layers, 64>>>(g->states, g->cfg.num_layers, g->NB);
+  MOE_LAUNCHED();
+  MOE_CUDA(cudaMemset(g->err, 0, sizeof(int)));
+  MOE_CUDA(cudaDeviceSynchronize());
+  return MOE_OK;
+}
+
+moe_status moe_engine_decode(moe_engine* g, const float* h_in_dev, int64_t T, float* h_out_dev,
+                             void* stream) {
+  MOE_REQUIRE(g, "null engine");
+  MOE_REQUIRE(T >= 0, "negative token count");
+  if (g->worker_error.load()) {
+    set_error("transfer thread failed: %s", g->worker_msg.c_str());
+    return MOE_CUDA_ERROR;
+  }
+  MOE_CUDA(cudaSetDevice(g->device));
+  cudaStream_t s = as_stream(stream);
+  const moe_engine_config& c = g->cfg;
+  const int L = c.num_layers, K = c.top_k, D = g->dpad, d = g->d;
+  const size_t msz = g->bf16 ? 2 : 4;
+  const int mix_grid = std::max(1, std::min(D / 8, 148 * 2));
+  const size_t mix_smem = static_cast<size_t>(D) * 8;
+  const int up_rows = g->bf16 ? g->f : D;
+  const int up_grid = std::max(1, std::min(up_rows / 8, 148 * 2));
+  const int down_grid = std::max(1, std::min(D / 8, 148));
+  const size_t up_smem = static_cast<size_t>(D) * 4;
+  const size_t down_smem = static_cast<size_t>(g->f) * 4;
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(mix_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mix_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(swiglu_up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(toy_up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(down_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(down_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attrs = true;
+  }
+  MOE_REQUIRE(mix_smem <= 200 * 1024 && down_smem <= 200 * 1024, "hidden/ffn dims too large");
+  for (int64_t t = 0; t < T; ++t) {
+    const long long tok = g->tokens_done + t;
+    StepRecord* trec = g->ring + (tok % c.max_tokens) * L;
+    const float* x = h_in_dev + t * d;
+    if (D != d) {
+      MOE_CUDA(cudaMemcpyAsync(g->x_pad, x, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+      x = g->x_pad;
+    }
+    for (int l = 0; l < L; ++l) {
+      const long long seq = tok * L + l;
+      float* hm = g->h_mid + (l & 1) * D;
+      const float* hm_prev = g->h_mid + ((l + 1) & 1) * D;
+      MixParams mp{l == 0 ? x : nullptr, hm_prev, g->y, l == 0 ? nullptr : trec + (l - 1),
+                   static_cast<char*>(g->mixing) + static_cast<size_t>(l) * D * D * msz,
+                   c.mixing_scale, D, K, g->h_in, hm};
+      if (g->bf16)
+        mix_kernel<true><<<mix_grid, 256, mix_smem, s>>>(mp);
+      else
+        mix_kernel<false><<<mix_grid, 256, mix_smem, s>>>(mp);
+      MOE_LAUNCHED();
+      GateParams gp{hm, g->h_in, g->gate_w, g->gate_b, l, L, c.num_experts, K, D, c.cache_size,
+                    g->NB, c.policy, c.decay_factor, c.decay_period, c.record_speculation,
+                    c.prefetch, c.renormalize, seq, g->states, trec + l, g->mail_d,
+                    g->consumed_d, g->ready_ctr, g->err, g->dstats};
+      gate_cache_kernel<<<1, 256, 0, s>>>(gp);
+      MOE_LAUNCHED();
+      FfnParams fp{hm, trec + l, g->states + l,
+                   g->pool + static_cast<long long>(l) * g->NB * g->expert_bytes, g->expert_bytes,
+                   D, g->f, K, 0, g->act, g->y};
+      for (int phase = 0; phase < 2; ++phase) {
+        if (phase == 1) {
+          if (p_waitValue32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(g->ready_ctr),
+                            static_cast<cuuint32_t>(seq + 1), CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+            set_error("cuStreamWaitValue32 failed");
+            return MOE_CUDA_ERROR;
+          }
+        }
+        fp.phase = phase;
+        if (g->bf16) {
+          swiglu_up_kernel<<<dim3(up_grid, K), 256, up_smem, s>>>(fp);
+          MOE_LAUNCHED();
+          down_kernel<true><<<dim3(down_grid, K), 256, down_smem, s>>>(fp);
+          MOE_LAUNCHED();
+        } else {
+          toy_up_kernel<<<dim3(up_grid, K), 256, up_smem, s>>>(fp);
+          MOE_LAUNCHED();
+          down_kernel<false><<<dim3(down_grid, K), 256, down_smem, s>>>(fp);
+          MOE_LAUNCHED();
+        }
+      }
+    }
+    float* out = h_out_dev + t * d;
+    float* dst = D != d ? g->out_pad : out;
+    finalize_kernel<<<(D + 255) / 256, 256, 0, s>>>(g->h_mid + ((L - 1) & 1) * D, g->y,
+                                                   trec + (L - 1), K, D, dst);
+    MOE_LAUNCHED();
+    if (D != d)
+      MOE_CUDA(cudaMemcpyAsync(out, g->out_pad, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+  }
+  g->tokens_done += T;
+  return MOE_OK;
+}
+
+moe_status moe_engine_sync(moe_engine* g) {
+  MOE_REQUIRE(g, "null engine");
+  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_CUDA(cudaDeviceSynchronize());
+  if (g->worker_error.load()) {
+    set_error("transfer thread failed: %s", g->worker_msg.c_str());
+    return MOE_CUDA_ERROR;
+  }
+  int h = 0;
+  MOE_CUDA(cudaMemcpy(&h, g->err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h) {
+    MOE_CUDA(cudaMemset(g->err, 0, sizeof(int)));
+    if (h & 1) {
+      set_error("gate logits are not finite");
+      return MOE_NONFINITE;
+    }
+    set_error("cache policy found no eviction candidate");
+    return MOE_INVALID_CONFIG;
+  }
+  return MOE_OK;
+}
+
+moe_status moe_engine_records(moe_engine* g, int64_t t0, int64_t T, int64_t* acts,
+                              int64_t* guessed, uint8_t* resident_before, uint8_t* evicted,
+                              float* probs) {
+  MOE_REQUIRE(g, "null engine");
+  const moe_engine_config& c = g->cfg;
+  MOE_REQUIRE(t0 >= 0 && T >= 0 && t0 + T <= g->tokens_done, "tokens [%lld, %lld) not decoded",
+              (long long)t0, (long long)(t0 + T));
+  MOE_REQUIRE(g->tokens_done - t0 <= c.max_tokens, "tokens [%lld, ...) left the record ring",
+              (long long)t0);
+  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_CUDA(cudaDeviceSynchronize());
+  const int L = c.num_layers, K = c.top_k, E = c.num_experts;
+  std::vector<StepRecord> buf(static_cast<size_t>(L));
+  for (int64_t t = 0; t < T; ++t) {
+    const long long tok = t0 + t;
+    MOE_CUDA(cudaMemcpy(buf.data(), g->ring + (tok % c.max_tokens) * L, sizeof(StepRecord) * L,
+                        cudaMemcpyDeviceToHost));
+    for (int l = 0; l < L; ++l) {
+      const StepRecord& r = buf[l];
+      for (int j = 0; j < K; ++j) {
+        if (acts) acts[(t * L + l) * K + j] = r.acts[j];
+        if (probs) probs[(t * L + l) * K + j] = r.prob[j];
+        if (guessed && l >= 1) guessed[(t * (L - 1) + (l - 1)) * K + j] = r.guess[j];
+      }
+      for (int e = 0; e < E; ++e) {
+        if (resident_before) resident_before[(t * L + l) * E + e] = (r.rb >> e) & 1u;
+        if (evicted) evicted[(t * L + l) * E + e] = (r.ev >> e) & 1u;
+      }
+    }
+  }
+  return MOE_OK;
+}
+
+moe_status moe_engine_stats(moe_engine* g, moe_stats* out) {
+  MOE_REQUIRE(g && out, "null argument");
+  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_CUDA(cudaDeviceSynchronize());
+  MOE_CUDA(cudaStreamSynchronize(g->copy_stream));
+  DeviceStats ds{};
+  MOE_CUDA(cudaMemcpy(&ds, g->dstats, sizeof(ds), cudaMemcpyDeviceToHost));
+  std::lock_guard<std::mutex> lk(g->stats_mu);
+  for (auto& e : g->busy_events) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, e.first, e.second) == cudaSuccess) g->st.copy_busy_ms += ms;
+    g->free_events.push_back(e);
+  }
+  g->busy_events.clear();
+  *out = g->st;
+  out->hits = static_cast<int64_t>(ds.hits);
+  out->misses = static_cast<int64_t>(ds.misses);
+  out->tokens = g->tokens_done;
+  out->steps = g->tokens_done * g->cfg.num_layers;
+  out->expert_bytes = g->expert_bytes;
+  return MOE_OK;
+}
+
+}  // extern "C"

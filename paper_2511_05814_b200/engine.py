@@ -1,0 +1,268 @@
+"""OffloadEngine: the MoE-offloading decode engine behind the C ABI (include/moeb200.h).
+
+Experts live in pinned host DRAM; each layer owns a fixed-size HBM expert cache managed
+by a device-resident policy (LRU / LFU / LFU-aged, the reference's semantics); misses are
+streamed over PCIe by the copy engine.  Host code here only builds configs, moves weights
+in, and reads step records / statistics back.
+
+Typical use (Mixtral-8x7B shape, synthetic weights):
+
+    cfg = EngineConfig.mixtral_8x7b(cache_size=4, policy=PolicyKind.lfu())
+    with OffloadEngine(cfg) as eng:
+        eng.init_random(seed=42)
+        h_out = eng.decode(h_in)            # (T, d) float32, host or CUDA
+        log = eng.event_log(0, T)           # CacheEventLog (simulate.py format)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError
+from .policies import OPT, PolicyKind
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    num_layers: int
+    num_experts: int
+    top_k: int
+    hidden_dim: int
+    ffn_dim: int = 0
+    expert_kind: str = "swiglu"          # "swiglu" (bf16) | "toy_tanh" (f32)
+    cache_size: int = 4
+    policy: PolicyKind = field(default_factory=PolicyKind.lru)
+    mixing_scale: float = 0.1
+    prefetch: str = "off"                # "off" | "early" (gate_{l+1} on h'_l)
+    renormalize: bool = False            # Mixtral routing (renormalised top-k); ref: False
+    record_speculation: bool = True
+    max_tokens: int = 4096
+    chunk_bytes: int = 16 << 20
+    prefetch_depth: int = 2
+    device: int = 0
+
+    @staticmethod
+    def mixtral_8x7b(**kw) -> "EngineConfig":
+        """Mixtral-8x7B shape (L=32, E=8, K=2, d=4096, f=14336), alpha = 0.1*sqrt(16/d)."""
+        base = dict(num_layers=32, num_experts=8, top_k=2, hidden_dim=4096, ffn_dim=14336,
+                    expert_kind="swiglu", mixing_scale=0.1 * math.sqrt(16 / 4096))
+        base.update(kw)
+        return EngineConfig(**base)
+
+    @staticmethod
+    def mixtral_8x22b(**kw) -> "EngineConfig":
+        """Mixtral-8x22B shape (L=56, E=8, K=2, d=6144, f=16384)."""
+        base = dict(num_layers=56, num_experts=8, top_k=2, hidden_dim=6144, ffn_dim=16384,
+                    expert_kind="swiglu", mixing_scale=0.1 * math.sqrt(16 / 6144))
+        base.update(kw)
+        return EngineConfig(**base)
+
+    @property
+    def expert_bytes(self) -> int:
+        if self.expert_kind == "swiglu":
+            return 3 * self.ffn_dim * self.hidden_dim * 2
+        d8 = (self.hidden_dim + 7) // 8 * 8
+        return 2 * d8 * d8 * 4
+
+    def to_c(self) -> _native.EngineConfigC:
+        if self.policy.name == OPT:
+            raise ConfigError("the live engine cannot run opt (it needs the future stream)")
+        kinds = {"toy_tanh": _native.EXPERT_TOY_TANH_F32, "swiglu": _native.EXPERT_SWIGLU_BF16}
+        if self.expert_kind not in kinds:
+            raise ConfigError(f"unknown expert kind {self.expert_kind!r}")
+        modes = {"off": _native.PREFETCH_OFF, "early": _native.PREFETCH_EARLY}
+        if self.prefetch not in modes:
+            raise ConfigError(f"unknown prefetch mode {self.prefetch!r}")
+        code, df, dp = self.policy.device_params()
+        return _native.EngineConfigC(
+            num_layers=self.num_layers, num_experts=self.num_experts, top_k=self.top_k,
+            hidden_dim=self.hidden_dim, ffn_dim=self.ffn_dim, expert_kind=kinds[self.expert_kind],
+            cache_size=self.cache_size, policy=code, decay_factor=df, decay_period=dp,
+            mixing_scale=self.mixing_scale, prefetch=modes[self.prefetch],
+            renormalize=int(self.renormalize), record_speculation=int(self.record_speculation),
+            max_tokens=self.max_tokens, chunk_bytes=self.chunk_bytes,
+            prefetch_depth=self.prefetch_depth, device=self.device)
+
+
+class OffloadEngine:
+    """Owns one libmoeb200 engine (one per GPU, driven by one host thread)."""
+
+    def __init__(self, config: EngineConfig):
+        import torch
+
+        self.config = config
+        self._lib = _native.lib()
+        self._dev = torch.device("cuda", config.device)
+        c = config.to_c()
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self._dev):
+            _native.check(self._lib.moe_engine_create(ctypes.byref(c), ctypes.byref(handle)))
+        self._h = handle
+        self.tokens_done = 0
+
+    # -- lifetime --
+    def close(self) -> None:
+        if self._h:
+            _native.check(self._lib.moe_engine_destroy(self._h))
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- weights --
+    def init_random(self, seed: int = 42) -> None:
+        """Synthetic Mixtral-shaped bf16 weights from the counter hash."""
+        _native.check(self._lib.moe_engine_init_random(self._h, int(seed)))
+
+    def load_toy_model(self, model) -> None:
+        """Upload a ToyMoeModel's weights (reference layout, rounded to f32)."""
+        cfg = self.config
+        for l in range(cfg.num_layers):
+            mix = np.ascontiguousarray(model.mixing[l], dtype=np.float32)
+            gw = np.ascontiguousarray(model.gates[l].weights, dtype=np.float32)
+            b = model.gates[l].bias
+            gb = np.ascontiguousarray(b, dtype=np.float32) if b is not None else None
+            _native.check(self._lib.moe_engine_set_dense_f32(
+                self._h, l, mix.ctypes.data, gw.ctypes.data,
+                gb.ctypes.data if gb is not None else None))
+            for e in range(cfg.num_experts):
+                w1 = np.ascontiguousarray(model.expert_w1[l, e], dtype=np.float32)
+                w2 = np.ascontiguousarray(model.expert_w2[l, e], dtype=np.float32)
+                _native.check(self._lib.moe_engine_set_toy_expert_f32(
+                    self._h, l, e, w1.ctypes.data, w2.ctypes.data))
+
+    def expert_block(self, layer: int, expert: int) -> np.ndarray:
+        """Zero-copy uint8 view of one expert block in the pinned host store."""
+        ptr, n = ctypes.c_void_p(), ctypes.c_int64()
+        _native.check(self._lib.moe_engine_expert_host_ptr(self._h, layer, expert,
+                                                           ctypes.byref(ptr), ctypes.byref(n)))
+        buf = (ctypes.c_uint8 * n.value).from_address(ptr.value)
+        return np.frombuffer(buf, dtype=np.uint8)
+
+    def swiglu_weights(self, layer: int, expert: int):
+        """(w1, w3, w2) of one SwiGLU expert as bf16-bit uint16 arrays ([f,d], [f,d], [d,f])."""
+        cfg = self.config
+        f, d = cfg.ffn_dim, cfg.hidden_dim
+        blk = self.expert_block(layer, expert).view(np.uint16)
+        return (blk[: f * d].reshape(f, d), blk[f * d: 2 * f * d].reshape(f, d),
+                blk[2 * f * d:].reshape(d, f))
+
+    def dense_weights(self, layer: int):
+        """Device-layout dense weights: (mixing [d_out, d_in] as uint16 bf16 bits or f32,
+        gate_w [E, d] f32, gate_b [E] f32)."""
+        cfg = self.config
+        D = cfg.hidden_dim if cfg.expert_kind == "swiglu" else (cfg.hidden_dim + 7) // 8 * 8
+        mix = np.empty((D, D), np.uint16 if cfg.expert_kind == "swiglu" else np.float32)
+        gw = np.empty((cfg.num_experts, D), np.float32)
+        gb = np.empty(cfg.num_experts, np.float32)
+        _native.check(self._lib.moe_engine_dense_host(self._h, layer, mix.ctypes.data,
+                                                      gw.ctypes.data, gb.ctypes.data))
+        return mix, gw, gb
+
+    # -- decode --
+    def reset(self) -> None:
+        """Cold caches (policies.warm_state) for every layer."""
+        _native.check(self._lib.moe_engine_reset(self._h))
+
+    def decode_device(self, h_in, h_out=None, stream=None):
+        """Enqueue decode of h_in (T, d) float32 CUDA tensor; returns h_out without syncing."""
+        import torch
+
+        d = self.config.hidden_dim
+        if h_in.dtype != torch.float32 or h_in.device.type != "cuda" or h_in.dim() != 2 or h_in.shape[1] != d:
+            raise ConfigError(f"h_in must be a (T, {d}) float32 CUDA tensor")
+        h_in = h_in.contiguous()
+        T = h_in.shape[0]
+        if h_out is None:
+            h_out = torch.empty_like(h_in)
+        _native.check(self._lib.moe_engine_decode(self._h, h_in.data_ptr(), T, h_out.data_ptr(),
+                                                  _native.stream_ptr(stream)))
+        self.tokens_done += T
+        return h_out
+
+    def sync(self) -> None:
+        _native.check(self._lib.moe_engine_sync(self._h))
+
+    def decode(self, h_in) -> np.ndarray:
+        """Public decode: host (T, d) array in, host (T, d) float32 out (copies included)."""
+        import torch
+
+        x = torch.as_tensor(np.ascontiguousarray(h_in, dtype=np.float32))
+        x = x.pin_memory().to(self._dev, non_blocking=True)
+        y = self.decode_device(x)
+        out = y.cpu().numpy()
+        self.sync()
+        return out
+
+    # -- records / stats --
+    def records(self, t0: int, T: int) -> dict:
+        cfg = self.config
+        L, K, E = cfg.num_layers, cfg.top_k, cfg.num_experts
+        acts = np.zeros((T, L, K), np.int64)
+        guessed = np.zeros((T, max(L - 1, 0), K), np.int64)
+        rb = np.zeros((T, L, E), np.uint8)
+        ev = np.zeros((T, L, E), np.uint8)
+        probs = np.zeros((T, L, K), np.float32)
+        _native.check(self._lib.moe_engine_records(
+            self._h, t0, T, acts.ctypes.data, guessed.ctypes.data if L > 1 else None,
+            rb.ctypes.data, ev.ctypes.data, probs.ctypes.data))
+        return {"acts": acts, "guessed": guessed, "resident_before": rb, "evicted": ev,
+                "probs": probs}
+
+    def event_log(self, t0: int, T: int, warmup_tokens: int = 0):
+        """The engine's own cache decisions as a CacheEventLog (simulate.py format)."""
+        from .simulate import CacheEventLog, SimConfig
+        from .traces import ModelShape
+
+        cfg = self.config
+        rec = self.records(t0, T)
+        layers = tuple(range(cfg.num_layers))
+        return CacheEventLog(
+            config=SimConfig(policy=cfg.policy, cache_size=cfg.cache_size,
+                             warmup_tokens=warmup_tokens),
+            shape=ModelShape(cfg.num_layers, cfg.num_experts, cfg.top_k), layers=layers,
+            activated={l: np.ascontiguousarray(rec["acts"][:, l, :]) for l in layers},
+            resident_before={l: np.ascontiguousarray(rec["resident_before"][:, l, :]) for l in layers},
+            evicted={l: np.ascontiguousarray(rec["evicted"][:, l, :]) for l in layers},
+            num_tokens=T)
+
+    def stats(self) -> dict:
+        s = _native.StatsC()
+        _native.check(self._lib.moe_engine_stats(self._h, ctypes.byref(s)))
+        return {name: getattr(s, name) for name, _ in _native.StatsC._fields_}
+
+
+def hash_weights(seed: int, tensor_id: int, std: float, n: int, dtype: str = "bf16"):
+    """Device tensor of n synthetic values (counter hash; bf16 returned as uint16 bits)."""
+    import torch
+
+    lib = _native.lib()
+    if dtype == "bf16":
+        out = torch.empty(n, dtype=torch.int16, device="cuda")
+        _native.check(lib.moe_hash_weights_bf16(seed, tensor_id, std, n, out.data_ptr(),
+                                                _native.stream_ptr()))
+    else:
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+        _native.check(lib.moe_hash_weights_f32(seed, tensor_id, std, n, out.data_ptr(),
+                                               _native.stream_ptr()))
+    return out
+
+
+def tensor_id(kind: int, layer: int = 0, expert: int = 0, matrix: int = 0) -> int:
+    """kind: 1 mixing, 2 gate_w, 3 gate_b, 4 expert (matrix 1 w1, 2 w3, 3 w2), 5 inputs."""
+    return (kind << 40) | (layer << 16) | (expert << 4) | matrix
