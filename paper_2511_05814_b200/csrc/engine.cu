@@ -1,20 +1,25 @@
 // Host runtime of the offload decode engine: weights in pinned host DRAM, a fixed-size
-// per-layer expert cache in HBM, and a transfer thread that forwards the device's load
-// decisions to the copy engine.
+// per-layer expert cache in HBM, and a forwarder that hands the device's load decisions to
+// the copy engine.
 //
 // Per (token t, layer l), on the caller's compute stream:
 //   mix_kernel        h_in -> h' = h_in + alpha * M h_in                 (toymoe.py:140)
 //   gate_cache_kernel gate, softmax, top-k, guess, policy step, buffers  (toymoe.py:99-115,
 //                     178-180; kernels.py:89-145) -> step record + mailbox entry
 //   up/down (phase 0) experts that hit: run while the misses are in flight
-//   cuStreamWaitValue32(ready >= seq + 1)   (released by the copy stream after the misses land)
+//   [cudaStreamWaitEvent on the copy stream's event, only if the step has demand copies]
 //   up/down (phase 1) experts that missed
-// The transfer thread polls the mailbox (mapped pinned memory), issues cudaMemcpyAsync of
-// the missed expert blocks on the copy stream, then cuStreamWriteValue32(ready, seq + 1).
+// The calling thread runs in lockstep one layer behind the GPU: it polls the mailbox
+// (mapped pinned memory) for the gate's decision, issues cudaMemcpyAsync of the missed
+// expert blocks on the copy stream, and orders phase 1 after them with an event.  The
+// host never chooses anything: the device picked the experts and the HBM buffers.
+// (Cross-stream waits on memory flags -- cuStreamWaitValue or a spinning kernel -- were
+// measured to stall copies queued behind them on this driver; every dependency here is
+// CUDA-visible.)  While it waits for the next decision
+// the thread trickles speculative-prefetch chunks onto the copy stream.
 #include "engine_kernels.cuh"
 #include "hash.cuh"
 
-#include <cuda.h>
 #include <sys/mman.h>
 #include <unistd.h>
 
@@ -24,7 +29,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
-#include <map>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -36,66 +40,45 @@ moe_status launch_hash_bf16(uint64_t seed, uint64_t tid, float std, long long n,
 moe_status launch_hash_f32(uint64_t seed, uint64_t tid, float std, long long n, float* out,
                            cudaStream_t s);
 
-// ---- driver entry points (stream memory operations) ------------------------------------
-typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-static PFN_waitValue32 p_waitValue32 = nullptr;
-static PFN_writeValue32 p_writeValue32 = nullptr;
-
-static moe_status load_driver_entry_points() {
-  static std::once_flag once;
-  static moe_status st = MOE_OK;
-  std::call_once(once, [] {
-    cudaDriverEntryPointQueryResult q1, q2;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", reinterpret_cast<void**>(&p_waitValue32),
-                                cudaEnableDefault, &q1) != cudaSuccess ||
-        q1 != cudaDriverEntryPointSuccess ||
-        cudaGetDriverEntryPoint("cuStreamWriteValue32",
-                                reinterpret_cast<void**>(&p_writeValue32), cudaEnableDefault,
-                                &q2) != cudaSuccess ||
-        q2 != cudaDriverEntryPointSuccess) {
-      set_error("stream memory operations (cuStreamWaitValue32/WriteValue32) unavailable");
-      st = MOE_CUDA_ERROR;
-    }
-  });
-  return st;
-}
-
 // ---- pinned host store ------------------------------------------------------------------
-// Anonymous mapping with transparent huge pages, first-touched by all host threads in
-// parallel, then page-locked with cudaHostRegister (portable: usable from every context).
+// Default: cudaHostAlloc (portable).  MOE_PIN_MODE=register: anonymous mapping with
+// transparent huge pages, first-touched by all host threads in parallel, then
+// cudaHostRegister (faster to set up for the 90 GB Mixtral-8x7B store).
 struct PinnedStore {
   char* base = nullptr;
   size_t bytes = 0;
   bool registered = false;
   bool via_alloc = false;
+  double setup_ms = 0;
 
   moe_status allocate(size_t n) {
+    const auto t0 = std::chrono::steady_clock::now();
     bytes = n;
     const char* mode = getenv("MOE_PIN_MODE");
-    if (mode && strcmp(mode, "alloc") == 0) {
+    if (!(mode && strcmp(mode, "register") == 0)) {
       via_alloc = true;
       MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&base), n, cudaHostAllocPortable));
-      return MOE_OK;
+    } else {
+      void* p = mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+      if (p == MAP_FAILED) {
+        set_error("mmap of %zu bytes for the expert store failed", n);
+        return MOE_OOM;
+      }
+      base = static_cast<char*>(p);
+      madvise(base, n, MADV_HUGEPAGE);
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+      const size_t per = ((n + hw - 1) / hw + 4095) & ~size_t(4095);
+      std::vector<std::thread> th;
+      for (unsigned i = 0; i < hw; ++i)
+        th.emplace_back([this, i, per] {
+          const size_t lo = i * per, hi = std::min(bytes, lo + per);
+          for (size_t o = lo; o < hi; o += 4096) base[o] = 0;
+        });
+      for (auto& x : th) x.join();
+      MOE_CUDA(cudaHostRegister(base, n, cudaHostRegisterPortable));
+      registered = true;
     }
-    void* p = mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
-    if (p == MAP_FAILED) {
-      set_error("mmap of %zu bytes for the expert store failed", n);
-      return MOE_OOM;
-    }
-    base = static_cast<char*>(p);
-    madvise(base, n, MADV_HUGEPAGE);
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t per = ((n + hw - 1) / hw + 4095) & ~size_t(4095);
-    std::vector<std::thread> th;
-    for (unsigned i = 0; i < hw; ++i)
-      th.emplace_back([this, i, per] {
-        const size_t lo = i * per, hi = std::min(bytes, lo + per);
-        for (size_t o = lo; o < hi; o += 4096) base[o] = 0;
-      });
-    for (auto& x : th) x.join();
-    MOE_CUDA(cudaHostRegister(base, n, cudaHostRegisterPortable));
-    registered = true;
+    setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return MOE_OK;
   }
   void release() {
@@ -136,37 +119,42 @@ struct moe_engine {
   StepRecord* ring = nullptr;    // [max_tokens][L]
   float *h_in = nullptr, *h_mid = nullptr, *y = nullptr, *act = nullptr;
   float *x_pad = nullptr, *out_pad = nullptr;  // padded token staging when d % 8 != 0
-  unsigned int* ready_ctr = nullptr;
   int* err = nullptr;
   DeviceStats* dstats = nullptr;
 
   // mapped pinned memory shared with the device
   MailRecord* mail_h = nullptr;
   MailRecord* mail_d = nullptr;
-  volatile long long* consumed_h = nullptr;
-  long long* consumed_d = nullptr;
-  volatile unsigned int* chunk_done_h = nullptr;
-  CUdeviceptr chunk_done_d = 0;
+  HostControl* ctl_h = nullptr;
+  HostControl* ctl_d = nullptr;
 
   PinnedStore store;
   cudaStream_t copy_stream = nullptr;
 
-  // transfer thread
-  std::thread worker;
-  std::atomic<bool> stop{false};
-  std::atomic<long long> next_mail{0};  // first mail seq not yet processed
-  long long tokens_done = 0;            // absolute tokens enqueued
+  // forwarder state (driven by the thread calling decode)
+  long long next_mail = 0;    // first mail seq not yet forwarded
+  long long tokens_done = 0;  // absolute tokens enqueued
   std::deque<PrefetchJob> jobs;
-  unsigned int chunks_issued = 0;
+  std::deque<cudaEvent_t> prefetch_inflight;  // one event per prefetch chunk in flight
+  std::vector<cudaEvent_t> sync_events;       // free list (timing disabled)
+  std::vector<cudaEvent_t> order_events;      // ring of events ordering phase 1 after copies
+  size_t order_next = 0;
   std::mutex stats_mu;
   moe_stats st{};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_events;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> free_events;
-  std::atomic<int> worker_error{0};
-  std::string worker_msg;
+  bool debug = getenv("MOE_DEBUG") != nullptr;
 };
 
 namespace {
+
+#define TRY(x)                     \
+  do {                             \
+    moe_status _s = (x);           \
+    if (_s != MOE_OK) return _s;   \
+  } while (0)
+
+moe_status create_resources(moe_engine* g);
 
 moe_status issue_copy(moe_engine* g, int layer, int buf, int expert, long long off, long long n) {
   char* dst = g->pool + (static_cast<long long>(layer) * g->NB + buf) * g->expert_bytes + off;
@@ -176,24 +164,36 @@ moe_status issue_copy(moe_engine* g, int layer, int buf, int expert, long long o
   return MOE_OK;
 }
 
-std::pair<cudaEvent_t, cudaEvent_t> take_events(moe_engine* g) {
+std::pair<cudaEvent_t, cudaEvent_t> take_timing_events(moe_engine* g) {
   std::lock_guard<std::mutex> lk(g->stats_mu);
   if (!g->free_events.empty()) {
     auto e = g->free_events.back();
     g->free_events.pop_back();
     return e;
   }
-  cudaEvent_t a, b;
+  cudaEvent_t a = nullptr, b = nullptr;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   return {a, b};
 }
 
-// Process one mailbox entry: cancels, new prefetches, demand copies, release.
-moe_status handle_mail(moe_engine* g, const MailRecord& m) {
+cudaEvent_t take_sync_event(moe_engine* g) {
+  if (!g->sync_events.empty()) {
+    cudaEvent_t e = g->sync_events.back();
+    g->sync_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+
+// Forward one mailbox entry: cancels, demand copies, new prefetch jobs.  Returns through
+// *has_demand whether the compute stream must wait for the copy stream.
+moe_status handle_mail(moe_engine* g, const MailRecord& m, bool* has_demand) {
   const long long chunk = g->cfg.chunk_bytes;
   const long long nchunks = (g->expert_bytes + chunk - 1) / chunk;
-  // cancelled staging buffers of this step's layer: stop their remaining chunks
+  // cancelled staging buffers of this step's layer: stop issuing their remaining chunks
   for (int i = 0; i < m.n_cancel; ++i)
     for (auto& j : g->jobs)
       if (!j.cancelled && !j.adopted && j.layer == m.layer && j.buf == m.cancel_buf[i]) {
@@ -202,10 +202,10 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m) {
         g->st.prefetch_wasted_bytes += std::min(j.next_chunk * chunk, g->expert_bytes);
       }
   long long demand = 0;
-  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  std::pair<cudaEvent_t, cudaEvent_t> tev{nullptr, nullptr};
   if (m.n_demand > 0) {
-    ev = take_events(g);
-    MOE_CUDA(cudaEventRecord(ev.first, g->copy_stream));
+    tev = take_timing_events(g);
+    MOE_CUDA(cudaEventRecord(tev.first, g->copy_stream));
   }
   for (int i = 0; i < m.n_demand; ++i) {
     const int e = m.demand_expert[i], b = m.demand_buf[i];
@@ -227,50 +227,61 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m) {
       demand += n;
     }
   }
-  if (m.n_demand > 0) MOE_CUDA(cudaEventRecord(ev.second, g->copy_stream));
-  if (m.n_demand > 0 || m.need_ack) {
-    if (p_writeValue32(reinterpret_cast<CUstream>(g->copy_stream),
-                       reinterpret_cast<CUdeviceptr>(g->ready_ctr),
-                       static_cast<cuuint32_t>(m.seq + 1), 0) != CUDA_SUCCESS) {
-      set_error("cuStreamWriteValue32 failed");
-      return MOE_CUDA_ERROR;
-    }
-  }
-  // new prefetches for layer + 1 (issued chunk by chunk from the idle loop)
-  for (int i = 0; i < m.n_prefetch; ++i) {
+  if (m.n_demand > 0) MOE_CUDA(cudaEventRecord(tev.second, g->copy_stream));
+  *has_demand = m.n_demand > 0;
+  for (int i = 0; i < m.n_prefetch; ++i)
     g->jobs.push_back(PrefetchJob{m.layer + 1, m.prefetch_buf[i], m.prefetch_expert[i], 0,
                                   nchunks, false, false});
-  }
   std::lock_guard<std::mutex> lk(g->stats_mu);
   g->st.demand_bytes += demand;
   g->st.h2d_bytes += demand;
   g->st.prefetch_issued += m.n_prefetch;
-  if (m.n_demand > 0) g->busy_events.push_back(ev);
+  if (m.n_demand > 0) g->busy_events.push_back(tev);
   return MOE_OK;
+}
+
+// Fold completed demand-copy timing pairs into copy_busy_ms and recycle them.
+void recycle_busy_events(moe_engine* g) {
+  std::lock_guard<std::mutex> lk(g->stats_mu);
+  size_t keep = 0;
+  for (size_t i = 0; i < g->busy_events.size(); ++i) {
+    auto e = g->busy_events[i];
+    float ms = 0.f;
+    if (keep == 0 && cudaEventQuery(e.second) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, e.first, e.second) == cudaSuccess) {
+      g->st.copy_busy_ms += ms;
+      g->free_events.push_back(e);
+    } else {
+      g->busy_events[keep++] = e;
+    }
+  }
+  g->busy_events.resize(keep);
 }
 
 // Issue one chunk of the oldest live prefetch job if the in-flight budget allows.
 moe_status pump_prefetch(moe_engine* g, bool* did) {
   *did = false;
+  if (g->busy_events.size() > 16) recycle_busy_events(g);
+  while (!g->prefetch_inflight.empty() &&
+         cudaEventQuery(g->prefetch_inflight.front()) == cudaSuccess) {
+    g->sync_events.push_back(g->prefetch_inflight.front());
+    g->prefetch_inflight.pop_front();
+  }
   while (!g->jobs.empty() &&
          (g->jobs.front().cancelled || g->jobs.front().adopted ||
           g->jobs.front().next_chunk >= g->jobs.front().n_chunks))
     g->jobs.pop_front();
   if (g->jobs.empty()) return MOE_OK;
-  const unsigned int done = *g->chunk_done_h;
-  if (g->chunks_issued - done >= static_cast<unsigned int>(g->cfg.prefetch_depth)) return MOE_OK;
+  if (g->prefetch_inflight.size() >= static_cast<size_t>(g->cfg.prefetch_depth)) return MOE_OK;
   PrefetchJob& j = g->jobs.front();
   const long long chunk = g->cfg.chunk_bytes;
   const long long off = j.next_chunk * chunk, n = std::min(chunk, g->expert_bytes - off);
   moe_status s = issue_copy(g, j.layer, j.buf, j.expert, off, n);
   if (s != MOE_OK) return s;
   j.next_chunk += 1;
-  g->chunks_issued += 1;
-  if (p_writeValue32(reinterpret_cast<CUstream>(g->copy_stream), g->chunk_done_d,
-                     g->chunks_issued, 0) != CUDA_SUCCESS) {
-    set_error("cuStreamWriteValue32 failed");
-    return MOE_CUDA_ERROR;
-  }
+  cudaEvent_t ev = take_sync_event(g);
+  MOE_CUDA(cudaEventRecord(ev, g->copy_stream));
+  g->prefetch_inflight.push_back(ev);
   std::lock_guard<std::mutex> lk(g->stats_mu);
   g->st.prefetch_bytes += n;
   g->st.h2d_bytes += n;
@@ -278,37 +289,41 @@ moe_status pump_prefetch(moe_engine* g, bool* did) {
   return MOE_OK;
 }
 
-void worker_main(moe_engine* g) {
-  cudaSetDevice(g->device);
-  long long idle = 0;
-  while (!g->stop.load(std::memory_order_relaxed)) {
-    const long long seq = g->next_mail.load(std::memory_order_relaxed);
-    MailRecord& m = g->mail_h[seq % kMailRing];
-    if (m.ready == seq + 1) {
-      std::atomic_thread_fence(std::memory_order_acquire);
-      MailRecord copy;
-      memcpy(&copy, const_cast<MailRecord*>(&m), sizeof(MailRecord));
-      moe_status s = handle_mail(g, copy);
-      if (s != MOE_OK) {
-        g->worker_msg = moe_last_error();
-        g->worker_error.store(s);
-        return;
-      }
-      g->next_mail.store(seq + 1, std::memory_order_release);
-      *g->consumed_h = seq + 1;
-      idle = 0;
-      continue;
-    }
+// Wait for the gate's mail of step `seq` (the GPU is at most one step ahead), pumping
+// prefetch chunks meanwhile.  A stream that finished or failed without posting it is an
+// error, never a hang.
+moe_status await_mail(moe_engine* g, long long seq, cudaStream_t compute, MailRecord* out) {
+  MailRecord& m = g->mail_h[seq % kMailRing];
+  long long spins = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  while (m.ready != seq + 1) {
     bool did = false;
-    moe_status s = pump_prefetch(g, &did);
-    if (s != MOE_OK) {
-      g->worker_msg = moe_last_error();
-      g->worker_error.store(s);
-      return;
-    }
+    TRY(pump_prefetch(g, &did));
     if (did) continue;
-    if (++idle > 200000) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    if ((++spins & 1023) == 0) {
+      const cudaError_t q = cudaStreamQuery(compute);
+      if (q != cudaSuccess && q != cudaErrorNotReady) {
+        set_error("compute stream failed while waiting for step %lld: %s", seq, cudaGetErrorString(q));
+        return MOE_CUDA_ERROR;
+      }
+      if (q == cudaSuccess && m.ready != seq + 1) {
+        std::atomic_thread_fence(std::memory_order_acquire);
+        if (m.ready != seq + 1) {
+          set_error("gate of step %lld finished without posting its decision", seq);
+          return MOE_CUDA_ERROR;
+        }
+      }
+      const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (waited > 120.0) {
+        set_error("no gate decision for step %lld after %.0f s", seq, waited);
+        return MOE_CUDA_ERROR;
+      }
+      if (spins > (1 << 16)) std::this_thread::yield();
+    }
   }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  memcpy(out, const_cast<MailRecord*>(&m), sizeof(MailRecord));
+  return MOE_OK;
 }
 
 moe_status alloc_device(void** p, size_t n) {
@@ -316,12 +331,6 @@ moe_status alloc_device(void** p, size_t n) {
   MOE_CUDA(cudaMemset(*p, 0, n));
   return MOE_OK;
 }
-
-#define TRY(x)                     \
-  do {                             \
-    moe_status _s = (x);           \
-    if (_s != MOE_OK) return _s;   \
-  } while (0)
 
 int round8(int x) { return (x + 7) / 8 * 8; }
 
@@ -351,7 +360,11 @@ moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) 
   MOE_REQUIRE(c.prefetch == MOE_PREFETCH_OFF || c.prefetch == MOE_PREFETCH_EARLY,
               "unknown prefetch mode %d", c.prefetch);
   MOE_REQUIRE(c.max_tokens >= 1, "max_tokens must be >= 1");
-  TRY(load_driver_entry_points());
+  MOE_REQUIRE(c.expert_kind != MOE_EXPERT_SWIGLU_BF16 ||
+                  (c.hidden_dim % 8 == 0 && c.ffn_dim >= 8 && c.ffn_dim % 8 == 0),
+              "SwiGLU experts need hidden_dim and ffn_dim multiples of 8");
+  MOE_REQUIRE(c.cache_size + (c.prefetch ? c.top_k : 0) <= kMaxBuf,
+              "cache_size + staging buffers must be <= %d", kMaxBuf);
 
   auto* g = new moe_engine();
   g->cfg = c;
@@ -361,8 +374,6 @@ moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) 
   g->d = c.hidden_dim;
   g->bf16 = c.expert_kind == MOE_EXPERT_SWIGLU_BF16;
   if (g->bf16) {
-    MOE_REQUIRE(c.hidden_dim % 8 == 0 && c.ffn_dim >= 8 && c.ffn_dim % 8 == 0,
-                "SwiGLU experts need hidden_dim and ffn_dim multiples of 8");
     g->dpad = c.hidden_dim;
     g->f = c.ffn_dim;
     g->expert_bytes = 3ll * g->f * g->dpad * 2;
@@ -373,10 +384,24 @@ moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) 
   }
   g->S = c.prefetch ? c.top_k : 0;
   g->NB = c.cache_size + g->S;
-  MOE_REQUIRE(g->NB <= kMaxBuf, "cache_size + staging buffers must be <= %d", kMaxBuf);
+  const moe_status st = create_resources(g);
+  if (st != MOE_OK) {
+    const std::string msg = moe_last_error();
+    moe_engine_destroy(g);
+    set_error("%s", msg.c_str());
+    return st;
+  }
+  *out = g;
+  return MOE_OK;
+}
+
+}  // extern "C"
+
+namespace {
+moe_status create_resources(moe_engine* g) {
+  const moe_engine_config& c = g->cfg;
   const int L = c.num_layers, E = c.num_experts, K = c.top_k, D = g->dpad;
   MOE_CUDA(cudaSetDevice(g->device));
-
   const size_t msz = g->bf16 ? 2 : 4;
   TRY(alloc_device(reinterpret_cast<void**>(&g->pool), static_cast<size_t>(L) * g->NB * g->expert_bytes));
   TRY(alloc_device(&g->mixing, static_cast<size_t>(L) * D * D * msz));
@@ -388,7 +413,6 @@ moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) 
   TRY(alloc_device(reinterpret_cast<void**>(&g->h_mid), sizeof(float) * 2 * D));
   TRY(alloc_device(reinterpret_cast<void**>(&g->y), sizeof(float) * K * D));
   TRY(alloc_device(reinterpret_cast<void**>(&g->act), sizeof(float) * K * g->f));
-  TRY(alloc_device(reinterpret_cast<void**>(&g->ready_ctr), sizeof(unsigned int)));
   TRY(alloc_device(reinterpret_cast<void**>(&g->err), sizeof(int)));
   TRY(alloc_device(reinterpret_cast<void**>(&g->dstats), sizeof(DeviceStats)));
   if (D != g->d) {
@@ -399,39 +423,44 @@ moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) 
                          cudaHostAllocMapped | cudaHostAllocPortable));
   memset(g->mail_h, 0, sizeof(MailRecord) * kMailRing);
   MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g->mail_d), g->mail_h, 0));
-  long long* consumed = nullptr;
-  MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&consumed), sizeof(long long),
+  MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->ctl_h), sizeof(HostControl),
                          cudaHostAllocMapped | cudaHostAllocPortable));
-  *consumed = 0;
-  g->consumed_h = consumed;
-  MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g->consumed_d), consumed, 0));
-  unsigned int* cd = nullptr;
-  MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cd), sizeof(unsigned int),
-                         cudaHostAllocMapped | cudaHostAllocPortable));
-  *cd = 0;
-  g->chunk_done_h = cd;
-  void* cdd = nullptr;
-  MOE_CUDA(cudaHostGetDevicePointer(&cdd, cd, 0));
-  g->chunk_done_d = reinterpret_cast<CUdeviceptr>(cdd);
+  memset(g->ctl_h, 0, sizeof(HostControl));
+  MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g->ctl_d), g->ctl_h, 0));
   MOE_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
-
+  // every event the forwarder will need, created up front (no allocation on the hot path)
+  for (int i = 0; i < 64; ++i) {
+    cudaEvent_t e = nullptr;
+    MOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g->sync_events.push_back(e);
+  }
+  for (int i = 0; i < 8; ++i) {
+    cudaEvent_t e = nullptr;
+    MOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g->order_events.push_back(e);
+  }
+  for (int i = 0; i < 4 * c.num_layers; ++i) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    MOE_CUDA(cudaEventCreate(&a));
+    MOE_CUDA(cudaEventCreate(&b));
+    g->free_events.push_back({a, b});
+  }
   TRY(g->store.allocate(static_cast<size_t>(L) * E * g->expert_bytes));
   reset_states_kernel<<<L, 64>>>(g->states, L, g->NB);
   MOE_LAUNCHED();
   MOE_CUDA(cudaDeviceSynchronize());
   g->st.expert_bytes = g->expert_bytes;
-  g->worker = std::thread(worker_main, g);
-  *out = g;
   return MOE_OK;
 }
+}  // namespace
+
+extern "C" {
 
 moe_status moe_engine_destroy(moe_engine* g) {
   if (!g) return MOE_OK;
   cudaSetDevice(g->device);
   cudaDeviceSynchronize();
-  g->stop.store(true);
-  if (g->worker.joinable()) g->worker.join();
-  cudaStreamSynchronize(g->copy_stream);
+  if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);
   for (auto& e : g->busy_events) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -440,13 +469,15 @@ moe_status moe_engine_destroy(moe_engine* g) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
   }
+  for (auto e : g->sync_events) cudaEventDestroy(e);
+  for (auto e : g->prefetch_inflight) cudaEventDestroy(e);
+  for (auto e : g->order_events) cudaEventDestroy(e);
   void* dev[] = {g->pool, g->mixing, g->gate_w, g->gate_b, g->states, g->ring, g->h_in,
-                 g->h_mid, g->y, g->act, g->ready_ctr, g->err, g->dstats, g->x_pad, g->out_pad};
+                 g->h_mid, g->y, g->act, g->err, g->dstats, g->x_pad, g->out_pad};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (g->mail_h) cudaFreeHost(g->mail_h);
-  if (g->consumed_h) cudaFreeHost(const_cast<long long*>(g->consumed_h));
-  if (g->chunk_done_h) cudaFreeHost(const_cast<unsigned int*>(g->chunk_done_h));
+  if (g->ctl_h) cudaFreeHost(g->ctl_h);
   if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
   g->store.release();
   delete g;
@@ -561,6 +592,7 @@ moe_status moe_engine_reset(moe_engine* g) {
   MOE_CUDA(cudaSetDevice(g->device));
   MOE_CUDA(cudaDeviceSynchronize());
   MOE_CUDA(cudaStreamSynchronize(g->copy_stream));
+  g->jobs.clear();
   reset_states_kernel<<<g->cfg.num_layers, 64>>>(g->states, g->cfg.num_layers, g->NB);
   MOE_LAUNCHED();
   MOE_CUDA(cudaMemset(g->err, 0, sizeof(int)));
@@ -572,10 +604,6 @@ moe_status moe_engine_decode(moe_engine* g, const float* h_in_dev, int64_t T, fl
                              void* stream) {
   MOE_REQUIRE(g, "null engine");
   MOE_REQUIRE(T >= 0, "negative token count");
-  if (g->worker_error.load()) {
-    set_error("transfer thread failed: %s", g->worker_msg.c_str());
-    return MOE_CUDA_ERROR;
-  }
   MOE_CUDA(cudaSetDevice(g->device));
   cudaStream_t s = as_stream(stream);
   const moe_engine_config& c = g->cfg;
@@ -599,6 +627,20 @@ moe_status moe_engine_decode(moe_engine* g, const float* h_in_dev, int64_t T, fl
     attrs = true;
   }
   MOE_REQUIRE(mix_smem <= 200 * 1024 && down_smem <= 200 * 1024, "hidden/ffn dims too large");
+  auto launch_ffn = [&](FfnParams fp) -> moe_status {
+    if (g->bf16) {
+      swiglu_up_kernel<<<dim3(up_grid, K), 256, up_smem, s>>>(fp);
+      MOE_LAUNCHED();
+      down_kernel<true><<<dim3(down_grid, K), 256, down_smem, s>>>(fp);
+      MOE_LAUNCHED();
+    } else {
+      toy_up_kernel<<<dim3(up_grid, K), 256, up_smem, s>>>(fp);
+      MOE_LAUNCHED();
+      down_kernel<false><<<dim3(down_grid, K), 256, down_smem, s>>>(fp);
+      MOE_LAUNCHED();
+    }
+    return MOE_OK;
+  };
   for (int64_t t = 0; t < T; ++t) {
     const long long tok = g->tokens_done + t;
     StepRecord* trec = g->ring + (tok % c.max_tokens) * L;
@@ -622,33 +664,30 @@ moe_status moe_engine_decode(moe_engine* g, const float* h_in_dev, int64_t T, fl
       GateParams gp{hm, g->h_in, g->gate_w, g->gate_b, l, L, c.num_experts, K, D, c.cache_size,
                     g->NB, c.policy, c.decay_factor, c.decay_period, c.record_speculation,
                     c.prefetch, c.renormalize, seq, g->states, trec + l, g->mail_d,
-                    g->consumed_d, g->ready_ctr, g->err, g->dstats};
+                    g->ctl_d, g->err, g->dstats};
       gate_cache_kernel<<<1, 256, 0, s>>>(gp);
       MOE_LAUNCHED();
       FfnParams fp{hm, trec + l, g->states + l,
                    g->pool + static_cast<long long>(l) * g->NB * g->expert_bytes, g->expert_bytes,
                    D, g->f, K, 0, g->act, g->y};
-      for (int phase = 0; phase < 2; ++phase) {
-        if (phase == 1) {
-          if (p_waitValue32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(g->ready_ctr),
-                            static_cast<cuuint32_t>(seq + 1), CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
-            set_error("cuStreamWaitValue32 failed");
-            return MOE_CUDA_ERROR;
-          }
-        }
-        fp.phase = phase;
-        if (g->bf16) {
-          swiglu_up_kernel<<<dim3(up_grid, K), 256, up_smem, s>>>(fp);
-          MOE_LAUNCHED();
-          down_kernel<true><<<dim3(down_grid, K), 256, down_smem, s>>>(fp);
-          MOE_LAUNCHED();
-        } else {
-          toy_up_kernel<<<dim3(up_grid, K), 256, up_smem, s>>>(fp);
-          MOE_LAUNCHED();
-          down_kernel<false><<<dim3(down_grid, K), 256, down_smem, s>>>(fp);
-          MOE_LAUNCHED();
-        }
+      TRY(launch_ffn(fp));  // phase 0: experts that hit run while the misses are fetched
+      // forward the device's decision for this step (lockstep, one step behind the GPU)
+      MailRecord m;
+      TRY(await_mail(g, seq, s, &m));
+      if (g->debug)
+        fprintf(stderr, "[moe] seq=%lld layer=%d demand=%d cancel=%d prefetch=%d\n", m.seq,
+                m.layer, m.n_demand, m.n_cancel, m.n_prefetch);
+      bool has_demand = false;
+      TRY(handle_mail(g, m, &has_demand));
+      g->next_mail = seq + 1;
+      g->ctl_h->consumed = seq + 1;
+      if (has_demand) {
+        cudaEvent_t ev = g->order_events[g->order_next++ % g->order_events.size()];
+        MOE_CUDA(cudaEventRecord(ev, g->copy_stream));
+        MOE_CUDA(cudaStreamWaitEvent(s, ev, 0));
       }
+      fp.phase = 1;
+      TRY(launch_ffn(fp));
     }
     float* out = h_out_dev + t * d;
     float* dst = D != d ? g->out_pad : out;
@@ -666,10 +705,6 @@ moe_status moe_engine_sync(moe_engine* g) {
   MOE_REQUIRE(g, "null engine");
   MOE_CUDA(cudaSetDevice(g->device));
   MOE_CUDA(cudaDeviceSynchronize());
-  if (g->worker_error.load()) {
-    set_error("transfer thread failed: %s", g->worker_msg.c_str());
-    return MOE_CUDA_ERROR;
-  }
   int h = 0;
   MOE_CUDA(cudaMemcpy(&h, g->err, sizeof(int), cudaMemcpyDeviceToHost));
   if (h) {
@@ -724,13 +759,8 @@ moe_status moe_engine_stats(moe_engine* g, moe_stats* out) {
   MOE_CUDA(cudaStreamSynchronize(g->copy_stream));
   DeviceStats ds{};
   MOE_CUDA(cudaMemcpy(&ds, g->dstats, sizeof(ds), cudaMemcpyDeviceToHost));
+  recycle_busy_events(g);
   std::lock_guard<std::mutex> lk(g->stats_mu);
-  for (auto& e : g->busy_events) {
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, e.first, e.second) == cudaSuccess) g->st.copy_busy_ms += ms;
-    g->free_events.push_back(e);
-  }
-  g->busy_events.clear();
   *out = g->st;
   out->hits = static_cast<int64_t>(ds.hits);
   out->misses = static_cast<int64_t>(ds.misses);

@@ -52,6 +52,13 @@ struct DeviceStats {
   unsigned long long hits, misses;
 };
 
+// Mapped pinned control block shared by the device and the host forwarder.
+struct HostControl {
+  volatile long long consumed;      // host -> device: mails fully processed (back-pressure)
+  volatile unsigned int gate_done;  // device -> host: last gate seq + 1 (diagnostics)
+  volatile unsigned int pad;
+};
+
 // ---------------------------------------------------------------------------------------
 // Vector staging: x (n floats) is kept in shared memory as two float4 planes so that a lane
 // reading the 8 activations matching one 16-byte weight vector hits consecutive banks.
@@ -197,8 +204,7 @@ struct GateParams {
   LayerState* states;      // [L]
   StepRecord* rec;         // this step's record
   MailRecord* mail;        // ring base (device view of mapped pinned memory)
-  const volatile long long* host_consumed;  // mails the host has finished (mapped)
-  unsigned int* ready_ctr; // compute stream waits on ready_ctr >= seq + 1
+  HostControl* ctl;        // device view of the mapped control block
   int* err;
   DeviceStats* stats;
 };
@@ -408,7 +414,7 @@ __global__ void __launch_bounds__(256) gate_cache_kernel(GateParams p) {
     }
   }
   // ring back-pressure: if the host is far behind, make it acknowledge this step
-  const long long consumed = *p.host_consumed;
+  const long long consumed = p.ctl->consumed;
   const int need_ack = (p.seq - consumed) >= (kMailRing / 2) ? 1 : 0;
   mr->seq = p.seq;
   mr->layer = p.layer;
@@ -418,10 +424,10 @@ __global__ void __launch_bounds__(256) gate_cache_kernel(GateParams p) {
   mr->need_ack = need_ack;
   __threadfence_system();
   mr->ready = p.seq + 1;
-  __threadfence_system();
-  // steps the host need not gate are released by the device itself
-  if (nd == 0 && !need_ack) atomicMax(p.ready_ctr, static_cast<unsigned int>(p.seq + 1));
+  p.ctl->gate_done = static_cast<unsigned int>(p.seq + 1);
 }
+
+
 
 // ---- K3: expert FFN over the selected slots ---------------------------------------------
 struct FfnParams {

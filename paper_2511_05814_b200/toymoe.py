@@ -76,7 +76,7 @@ class ToyMoeModel:
 def _cuda_f64(a) -> "torch.Tensor":
     import torch
 
-    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device="cuda")
+    return torch.tensor(np.array(a, dtype=np.float64, copy=True), device="cuda")
 
 
 def _gate_on_device(values: np.ndarray, gate: GatingNetwork, k: int):
@@ -93,9 +93,11 @@ def _gate_on_device(values: np.ndarray, gate: GatingNetwork, k: int):
     lib = _native.lib()
     order = torch.empty(max(k, 1), dtype=torch.int64, device="cuda")
     probs = torch.empty(E, dtype=torch.float64, device="cuda")
+    # keep every device tensor referenced until the call returns
+    t_v, t_w = _cuda_f64(v), _cuda_f64(w)
     bias = _cuda_f64(gate.bias) if gate.bias is not None else None
     _native.check(lib.moe_gate_topk_f64(
-        _cuda_f64(v).data_ptr(), _cuda_f64(w).data_ptr(), bias.data_ptr() if bias is not None else None,
+        t_v.data_ptr(), t_w.data_ptr(), bias.data_ptr() if bias is not None else None,
         d, E, int(k), order.data_ptr(), probs.data_ptr(), _native.stream_ptr()))
     return order.cpu().numpy()[:k], probs.cpu().numpy()
 
@@ -133,10 +135,11 @@ def forward_token(model: ToyMoeModel, h_in: HiddenState, layer: int):
     sel = torch.empty(K, dtype=torch.int64, device="cuda")
     probs = torch.empty(E, dtype=torch.float64, device="cuda")
     bias = _cuda_f64(gate.bias) if gate.bias is not None else None
+    t = [_cuda_f64(a) for a in (x, model.mixing[layer], gate.weights, model.expert_w1[layer],
+                                model.expert_w2[layer])]
     _native.check(lib.moe_toy_forward_f64(
-        _cuda_f64(x).data_ptr(), _cuda_f64(model.mixing[layer]).data_ptr(),
-        _cuda_f64(gate.weights).data_ptr(), bias.data_ptr() if bias is not None else None,
-        _cuda_f64(model.expert_w1[layer]).data_ptr(), _cuda_f64(model.expert_w2[layer]).data_ptr(),
+        t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(),
+        bias.data_ptr() if bias is not None else None, t[3].data_ptr(), t[4].data_ptr(),
         d, E, K, float(cfg.mixing_scale), out.data_ptr(), sel.data_ptr(), probs.data_ptr(),
         _native.stream_ptr()))
     return HiddenState(values=out.cpu().numpy(), layer=layer), frozenset(sel.cpu().tolist())

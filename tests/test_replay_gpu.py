@@ -7,7 +7,8 @@ import pytest
 
 import oracle
 from conftest import golden_streams, random_stream
-from paper_2511_05814_b200 import kernels, simulate as sim
+from paper_2511_05814_b200 import kernels
+from paper_2511_05814_b200.simulate import SimConfig, simulate
 from paper_2511_05814_b200.errors import ConfigError
 from paper_2511_05814_b200.policies import CacheState, PolicyKind, policy_step, warm_state
 from paper_2511_05814_b200.traces import ActivationTrace, ModelShape
@@ -185,15 +186,15 @@ def test_simulate_on_gpu_layer_independence_and_compulsory(rng):
     shape = ModelShape(4, 8, 2)
     acts = np.stack([random_stream(rng, 8, 2, 25) for _ in range(4)], axis=1)
     tr = ActivationTrace(shape, acts)
-    full = sim.simulate(tr, sim.SimConfig(PolicyKind.lru(), 4))
+    full = simulate(tr, SimConfig(PolicyKind.lru(), 4))
     for l in range(4):
-        solo = sim.simulate(tr, sim.SimConfig(PolicyKind.lru(), 4, layers=(l,)))
+        solo = simulate(tr, SimConfig(PolicyKind.lru(), 4, layers=(l,)))
         assert np.array_equal(solo.resident_before[l], full.resident_before[l])
     for pol in ("lru", "lfu", "lfu-aged:0.5:16", "opt"):
-        log = sim.simulate(tr, sim.SimConfig(PolicyKind.parse(pol), 8))
+        log = simulate(tr, SimConfig(PolicyKind.parse(pol), 8))
         for l in range(4):
             assert int(log.miss_counts(l).sum()) == len(np.unique(acts[:, l, :]))
     with pytest.raises(ConfigError):
-        sim.simulate(tr, sim.SimConfig(PolicyKind.lru(), 1))
+        simulate(tr, SimConfig(PolicyKind.lru(), 1))
     with pytest.raises(ConfigError):
-        sim.simulate(tr, sim.SimConfig(PolicyKind.lru(), 4, layers=(7,)))
+        simulate(tr, SimConfig(PolicyKind.lru(), 4, layers=(7,)))

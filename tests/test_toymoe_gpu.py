@@ -8,7 +8,7 @@ import pytest
 
 import oracle
 from conftest import GOLDEN
-from paper_2511_05814_b200 import simulate as sim
+from paper_2511_05814_b200.simulate import SimConfig, simulate
 from paper_2511_05814_b200.engine import EngineConfig, OffloadEngine
 from paper_2511_05814_b200.errors import ConfigError
 from paper_2511_05814_b200.metrics import cache_metrics, speculation_metrics
@@ -104,7 +104,7 @@ def test_run_model_t1_byte_identical_traces():
     assert format_trace(spec) == (GOLDEN / "toy_t1" / "speculation.jsonl").read_bytes()
     for pol in ("lru", "lfu"):
         for C in (2, 4):
-            log = sim.simulate(act, sim.SimConfig(PolicyKind.parse(pol), C))
+            log = simulate(act, SimConfig(PolicyKind.parse(pol), C))
             assert format_event_log(log) == (GOLDEN / "toy_t1" / f"events_{pol}_c{C}.jsonl").read_bytes()
 
 
