@@ -132,6 +132,10 @@ typedef struct {
   int64_t chunk_bytes;    /* transfer chunk size (prefetch cancellation granularity) */
   int32_t prefetch_depth; /* max prefetch chunks in flight on the copy stream */
   int32_t device;
+  int32_t rms_norm;       /* 1: RMSNorm (unit scale) of h' before gate and experts, as in
+                             Mixtral; keeps the SwiGLU residual stream finite.  0: reference
+                             toy semantics (no norm, toymoe.py:138-146). */
+  float rms_eps;          /* RMSNorm epsilon (Mixtral: 1e-5) */
 } moe_engine_config;
 
 typedef struct {
@@ -158,8 +162,10 @@ moe_status moe_engine_set_dense_f32(moe_engine* eng, int32_t layer, const float*
 /* One toy expert from host memory, reference layout: w1, w2 (d, d) f32 (toymoe.py:82-83). */
 moe_status moe_engine_set_toy_expert_f32(moe_engine* eng, int32_t layer, int32_t expert,
                                          const float* w1, const float* w2);
-/* Synthetic Mixtral-shaped weights from the counter-hash generator (moe_hash_weights). */
-moe_status moe_engine_init_random(moe_engine* eng, uint64_t seed);
+/* Synthetic Mixtral-shaped weights from the counter-hash generator (moe_hash_weights).
+ * gate_bias_std is the reference's expert-imbalance knob (toymoe `skew`, toymoe.py:75);
+ * see DESIGN.md for the value the bench uses. */
+moe_status moe_engine_init_random(moe_engine* eng, uint64_t seed, float gate_bias_std);
 /* Host view of one expert block in the pinned store ([w1 | w3 | w2] bf16 or [W1t | W2t] f32). */
 moe_status moe_engine_expert_host_ptr(moe_engine* eng, int32_t layer, int32_t expert,
                                       void** ptr, int64_t* bytes);
@@ -170,6 +176,25 @@ moe_status moe_engine_dense_host(moe_engine* eng, int32_t layer, void* mixing, f
 
 /* Reset every per-layer cache to the cold state (policies.warm_state, policies.py:133-137). */
 moe_status moe_engine_reset(moe_engine* eng);
+
+/* Switch policy / cache size / prefetch mode and reset to cold caches.  cache_size may not
+ * exceed the capacity given at creation; prefetch needs the engine to have been created
+ * with prefetch != OFF (staging buffers are allocated then). */
+moe_status moe_engine_set_mode(moe_engine* eng, int32_t policy, double decay_factor,
+                               int64_t decay_period, int32_t cache_size, int32_t prefetch);
+
+/* Per-launch CUDA-event timing of the engine's kernels (recorded on the compute stream). */
+typedef struct {
+  double mix_ms, gate_ms, ffn_ms, finalize_ms; /* summed device time per kernel class */
+  int64_t mix_launches, gate_launches, ffn_launches, finalize_launches;
+  int64_t ffn_expert_runs; /* expert FFN executions (K per step) covered by ffn_ms */
+  double ffn_active_ms;     /* device time of the FFN launches that processed >= 1 expert */
+  int64_t ffn_active_bytes; /* weight bytes those launches streamed (device-counted) */
+  int64_t ffn_active_launches;
+} moe_kernel_times;
+moe_status moe_engine_profile(moe_engine* eng, int32_t enable);
+/* Resolves outstanding events (synchronises) and returns the running totals. */
+moe_status moe_engine_kernel_times(moe_engine* eng, moe_kernel_times* out);
 
 /* Decode T tokens: h_in_dev (T, d) f32 device, h_out_dev (T, d) f32 device.
  * Token t's step records go to ring position (tokens_done + t) % max_tokens. */
@@ -189,6 +214,17 @@ moe_status moe_engine_records(moe_engine* eng, int64_t t0, int64_t T, int64_t* a
                               float* probs);
 
 moe_status moe_engine_stats(moe_engine* eng, moe_stats* out);
+
+/* ---- kernel microbenchmark (tuning aid) --------------------------------------------- */
+
+/* Times one decode GEMV kernel in isolation on synthetic resident weights (4 rotating
+ * weight sets, so consecutive iterations miss in L2).  kernel: 0 stream mix, 1 stream up,
+ * 2 stream down (bulk-copy pipelines), 3/4/5 the same ops as plain LDG kernels.
+ * stage_kb / max_stages / grid / rpb (rows per block: 8, 4, 2) tune the stream kernels;
+ * 0 selects the engine's default for each. */
+moe_status moe_microbench_gemv(int32_t kernel, int32_t d, int32_t f, int32_t experts,
+                               int32_t stage_kb, int32_t max_stages, int32_t grid, int32_t rpb,
+                               int32_t iters, float* ms_per_iter, int64_t* bytes_per_iter);
 
 /* ---- synthetic weights (counter hash), shared with oracle/weights.c ---------------- */
 

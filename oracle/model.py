@@ -18,7 +18,7 @@ import math
 
 import numpy as np
 
-from .native import hash_fill, replay_policy
+from .native import hash_fill, hash_fill_t, replay_policy
 
 
 def softmax(z: np.ndarray) -> np.ndarray:
@@ -98,49 +98,53 @@ def _std(n: int) -> float:
 
 class MixtralRef:
     """CPU decode of the Mixtral-shaped engine path (SwiGLU experts) on identical inputs.
+    With rms_norm, h' is RMS-normalised (unit scale, as Mixtral's pre-MoE norm) before the
+    gate and the experts; the residual adds to the un-normalised h'.
 
     Weights are regenerated from the counter hash exactly as the engine's init_random:
-    mixing [d_out, d_in] bf16 std 1; gate_w [E, d] f32 std 1/sqrt(d); gate_b [E] f32 std 1;
+    mixing [d_out, d_in] bf16 std 1; gate_w [E, d] f32 std 1/sqrt(d); gate_b [E] f32 std
+    gate_bias_std (default 0.25, engine.DEFAULT_GATE_BIAS_STD);
     w1, w3 [f, d] bf16 std 1/sqrt(d); w2 [d, f] bf16 std 1/sqrt(f).
     """
 
     def __init__(self, L, E, K, d, f, alpha, seed=42, layout="ref", threads=None,
-                 layers=None, renormalize=False):
+                 layers=None, renormalize=False, rms_norm=False, rms_eps=1e-5,
+                 gate_bias_std=0.25):
         self.L, self.E, self.K, self.d, self.f = L, E, K, d, f
         self.alpha, self.seed, self.layout, self.threads = alpha, seed, layout, threads
         self.renormalize = renormalize
+        self.rms_norm, self.rms_eps = rms_norm, rms_eps
+        self.gate_bias_std = gate_bias_std
         self.dtype = np.float64 if layout == "ref" else np.float32
         self.layers = list(range(L)) if layers is None else list(layers)
         self._dense = {}
         self._experts = {}
 
-    def _fill(self, tid, std, n):
+    def _matrix(self, tid, std, rows, cols):
+        """A bf16 synthetic [rows, cols] (device layout) matrix, widened; in the reference
+        layout the transpose (cols, rows) so that `h @ W` is the device's `W_dev h`."""
         if self.layout == "ref":
-            return hash_fill(self.seed, tid, std, n, "f64", self.threads)
-        return hash_fill(self.seed, tid, std, n, "f64", self.threads).astype(np.float32)
+            return hash_fill_t(self.seed, tid, std, rows, cols, "f64", self.threads)
+        return hash_fill(self.seed, tid, std, rows * cols, "f32w", self.threads).reshape(rows, cols)
 
     def dense(self, l):
         if l not in self._dense:
             d, E = self.d, self.E
-            M = self._fill(_tid(1, l), 1.0, d * d).reshape(d, d)             # [out, in]
+            M = self._matrix(_tid(1, l), 1.0, d, d)
             gw = hash_fill(self.seed, _tid(2, l), _std(d), E * d, "f32", self.threads)
-            gb = hash_fill(self.seed, _tid(3, l), 1.0, E, "f32", self.threads)
+            gb = hash_fill(self.seed, _tid(3, l), self.gate_bias_std, E, "f32", self.threads)
             gw = gw.astype(self.dtype).reshape(E, d)
-            gb = gb.astype(self.dtype)
-            if self.layout == "ref":   # x @ M_ref with M_ref = M_dev^T, W_ref = Wg_dev^T
-                M, gw = np.ascontiguousarray(M.T), np.ascontiguousarray(gw.T)
-            self._dense[l] = (M, gw, gb)
+            if self.layout == "ref":   # x @ W_ref with W_ref = Wg_dev^T
+                gw = np.ascontiguousarray(gw.T)
+            self._dense[l] = (M, gw, gb.astype(self.dtype))
         return self._dense[l]
 
     def expert(self, l, e):
         if (l, e) not in self._experts:
             d, f = self.d, self.f
-            w1 = self._fill(_tid(4, l, e, 1), _std(d), f * d).reshape(f, d)
-            w3 = self._fill(_tid(4, l, e, 2), _std(d), f * d).reshape(f, d)
-            w2 = self._fill(_tid(4, l, e, 3), _std(f), f * d).reshape(d, f)
-            if self.layout == "ref":
-                w1, w3, w2 = (np.ascontiguousarray(w.T) for w in (w1, w3, w2))
-            self._experts[(l, e)] = (w1, w3, w2)
+            self._experts[(l, e)] = (self._matrix(_tid(4, l, e, 1), _std(d), f, d),
+                                     self._matrix(_tid(4, l, e, 2), _std(d), f, d),
+                                     self._matrix(_tid(4, l, e, 3), _std(f), d, f))
         return self._experts[(l, e)]
 
     def materialize(self, layers=None):
@@ -155,10 +159,12 @@ class MixtralRef:
         x = x.astype(self.dtype)
         if self.layout == "ref":
             h = x + self.alpha * (x @ M)
-            z = h @ gw + gb
+            hn = self._norm(h)
+            z = hn @ gw + gb
         else:
             h = x + np.float32(self.alpha) * (M @ x)
-            z = gw @ h + gb
+            hn = self._norm(h)
+            z = gw @ hn + gb
         if not np.isfinite(z).all():
             raise FloatingPointError("gate logits are not finite")
         sel = np.lexsort((np.arange(self.E), -z))[: self.K]
@@ -168,19 +174,26 @@ class MixtralRef:
         for e, pe in zip(sel, weights):
             w1, w3, w2 = self.expert(l, e)
             if self.layout == "ref":
-                a1, a3 = h @ w1, h @ w3
+                a1, a3 = hn @ w1, hn @ w3
                 act = a1 / (1.0 + np.exp(-a1)) * a3
                 out = out + pe * (act @ w2)
             else:
-                a1, a3 = w1 @ h, w3 @ h
+                a1, a3 = w1 @ hn, w3 @ hn
                 act = a1 / (np.float32(1.0) + np.exp(-a1)) * a3
                 out = out + pe * (w2 @ act)
         return out, sel, p, z
 
+    def _norm(self, h: np.ndarray) -> np.ndarray:
+        """Mixtral's RMSNorm with unit scale (engine rms_norm=1); identity otherwise."""
+        if not self.rms_norm:
+            return h
+        return h / np.sqrt(np.mean(h * h) + self.rms_eps)
+
     def guess(self, h: np.ndarray, l: int):
         """Reference-definition guess for layer l from the previous layer's output."""
         _, gw, gb = self.dense(l)
-        z = h.astype(self.dtype) @ gw + gb if self.layout == "ref" else gw @ h.astype(self.dtype) + gb
+        hn = self._norm(h.astype(self.dtype))
+        z = hn @ gw + gb if self.layout == "ref" else gw @ hn + gb
         return np.sort(np.lexsort((np.arange(self.E), -z))[: self.K])
 
     @staticmethod

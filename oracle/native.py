@@ -29,6 +29,10 @@ def oracle_lib() -> ctypes.CDLL:
     lib.oracle_hash_fill.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_float,
                                      ctypes.c_int64, ctypes.c_int, P, ctypes.c_int]
     lib.oracle_hash_fill.restype = None
+    lib.oracle_hash_fill_t.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_float,
+                                       ctypes.c_int64, ctypes.c_int64, ctypes.c_int, P,
+                                       ctypes.c_int]
+    lib.oracle_hash_fill_t.restype = None
     _lib = lib
     return lib
 
@@ -49,9 +53,21 @@ def replay_policy(acts, num_experts, capacity, policy, decay_factor, decay_perio
 
 def hash_fill(seed: int, tensor_id: int, std: float, n: int, kind: str = "bf16",
               threads: int | None = None) -> np.ndarray:
-    """Synthetic weights: kind 'bf16' (uint16 bits), 'f32', or 'f64' (bf16 widened)."""
-    code, dtype = {"bf16": (0, np.uint16), "f32": (1, np.float32), "f64": (2, np.float64)}[kind]
+    """Synthetic weights: kind 'bf16' (uint16 bits), 'f32', 'f64' / 'f32w' (bf16 widened)."""
+    code, dtype = {"bf16": (0, np.uint16), "f32": (1, np.float32), "f64": (2, np.float64),
+                   "f32w": (3, np.float32)}[kind]
     out = np.empty(n, dtype)
     oracle_lib().oracle_hash_fill(seed, tensor_id, std, n, code, out.ctypes.data,
                                   threads or os.cpu_count() or 1)
+    return out
+
+
+def hash_fill_t(seed: int, tensor_id: int, std: float, rows: int, cols: int, kind: str = "f64",
+                threads: int | None = None) -> np.ndarray:
+    """Transpose (cols, rows) of the logical (rows, cols) synthetic tensor; kind 'f64' / 'f32w'
+    (bf16-rounded, widened) or 'f32'."""
+    code, dtype = {"f32": (1, np.float32), "f64": (2, np.float64), "f32w": (3, np.float32)}[kind]
+    out = np.empty((cols, rows), dtype)
+    oracle_lib().oracle_hash_fill_t(seed, tensor_id, std, rows, cols, code, out.ctypes.data,
+                                    threads or os.cpu_count() or 1)
     return out

@@ -42,17 +42,18 @@ static void* run(void* p) {
     float v = value_at(j->key, (uint64_t)i, j->c);
     if (j->kind == 0) ((uint16_t*)j->out)[i] = to_bf16(v);
     else if (j->kind == 1) ((float*)j->out)[i] = v;
-    else {  /* bf16-rounded, widened to double: the oracle's "identical inputs" */
+    else {  /* bf16-rounded, widened: the oracle's "identical inputs" (2: f64, 3: f32) */
       uint32_t u = (uint32_t)to_bf16(v) << 16;
       float f;
       memcpy(&f, &u, 4);
-      ((double*)j->out)[i] = (double)f;
+      if (j->kind == 2) ((double*)j->out)[i] = (double)f;
+      else ((float*)j->out)[i] = f;
     }
   }
   return NULL;
 }
 
-/* kind 0: bf16 bits, 1: f32, 2: bf16 widened to f64 */
+/* kind 0: bf16 bits, 1: f32, 2: bf16 widened to f64, 3: bf16 widened to f32 */
 void oracle_hash_fill(uint64_t seed, uint64_t tensor_id, float std, int64_t n, int kind,
                       void* out, int threads) {
   if (threads < 1) threads = 1;
@@ -67,6 +68,47 @@ void oracle_hash_fill(uint64_t seed, uint64_t tensor_id, float std, int64_t n, i
     if (lo > hi) lo = hi;
     jobs[t] = (job_t){key, c, lo, hi, out, kind};
     pthread_create(&th[t], NULL, run, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+}
+
+/* The transpose of the logical (rows, cols) tensor: out[c * rows + r] = value(r * cols + c),
+ * widened bf16 -> f64 (kind 2) or f32 (kind 1).  Lets the CPU baseline hold every matrix in
+ * the reference's (d_in, d_out) layout without a separate transpose pass. */
+typedef struct { uint64_t key; float c; int64_t rows, cols, c0, c1; void* out; int kind; } tjob_t;
+
+static void* run_t(void* p) {
+  tjob_t* j = (tjob_t*)p;
+  for (int64_t cc = j->c0; cc < j->c1; ++cc)
+    for (int64_t r = 0; r < j->rows; ++r) {
+      float v = value_at(j->key, (uint64_t)(r * j->cols + cc), j->c);
+      if (j->kind == 1) {
+        ((float*)j->out)[cc * j->rows + r] = v;
+      } else {
+        uint32_t u = (uint32_t)to_bf16(v) << 16;
+        float f;
+        memcpy(&f, &u, 4);
+        if (j->kind == 2) ((double*)j->out)[cc * j->rows + r] = (double)f;
+        else ((float*)j->out)[cc * j->rows + r] = f;  /* kind 3: bf16 widened to f32 */
+      }
+    }
+  return NULL;
+}
+
+void oracle_hash_fill_t(uint64_t seed, uint64_t tensor_id, float std, int64_t rows, int64_t cols,
+                        int kind, void* out, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 64) threads = 64;
+  pthread_t th[64];
+  tjob_t jobs[64];
+  const uint64_t key = sm(seed ^ sm(tensor_id));
+  const float c = scale_of(std);
+  const int64_t per = (cols + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    int64_t c0 = t * per, c1 = c0 + per < cols ? c0 + per : cols;
+    if (c0 > c1) c0 = c1;
+    jobs[t] = (tjob_t){key, c, rows, cols, c0, c1, out, kind};
+    pthread_create(&th[t], NULL, run_t, &jobs[t]);
   }
   for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
 }

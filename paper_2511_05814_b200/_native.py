@@ -28,7 +28,8 @@ EXPORTED = (
     "moe_engine_create", "moe_engine_destroy", "moe_engine_set_dense_f32",
     "moe_engine_set_toy_expert_f32", "moe_engine_init_random", "moe_engine_expert_host_ptr",
     "moe_engine_dense_host", "moe_engine_reset", "moe_engine_decode", "moe_engine_sync",
-    "moe_engine_records", "moe_engine_stats",
+    "moe_engine_records", "moe_engine_stats", "moe_engine_set_mode", "moe_engine_profile",
+    "moe_engine_kernel_times", "moe_microbench_gemv",
     "moe_hash_weights_bf16", "moe_hash_weights_f32",
 )
 
@@ -43,7 +44,7 @@ class EngineConfigC(ctypes.Structure):
         ("prefetch", ctypes.c_int32), ("renormalize", ctypes.c_int32),
         ("record_speculation", ctypes.c_int32), ("max_tokens", ctypes.c_int32),
         ("chunk_bytes", ctypes.c_int64), ("prefetch_depth", ctypes.c_int32),
-        ("device", ctypes.c_int32),
+        ("device", ctypes.c_int32), ("rms_norm", ctypes.c_int32), ("rms_eps", ctypes.c_float),
     ]
 
 
@@ -52,6 +53,14 @@ class StatsC(ctypes.Structure):
         "tokens", "steps", "hits", "misses", "h2d_bytes", "demand_bytes", "prefetch_bytes",
         "prefetch_issued", "prefetch_used", "prefetch_wasted_bytes", "expert_bytes")] + [
         ("copy_busy_ms", ctypes.c_double)]
+
+
+class KernelTimesC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("mix_ms", "gate_ms", "ffn_ms", "finalize_ms")] + [
+        (n, ctypes.c_int64) for n in ("mix_launches", "gate_launches", "ffn_launches",
+                                      "finalize_launches", "ffn_expert_runs")] + [
+        ("ffn_active_ms", ctypes.c_double), ("ffn_active_bytes", ctypes.c_int64),
+        ("ffn_active_launches", ctypes.c_int64)]
 
 
 _P = ctypes.c_void_p
@@ -71,7 +80,7 @@ _SIGNATURES = {
     "moe_engine_destroy": ([_P], _I32),
     "moe_engine_set_dense_f32": ([_P, _I32, _P, _P, _P], _I32),
     "moe_engine_set_toy_expert_f32": ([_P, _I32, _I32, _P, _P], _I32),
-    "moe_engine_init_random": ([_P, _U64], _I32),
+    "moe_engine_init_random": ([_P, _U64, _F32], _I32),
     "moe_engine_expert_host_ptr": ([_P, _I32, _I32, ctypes.POINTER(_P), ctypes.POINTER(_I64)], _I32),
     "moe_engine_dense_host": ([_P, _I32, _P, _P, _P], _I32),
     "moe_engine_reset": ([_P], _I32),
@@ -79,6 +88,11 @@ _SIGNATURES = {
     "moe_engine_sync": ([_P], _I32),
     "moe_engine_records": ([_P, _I64, _I64, _P, _P, _P, _P, _P], _I32),
     "moe_engine_stats": ([_P, ctypes.POINTER(StatsC)], _I32),
+    "moe_engine_set_mode": ([_P, _I32, _F64, _I64, _I32, _I32], _I32),
+    "moe_engine_profile": ([_P, _I32], _I32),
+    "moe_engine_kernel_times": ([_P, ctypes.POINTER(KernelTimesC)], _I32),
+    "moe_microbench_gemv": ([_I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
+                             ctypes.POINTER(_F32), ctypes.POINTER(_I64)], _I32),
     "moe_hash_weights_bf16": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
     "moe_hash_weights_f32": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
 }

@@ -19,11 +19,13 @@
 // the thread trickles speculative-prefetch chunks onto the copy stream.
 #include "engine_kernels.cuh"
 #include "hash.cuh"
+#include "stream_gemv.cuh"
 
 #include <sys/mman.h>
 #include <unistd.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -117,7 +119,9 @@ struct moe_engine {
   float* gate_b = nullptr;       // [L][E]
   LayerState* states = nullptr;  // [L]
   StepRecord* ring = nullptr;    // [max_tokens][L]
-  float *h_in = nullptr, *h_mid = nullptr, *y = nullptr, *act = nullptr;
+  float *h_in = nullptr, *h_mid = nullptr, *h_norm = nullptr, *y = nullptr, *act = nullptr;
+  float* gate_part = nullptr;   // [148][3E + 2] partial gate logits from the mixing GEMV
+  float* norm_scale = nullptr;  // 1 / rms(h') of the current layer
   float *x_pad = nullptr, *out_pad = nullptr;  // padded token staging when d % 8 != 0
   int* err = nullptr;
   DeviceStats* dstats = nullptr;
@@ -144,6 +148,19 @@ struct moe_engine {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_events;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> free_events;
   bool debug = getenv("MOE_DEBUG") != nullptr;
+  unsigned long long* gate_phase_ns = nullptr;  // MOE_GATE_TIMING: per-phase gate kernel time
+  int cap_C = 0;  // policy slots allocated per layer (set_mode may use fewer)
+
+  // kernel profiling (moe_engine_profile): per-layer event sextets, resolved lazily
+  bool profiling = false;
+  std::vector<cudaEvent_t> prof_free;
+  std::vector<std::array<cudaEvent_t, 3>> prof_pending;  // before mix, after mix, after gate
+  std::vector<std::array<cudaEvent_t, 2>> prof_ffn;      // around each expert-FFN launch group
+  long long* prof_bytes_dev = nullptr;                    // per FFN launch: bytes streamed
+  static constexpr int kProfSlots = 1 << 16;
+  std::vector<std::array<cudaEvent_t, 2>> prof_final;
+  std::vector<int> prof_pending_k;
+  moe_kernel_times ktimes{};
 };
 
 namespace {
@@ -188,11 +205,27 @@ cudaEvent_t take_sync_event(moe_engine* g) {
   return e;
 }
 
-// Forward one mailbox entry: cancels, demand copies, new prefetch jobs.  Returns through
-// *has_demand whether the compute stream must wait for the copy stream.
-moe_status handle_mail(moe_engine* g, const MailRecord& m, bool* has_demand) {
+// Demand copy order and events of one step: misses in ascending expert id, each copied as
+// part A (w1|w3 or the toy W1t) then part B (w2 / W2t), each part followed by an event the
+// compute stream waits on before that expert's up / down kernel.
+struct DemandPlan {
+  int n = 0;
+  cudaEvent_t ev_a[kMaxK], ev_b[kMaxK];
+};
+
+long long part_a_bytes(const moe_engine* g) {
+  return g->bf16 ? 2ll * g->f * g->dpad * 2 : static_cast<long long>(g->dpad) * g->dpad * 4;
+}
+
+cudaEvent_t next_order_event(moe_engine* g) {
+  return g->order_events[g->order_next++ % g->order_events.size()];
+}
+
+// Forward one mailbox entry: cancels, demand copies, new prefetch jobs.
+moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
   const long long chunk = g->cfg.chunk_bytes;
   const long long nchunks = (g->expert_bytes + chunk - 1) / chunk;
+  const long long split = part_a_bytes(g);
   // cancelled staging buffers of this step's layer: stop issuing their remaining chunks
   for (int i = 0; i < m.n_cancel; ++i)
     for (auto& j : g->jobs)
@@ -201,34 +234,48 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, bool* has_demand) {
         std::lock_guard<std::mutex> lk(g->stats_mu);
         g->st.prefetch_wasted_bytes += std::min(j.next_chunk * chunk, g->expert_bytes);
       }
+  // demand entries in ascending expert id (the order the phase-1 kernels enumerate misses)
+  int order[kMaxK];
+  for (int i = 0; i < m.n_demand; ++i) order[i] = i;
+  std::sort(order, order + m.n_demand,
+            [&](int x, int y) { return m.demand_expert[x] < m.demand_expert[y]; });
   long long demand = 0;
   std::pair<cudaEvent_t, cudaEvent_t> tev{nullptr, nullptr};
   if (m.n_demand > 0) {
     tev = take_timing_events(g);
     MOE_CUDA(cudaEventRecord(tev.first, g->copy_stream));
   }
-  for (int i = 0; i < m.n_demand; ++i) {
+  plan->n = m.n_demand;
+  for (int k = 0; k < m.n_demand; ++k) {
+    const int i = order[k];
     const int e = m.demand_expert[i], b = m.demand_buf[i];
     long long from = 0;
     if (m.demand_adopt[i]) {
       for (auto& j : g->jobs)
         if (!j.cancelled && !j.adopted && j.layer == m.layer && j.buf == b && j.expert == e) {
           j.adopted = true;
-          from = j.next_chunk;
+          from = std::min(j.next_chunk * chunk, g->expert_bytes);
           break;
         }
       std::lock_guard<std::mutex> lk(g->stats_mu);
       g->st.prefetch_used += 1;
     }
-    for (long long c = from; c < nchunks; ++c) {
-      const long long off = c * chunk, n = std::min(chunk, g->expert_bytes - off);
-      moe_status s = issue_copy(g, m.layer, b, e, off, n);
-      if (s != MOE_OK) return s;
-      demand += n;
+    // part A: [from, split), then event; part B: [max(from, split), end), then event
+    if (from < split) {
+      TRY(issue_copy(g, m.layer, b, e, from, split - from));
+      demand += split - from;
     }
+    plan->ev_a[k] = next_order_event(g);
+    MOE_CUDA(cudaEventRecord(plan->ev_a[k], g->copy_stream));
+    const long long fb = std::max(from, split);
+    if (fb < g->expert_bytes) {
+      TRY(issue_copy(g, m.layer, b, e, fb, g->expert_bytes - fb));
+      demand += g->expert_bytes - fb;
+    }
+    plan->ev_b[k] = next_order_event(g);
+    MOE_CUDA(cudaEventRecord(plan->ev_b[k], g->copy_stream));
   }
   if (m.n_demand > 0) MOE_CUDA(cudaEventRecord(tev.second, g->copy_stream));
-  *has_demand = m.n_demand > 0;
   for (int i = 0; i < m.n_prefetch; ++i)
     g->jobs.push_back(PrefetchJob{m.layer + 1, m.prefetch_buf[i], m.prefetch_expert[i], 0,
                                   nchunks, false, false});
@@ -326,6 +373,64 @@ moe_status await_mail(moe_engine* g, long long seq, cudaStream_t compute, MailRe
   return MOE_OK;
 }
 
+cudaEvent_t take_prof_event(moe_engine* g) {
+  if (!g->prof_free.empty()) {
+    cudaEvent_t e = g->prof_free.back();
+    g->prof_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Fold every recorded event group into the running totals (caller synchronised).
+void resolve_profile(moe_engine* g) {
+  moe_kernel_times& k = g->ktimes;
+  for (size_t i = 0; i < g->prof_pending.size(); ++i) {
+    auto& e = g->prof_pending[i];
+    k.mix_ms += elapsed(e[0], e[1]);
+    k.gate_ms += elapsed(e[1], e[2]);
+    k.mix_launches += 1;
+    k.gate_launches += 1;
+    k.ffn_expert_runs += g->prof_pending_k[i];
+    for (int q = 0; q < 3; ++q) g->prof_free.push_back(e[q]);
+  }
+  std::vector<long long> bytes(g->prof_ffn.size(), 0);
+  if (g->bf16 && g->prof_bytes_dev && !bytes.empty())
+    cudaMemcpy(bytes.data(), g->prof_bytes_dev, sizeof(long long) * bytes.size(),
+               cudaMemcpyDeviceToHost);
+  for (size_t i = 0; i < g->prof_ffn.size(); ++i) {
+    auto& e = g->prof_ffn[i];
+    const float ms = elapsed(e[0], e[1]);
+    k.ffn_ms += ms;
+    k.ffn_launches += 1;
+    if (!g->bf16 || bytes[i] > 0) {
+      k.ffn_active_ms += ms;
+      k.ffn_active_bytes += bytes[i];
+      k.ffn_active_launches += 1;
+    }
+    g->prof_free.push_back(e[0]);
+    g->prof_free.push_back(e[1]);
+  }
+  g->prof_ffn.clear();
+  for (auto& e : g->prof_final) {
+    k.finalize_ms += elapsed(e[0], e[1]);
+    k.finalize_launches += 1;
+    g->prof_free.push_back(e[0]);
+    g->prof_free.push_back(e[1]);
+  }
+  g->prof_pending.clear();
+  g->prof_pending_k.clear();
+  g->prof_final.clear();
+}
+
 moe_status alloc_device(void** p, size_t n) {
   MOE_CUDA(cudaMalloc(p, n));
   MOE_CUDA(cudaMemset(*p, 0, n));
@@ -360,6 +465,7 @@ moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) 
   MOE_REQUIRE(c.prefetch == MOE_PREFETCH_OFF || c.prefetch == MOE_PREFETCH_EARLY,
               "unknown prefetch mode %d", c.prefetch);
   MOE_REQUIRE(c.max_tokens >= 1, "max_tokens must be >= 1");
+  MOE_REQUIRE(c.rms_norm == 0 || (c.rms_norm == 1 && c.rms_eps > 0.f), "bad rms_norm settings");
   MOE_REQUIRE(c.expert_kind != MOE_EXPERT_SWIGLU_BF16 ||
                   (c.hidden_dim % 8 == 0 && c.ffn_dim >= 8 && c.ffn_dim % 8 == 0),
               "SwiGLU experts need hidden_dim and ffn_dim multiples of 8");
@@ -368,7 +474,7 @@ moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) 
 
   auto* g = new moe_engine();
   g->cfg = c;
-  if (g->cfg.chunk_bytes <= 0) g->cfg.chunk_bytes = 16ll << 20;
+  if (g->cfg.chunk_bytes <= 0) g->cfg.chunk_bytes = 4ll << 20;
   if (g->cfg.prefetch_depth <= 0) g->cfg.prefetch_depth = 2;
   g->device = c.device;
   g->d = c.hidden_dim;
@@ -384,6 +490,7 @@ moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) 
   }
   g->S = c.prefetch ? c.top_k : 0;
   g->NB = c.cache_size + g->S;
+  g->cap_C = c.cache_size;
   const moe_status st = create_resources(g);
   if (st != MOE_OK) {
     const std::string msg = moe_last_error();
@@ -411,6 +518,9 @@ moe_status create_resources(moe_engine* g) {
   TRY(alloc_device(reinterpret_cast<void**>(&g->ring), sizeof(StepRecord) * L * static_cast<size_t>(c.max_tokens)));
   TRY(alloc_device(reinterpret_cast<void**>(&g->h_in), sizeof(float) * D));
   TRY(alloc_device(reinterpret_cast<void**>(&g->h_mid), sizeof(float) * 2 * D));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->h_norm), sizeof(float) * D));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->gate_part), sizeof(float) * 148 * (3 * kMaxE + 2)));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->norm_scale), sizeof(float)));
   TRY(alloc_device(reinterpret_cast<void**>(&g->y), sizeof(float) * K * D));
   TRY(alloc_device(reinterpret_cast<void**>(&g->act), sizeof(float) * K * g->f));
   TRY(alloc_device(reinterpret_cast<void**>(&g->err), sizeof(int)));
@@ -434,7 +544,7 @@ moe_status create_resources(moe_engine* g) {
     MOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     g->sync_events.push_back(e);
   }
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < 4 * kMaxK; ++i) {
     cudaEvent_t e = nullptr;
     MOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     g->order_events.push_back(e);
@@ -445,6 +555,8 @@ moe_status create_resources(moe_engine* g) {
     MOE_CUDA(cudaEventCreate(&b));
     g->free_events.push_back({a, b});
   }
+  if (getenv("MOE_GATE_TIMING"))
+    TRY(alloc_device(reinterpret_cast<void**>(&g->gate_phase_ns), 8 * sizeof(unsigned long long)));
   TRY(g->store.allocate(static_cast<size_t>(L) * E * g->expert_bytes));
   reset_states_kernel<<<L, 64>>>(g->states, L, g->NB);
   MOE_LAUNCHED();
@@ -472,8 +584,25 @@ moe_status moe_engine_destroy(moe_engine* g) {
   for (auto e : g->sync_events) cudaEventDestroy(e);
   for (auto e : g->prefetch_inflight) cudaEventDestroy(e);
   for (auto e : g->order_events) cudaEventDestroy(e);
+  for (auto e : g->prof_free) cudaEventDestroy(e);
+  for (auto& a : g->prof_pending)
+    for (auto e : a) cudaEventDestroy(e);
+  for (auto& a : g->prof_final)
+    for (auto e : a) cudaEventDestroy(e);
+  for (auto& a : g->prof_ffn)
+    for (auto e : a) cudaEventDestroy(e);
+  if (g->prof_bytes_dev) cudaFree(g->prof_bytes_dev);
+  if (g->gate_phase_ns) {
+    unsigned long long h[8] = {};
+    cudaMemcpy(h, g->gate_phase_ns, sizeof(h), cudaMemcpyDeviceToHost);
+    if (h[5])
+      fprintf(stderr, "[moe] gate kernel phases (avg ns over %llu): state+rms %llu, logits %llu, "
+              "route+policy %llu, bookkeeping %llu, writeback+mail %llu\n", h[5], h[0] / h[5],
+              h[1] / h[5], h[2] / h[5], h[3] / h[5], h[4] / h[5]);
+    cudaFree(g->gate_phase_ns);
+  }
   void* dev[] = {g->pool, g->mixing, g->gate_w, g->gate_b, g->states, g->ring, g->h_in,
-                 g->h_mid, g->y, g->act, g->err, g->dstats, g->x_pad, g->out_pad};
+                 g->h_mid, g->h_norm, g->gate_part, g->norm_scale, g->y, g->act, g->err, g->dstats, g->x_pad, g->out_pad};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (g->mail_h) cudaFreeHost(g->mail_h);
@@ -527,7 +656,7 @@ moe_status moe_engine_set_toy_expert_f32(moe_engine* g, int32_t layer, int32_t e
   return MOE_OK;
 }
 
-moe_status moe_engine_init_random(moe_engine* g, uint64_t seed) {
+moe_status moe_engine_init_random(moe_engine* g, uint64_t seed, float gate_bias_std) {
   MOE_REQUIRE(g, "null engine");
   MOE_REQUIRE(g->bf16, "init_random synthesises Mixtral-shaped (SwiGLU bf16) weights");
   MOE_CUDA(cudaSetDevice(g->device));
@@ -541,7 +670,7 @@ moe_status moe_engine_init_random(moe_engine* g, uint64_t seed) {
     TRY(launch_hash_bf16(seed, tensor_id(kTMixing, l, 0, 0), 1.f, 1ll * d * d, M, s));
     TRY(launch_hash_f32(seed, tensor_id(kTGateW, l, 0, 0), sd, 1ll * E * d,
                         g->gate_w + static_cast<size_t>(l) * E * d, s));
-    TRY(launch_hash_f32(seed, tensor_id(kTGateB, l, 0, 0), 1.f, E,
+    TRY(launch_hash_f32(seed, tensor_id(kTGateB, l, 0, 0), gate_bias_std, E,
                         g->gate_b + static_cast<size_t>(l) * E, s));
   }
   // experts: generate into a free HBM buffer, then copy down into the pinned store
@@ -627,18 +756,89 @@ moe_status moe_engine_decode(moe_engine* g, const float* h_in_dev, int64_t T, fl
     attrs = true;
   }
   MOE_REQUIRE(mix_smem <= 200 * 1024 && down_smem <= 200 * 1024, "hidden/ffn dims too large");
-  auto launch_ffn = [&](FfnParams fp) -> moe_status {
-    if (g->bf16) {
-      swiglu_up_kernel<<<dim3(up_grid, K), 256, up_smem, s>>>(fp);
-      MOE_LAUNCHED();
-      down_kernel<true><<<dim3(down_grid, K), 256, down_smem, s>>>(fp);
-      MOE_LAUNCHED();
-    } else {
-      toy_up_kernel<<<dim3(up_grid, K), 256, up_smem, s>>>(fp);
-      MOE_LAUNCHED();
-      down_kernel<false><<<dim3(down_grid, K), 256, down_smem, s>>>(fp);
-      MOE_LAUNCHED();
+  // bf16 path: bulk-copy streaming GEMVs (stream_gemv.cuh)
+  StreamGeom gmix{}, gup{}, gdown{};
+  if (g->bf16) {
+    gmix = stream_geometry(kModeMix, D, g->f);
+    gup = stream_geometry(kModeUp, D, g->f);
+    gdown = stream_geometry(kModeDown, D, g->f);
+    MOE_REQUIRE(gmix.ncb && gup.ncb && gdown.ncb,
+                "bf16 engine needs hidden_dim and ffn_dim multiples of 256");
+  }
+  const int grid_mix = stream_grid(1), grid_ffn = stream_grid(K);
+  // one expert-FFN launch group: phase 0 = hits, 1 = misses; only = -1 all, i = i-th miss
+  if (g->profiling && !g->prof_bytes_dev)
+    MOE_CUDA(cudaMalloc(&g->prof_bytes_dev, sizeof(long long) * moe_engine::kProfSlots));
+  auto prof_slot = [&]() -> long long* {
+    if (!g->profiling || g->prof_ffn.size() >= static_cast<size_t>(moe_engine::kProfSlots)) return nullptr;
+    return g->prof_bytes_dev + g->prof_ffn.size();
+  };
+  auto prof_begin = [&](std::array<cudaEvent_t, 2>& ev) -> moe_status {
+    if (g->profiling) {
+      if (g->prof_ffn.size() >= static_cast<size_t>(moe_engine::kProfSlots)) {
+        MOE_CUDA(cudaStreamSynchronize(s));
+        resolve_profile(g);
+      }
+      ev = {take_prof_event(g), take_prof_event(g)};
+      MOE_CUDA(cudaEventRecord(ev[0], s));
     }
+    return MOE_OK;
+  };
+  auto prof_end = [&](std::array<cudaEvent_t, 2>& ev) -> moe_status {
+    if (g->profiling) {
+      MOE_CUDA(cudaEventRecord(ev[1], s));
+      g->prof_ffn.push_back(ev);
+    }
+    return MOE_OK;
+  };
+  auto launch_ffn = [&](FfnParams fp, int only) -> moe_status {
+    if (g->bf16) {
+      StreamParams sp{};
+      sp.d = D;
+      sp.f = g->f;
+      sp.K = K;
+      sp.xin = fp.h_mid;
+      sp.xscale = c.rms_norm ? g->norm_scale : nullptr;
+      sp.rec = fp.rec;
+      sp.state = fp.state;
+      sp.pool = fp.pool;
+      sp.expert_bytes = fp.expert_bytes;
+      sp.phase = fp.phase;
+      sp.only = only;
+      sp.act = fp.act;
+      sp.yout = fp.y;
+      sp.prof_bytes = prof_slot();
+      const int grid = only >= 0 ? stream_grid(1) : grid_ffn;
+      MOE_CUDA(launch_stream<kModeUp>(gup, grid, sp, s));
+      MOE_LAUNCHED();
+      return MOE_OK;
+    }
+    toy_up_kernel<<<dim3(up_grid, K), 256, up_smem, s>>>(fp);
+    MOE_LAUNCHED();
+    return MOE_OK;
+  };
+  auto launch_down = [&](FfnParams fp, int only) -> moe_status {
+    if (g->bf16) {
+      StreamParams sp{};
+      sp.d = D;
+      sp.f = g->f;
+      sp.K = K;
+      sp.rec = fp.rec;
+      sp.state = fp.state;
+      sp.pool = fp.pool;
+      sp.expert_bytes = fp.expert_bytes;
+      sp.phase = fp.phase;
+      sp.only = only;
+      sp.act = fp.act;
+      sp.yout = fp.y;
+      sp.prof_bytes = prof_slot();
+      const int grid = only >= 0 ? stream_grid(1) : grid_ffn;
+      MOE_CUDA(launch_stream<kModeDown>(gdown, grid, sp, s));
+      MOE_LAUNCHED();
+      return MOE_OK;
+    }
+    down_kernel<false><<<dim3(down_grid, K), 256, down_smem, s>>>(fp);
+    MOE_LAUNCHED();
     return MOE_OK;
   };
   for (int64_t t = 0; t < T; ++t) {
@@ -656,44 +856,111 @@ moe_status moe_engine_decode(moe_engine* g, const float* h_in_dev, int64_t T, fl
       MixParams mp{l == 0 ? x : nullptr, hm_prev, g->y, l == 0 ? nullptr : trec + (l - 1),
                    static_cast<char*>(g->mixing) + static_cast<size_t>(l) * D * D * msz,
                    c.mixing_scale, D, K, g->h_in, hm};
-      if (g->bf16)
-        mix_kernel<true><<<mix_grid, 256, mix_smem, s>>>(mp);
-      else
+      std::array<cudaEvent_t, 3> pe{};
+      if (g->profiling) {
+        for (auto& e : pe) e = take_prof_event(g);
+        MOE_CUDA(cudaEventRecord(pe[0], s));
+      }
+      if (g->bf16) {
+        StreamParams sp{};
+        sp.d = D;
+        sp.f = g->f;
+        sp.K = K;
+        sp.x = mp.x;
+        sp.prev_mid = mp.prev_mid;
+        sp.y = mp.y;
+        sp.prev = mp.prev;
+        sp.M = static_cast<const uint16_t*>(mp.M);
+        sp.alpha = mp.alpha;
+        sp.h_in = mp.h_in;
+        sp.h_mid = mp.h_mid;
+        sp.gate_w = g->gate_w + static_cast<size_t>(l) * c.num_experts * D;
+        sp.gate_w_next = (c.prefetch == MOE_PREFETCH_EARLY && l + 1 < L)
+                             ? g->gate_w + static_cast<size_t>(l + 1) * c.num_experts * D
+                             : nullptr;
+        sp.E = c.num_experts;
+        sp.do_guess = c.record_speculation && l >= 1;
+        sp.part = g->gate_part;
+        MOE_CUDA(launch_stream<kModeMix>(gmix, grid_mix, sp, s));
+      } else {
         mix_kernel<false><<<mix_grid, 256, mix_smem, s>>>(mp);
+      }
       MOE_LAUNCHED();
+      if (g->profiling) MOE_CUDA(cudaEventRecord(pe[1], s));
       GateParams gp{hm, g->h_in, g->gate_w, g->gate_b, l, L, c.num_experts, K, D, c.cache_size,
-                    g->NB, c.policy, c.decay_factor, c.decay_period, c.record_speculation,
+                    c.cache_size + (c.prefetch ? g->S : 0), c.policy, c.decay_factor, c.decay_period, c.record_speculation,
                     c.prefetch, c.renormalize, seq, g->states, trec + l, g->mail_d,
-                    g->ctl_d, g->err, g->dstats};
-      gate_cache_kernel<<<1, 256, 0, s>>>(gp);
+                    g->ctl_d, g->err, g->dstats, c.rms_norm, c.rms_eps, g->h_norm,
+                    g->gate_phase_ns, g->bf16 ? g->gate_part : nullptr, grid_mix, g->norm_scale};
+      if (c.num_experts <= 8)
+        gate_cache_kernel<8><<<1, kGateThreads, 0, s>>>(gp);
+      else
+        gate_cache_kernel<kMaxE><<<1, kGateThreads, 0, s>>>(gp);
       MOE_LAUNCHED();
-      FfnParams fp{hm, trec + l, g->states + l,
+      if (g->profiling) MOE_CUDA(cudaEventRecord(pe[2], s));
+      FfnParams fp{(c.rms_norm && !g->bf16) ? g->h_norm : hm, trec + l, g->states + l,
                    g->pool + static_cast<long long>(l) * g->NB * g->expert_bytes, g->expert_bytes,
                    D, g->f, K, 0, g->act, g->y};
-      TRY(launch_ffn(fp));  // phase 0: experts that hit run while the misses are fetched
+      // phase 0: experts that hit run while the misses are fetched
+      std::array<cudaEvent_t, 2> fev{};
+      TRY(prof_begin(fev));
+      TRY(launch_ffn(fp, -1));
+      TRY(prof_end(fev));
+      TRY(prof_begin(fev));
+      TRY(launch_down(fp, -1));
+      TRY(prof_end(fev));
       // forward the device's decision for this step (lockstep, one step behind the GPU)
       MailRecord m;
       TRY(await_mail(g, seq, s, &m));
       if (g->debug)
         fprintf(stderr, "[moe] seq=%lld layer=%d demand=%d cancel=%d prefetch=%d\n", m.seq,
                 m.layer, m.n_demand, m.n_cancel, m.n_prefetch);
-      bool has_demand = false;
-      TRY(handle_mail(g, m, &has_demand));
+      DemandPlan plan;
+      TRY(handle_mail(g, m, &plan));
       g->next_mail = seq + 1;
       g->ctl_h->consumed = seq + 1;
-      if (has_demand) {
-        cudaEvent_t ev = g->order_events[g->order_next++ % g->order_events.size()];
-        MOE_CUDA(cudaEventRecord(ev, g->copy_stream));
-        MOE_CUDA(cudaStreamWaitEvent(s, ev, 0));
-      }
+      // phase 1: each missed expert's up runs once its w1|w3 landed (overlapping its w2
+      // copy), its down once w2 landed (overlapping the next expert's copy)
       fp.phase = 1;
-      TRY(launch_ffn(fp));
+      if (g->bf16) {
+        for (int i = 0; i < plan.n; ++i) {
+          MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_a[i], 0));
+          TRY(prof_begin(fev));
+          TRY(launch_ffn(fp, i));
+          TRY(prof_end(fev));
+          MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_b[i], 0));
+          TRY(prof_begin(fev));
+          TRY(launch_down(fp, i));
+          TRY(prof_end(fev));
+        }
+      } else if (plan.n > 0) {
+        MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_b[plan.n - 1], 0));
+        TRY(prof_begin(fev));
+        TRY(launch_ffn(fp, -1));
+        TRY(prof_end(fev));
+        TRY(prof_begin(fev));
+        TRY(launch_down(fp, -1));
+        TRY(prof_end(fev));
+      }
+      if (g->profiling) {
+        g->prof_pending.push_back(pe);
+        g->prof_pending_k.push_back(K);
+      }
     }
     float* out = h_out_dev + t * d;
     float* dst = D != d ? g->out_pad : out;
+    std::array<cudaEvent_t, 2> fe{};
+    if (g->profiling) {
+      fe = {take_prof_event(g), take_prof_event(g)};
+      MOE_CUDA(cudaEventRecord(fe[0], s));
+    }
     finalize_kernel<<<(D + 255) / 256, 256, 0, s>>>(g->h_mid + ((L - 1) & 1) * D, g->y,
                                                    trec + (L - 1), K, D, dst);
     MOE_LAUNCHED();
+    if (g->profiling) {
+      MOE_CUDA(cudaEventRecord(fe[1], s));
+      g->prof_final.push_back(fe);
+    }
     if (D != d)
       MOE_CUDA(cudaMemcpyAsync(out, g->out_pad, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
   }
@@ -749,6 +1016,43 @@ moe_status moe_engine_records(moe_engine* g, int64_t t0, int64_t T, int64_t* act
       }
     }
   }
+  return MOE_OK;
+}
+
+moe_status moe_engine_set_mode(moe_engine* g, int32_t policy, double decay_factor,
+                               int64_t decay_period, int32_t cache_size, int32_t prefetch) {
+  MOE_REQUIRE(g, "null engine");
+  MOE_REQUIRE(policy == MOE_P_LRU || policy == MOE_P_LFU || policy == MOE_P_LFU_AGED,
+              "the live engine runs lru/lfu/lfu-aged; opt needs the future and is offline-only");
+  MOE_REQUIRE(policy != MOE_P_LFU_AGED || (decay_period >= 1 && decay_factor > 0.0 &&
+                                            decay_factor <= 1.0),
+              "bad lfu-aged parameters");
+  MOE_REQUIRE(cache_size >= g->cfg.top_k && cache_size <= g->cap_C,
+              "cache_size must be in [top_k=%d, allocated %d], got %d", g->cfg.top_k, g->cap_C,
+              cache_size);
+  MOE_REQUIRE(prefetch == MOE_PREFETCH_OFF || (prefetch == MOE_PREFETCH_EARLY && g->S > 0),
+              "prefetch needs staging buffers: create the engine with prefetch enabled");
+  TRY(moe_engine_reset(g));
+  g->cfg.policy = policy;
+  g->cfg.decay_factor = decay_factor;
+  g->cfg.decay_period = decay_period;
+  g->cfg.cache_size = cache_size;
+  g->cfg.prefetch = prefetch;
+  return MOE_OK;
+}
+
+moe_status moe_engine_profile(moe_engine* g, int32_t enable) {
+  MOE_REQUIRE(g, "null engine");
+  g->profiling = enable != 0;
+  return MOE_OK;
+}
+
+moe_status moe_engine_kernel_times(moe_engine* g, moe_kernel_times* out) {
+  MOE_REQUIRE(g && out, "null argument");
+  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_CUDA(cudaDeviceSynchronize());
+  resolve_profile(g);
+  *out = g->ktimes;
   return MOE_OK;
 }
 

@@ -13,7 +13,7 @@ constexpr int kMailRing = 256;
 
 // Per-layer cache state, device resident (policies.CacheState, policies.py:104-117, in the
 // array form kernels.replay_policy keeps, kernels.py:70-75) plus the HBM buffer table.
-struct LayerState {
+struct __align__(16) LayerState {
   uint32_t resident;                 // bit e: expert e is policy-resident
   int32_t pad0;
   long long step;                    // tokens this layer has processed (CacheState.step)
@@ -39,14 +39,18 @@ struct StepRecord {
 // Mailbox entry the gate kernel hands to the host transfer thread (mapped pinned memory).
 // The device decides everything (which experts, which buffers); the host only forwards
 // the copies to the copy engine.
-struct MailRecord {
+struct __align__(16) MailRecord {
   long long seq;
   int32_t layer, n_demand, n_cancel, n_prefetch, need_ack, pad;
   int32_t demand_expert[kMaxK], demand_buf[kMaxK], demand_adopt[kMaxK];
   int32_t cancel_buf[kMaxK];
   int32_t prefetch_expert[kMaxK], prefetch_buf[kMaxK];
   volatile long long ready;  // seq + 1 once the fields above are visible
+  long long pad2;
 };
+static_assert(sizeof(MailRecord) % 16 == 0 && offsetof(MailRecord, ready) % 16 == 0,
+              "mail records are copied with 16-byte stores");
+static_assert(sizeof(LayerState) % 16 == 0, "layer state is copied with 16-byte stores");
 
 struct DeviceStats {
   unsigned long long hits, misses;
@@ -65,6 +69,17 @@ struct HostControl {
 __device__ __forceinline__ void stage_planes(const float* __restrict__ x, int n, float4* pa,
                                              float4* pb) {
   for (int i = threadIdx.x; i < n / 8; i += blockDim.x) {
+    const float4* src = reinterpret_cast<const float4*>(x) + 2 * i;
+    pa[i] = src[0];
+    pb[i] = src[1];
+  }
+}
+
+// Same, with an explicit participating thread count (warp-specialised kernels).
+__device__ __forceinline__ void stage_planes_n(const float* __restrict__ x, int n, float4* pa,
+                                               float4* pb, int nthreads) {
+#pragma unroll 4
+  for (int i = threadIdx.x; i < n / 8; i += nthreads) {
     const float4* src = reinterpret_cast<const float4*>(x) + 2 * i;
     pa[i] = src[0];
     pb[i] = src[1];
@@ -152,6 +167,21 @@ __device__ __forceinline__ float combine_elem(const float* h_mid, const float* y
   return v;
 }
 
+// Vectorised combine of 4 consecutive elements (float4 index i4): same arithmetic order.
+__device__ __forceinline__ float4 combine4(const float* h_mid, const float* y,
+                                           const StepRecord* rec, int K, int d, int i4) {
+  float4 v = reinterpret_cast<const float4*>(h_mid)[i4];
+  for (int j = 0; j < K; ++j) {
+    const float p = rec->prob[j];
+    const float4 yj = reinterpret_cast<const float4*>(y + static_cast<size_t>(j) * d)[i4];
+    v.x = __fadd_rn(v.x, __fmul_rn(p, yj.x));
+    v.y = __fadd_rn(v.y, __fmul_rn(p, yj.y));
+    v.z = __fadd_rn(v.z, __fmul_rn(p, yj.z));
+    v.w = __fadd_rn(v.w, __fmul_rn(p, yj.w));
+  }
+  return v;
+}
+
 // ---- K0: mixing GEMV, h' = h + alpha * (h @ M) (toymoe.py:140) ---------------------------
 struct MixParams {
   const float* x;          // layer 0 input row (token input), else nullptr
@@ -207,7 +237,22 @@ struct GateParams {
   HostControl* ctl;        // device view of the mapped control block
   int* err;
   DeviceStats* stats;
+  int rms_norm;            // 1: RMSNorm (no learned scale) before gate and experts
+  float rms_eps;
+  float* h_norm;           // out: expert input (h' / rms(h') when rms_norm)
+  unsigned long long* phase_ns;  // optional diagnostics: accumulated ns per kernel phase [8]
+  // fused path (bf16 engine): the mixing GEMV's CTAs already reduced their rows into
+  // part[c][job] (jobs: 3E logits + sum h'^2 + sum h_in^2); the gate sums them in CTA order
+  const float* part;
+  int nparts;
+  float* norm_scale;       // out: 1/rms(h') (or 1) for the up projection's input staging
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // top-k over lanes (value z on lane e < E), selection order: z desc, ties -> lower id.
 __device__ __forceinline__ void warp_topk(float z, bool valid, int K, int* out) {
@@ -237,36 +282,136 @@ __device__ __forceinline__ void sort_small(int* v, int n) {
   }
 }
 
-__global__ void __launch_bounds__(256) gate_cache_kernel(GateParams p) {
+// Copy `n` bytes (multiple of 16) with the calling threads (tid in [0, nthreads)).
+__device__ __forceinline__ void copy16(void* dst, const void* src, int n, int tid, int nthreads) {
+  int4* d = static_cast<int4*>(dst);
+  const int4* s = static_cast<const int4*>(src);
+  for (int i = tid; i < n / 16; i += nthreads) d[i] = s[i];
+}
+
+constexpr int kGateThreads = 512;  // d=4096: two float4 columns per thread, loads all in flight
+
+template <int EM>  // compile-time bound on E (8 for Mixtral) so the accumulators stay in registers
+__global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) {
   __shared__ float z[3][kMaxE];
+  __shared__ float red[2][kGateThreads / 32];
+  __shared__ __align__(16) LayerState sS, sS1;   // working copies of this / next layer's state
+  __shared__ __align__(16) MailRecord sM;
+  __shared__ long long s_consumed;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const bool do_guess = p.record_spec && p.layer >= 1;
   const bool do_prefetch = p.prefetch == MOE_PREFETCH_EARLY && p.layer + 1 < p.L;
-  // logits: job q = (which, expert); which 0 = route(h'), 1 = guess(h_in), 2 = early(h' , l+1)
-  const int njobs = 3 * p.E;
-  for (int q = warp; q < njobs; q += nwarps) {
-    const int which = q / p.E, e = q % p.E;
-    if ((which == 1 && !do_guess) || (which == 2 && !do_prefetch)) continue;
-    const int gl = which == 2 ? p.layer + 1 : p.layer;
-    const float* w = p.gate_w + (static_cast<size_t>(gl) * p.E + e) * p.d;
-    const float* v = which == 1 ? p.h_in : p.h_mid;
-    float acc = 0.f;
-    for (int i = lane; i < p.d / 4; i += 32) {
-      const float4 a = reinterpret_cast<const float4*>(w)[i];
-      const float4 b = reinterpret_cast<const float4*>(v)[i];
+  const unsigned long long t0 = p.phase_ns ? gtimer() : 0;
+  // stage the cache state in shared memory (its latency overlaps the logits below)
+  copy16(&sS, &p.states[p.layer], sizeof(LayerState), threadIdx.x, blockDim.x);
+  if (do_prefetch) copy16(&sS1, &p.states[p.layer + 1], sizeof(LayerState), threadIdx.x, blockDim.x);
+  if (threadIdx.x == 0) s_consumed = p.ctl->consumed;
+  // RMSNorm scales of h' (route, early guess, experts) and of h_in (reference guess)
+  float inv_mid = 1.f, inv_in = 1.f;
+  const int njob = 3 * p.E + 2;
+  if (p.part) {
+    // fused: sum the per-CTA partials, one warp per job, lanes over CTAs, then a fixed
+    // shuffle tree (the same order every call: deterministic)
+    for (int q = warp; q < njob; q += nwarps) {
+      float acc = 0.f;
+      for (int c = lane; c < p.nparts; c += 32) acc += p.part[c * njob + q];
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        if (q < 3 * p.E) z[q / p.E][q % p.E] = acc;
+        else red[q - 3 * p.E][0] = acc;
+      }
+    }
+    __syncthreads();
+    if (p.rms_norm) {
+      inv_mid = rsqrtf(red[0][0] / p.d + p.rms_eps);
+      inv_in = rsqrtf(red[1][0] / p.d + p.rms_eps);
+    }
+    if (threadIdx.x < 3 * p.E) {
+      const int which = threadIdx.x / p.E, e = threadIdx.x % p.E;
+      const int gl = which == 2 ? p.layer + 1 : p.layer;
+      if ((which == 1 && do_guess) || (which == 2 && do_prefetch) || which == 0)
+        z[which][e] = z[which][e] * (which == 1 ? inv_in : inv_mid) + p.gate_b[gl * p.E + e];
+    }
+    if (threadIdx.x == 0 && p.norm_scale) *p.norm_scale = inv_mid;
+  } else {
+    if (p.rms_norm) {
+      float sm = 0.f, si = 0.f;
+      for (int i = threadIdx.x; i < p.d; i += blockDim.x) {
+        const float a = p.h_mid[i];
+        sm = fmaf(a, a, sm);
+        if (do_guess) {
+          const float b = p.h_in[i];
+          si = fmaf(b, b, si);
+        }
+      }
+      sm = warp_sum(sm);
+      si = warp_sum(si);
+      if (lane == 0) {
+        red[0][warp] = sm;
+        red[1][warp] = si;
+      }
+      __syncthreads();
+      float tm = 0.f, ti = 0.f;
+      for (int w = 0; w < nwarps; ++w) {
+        tm += red[0][w];
+        ti += red[1][w];
+      }
+      inv_mid = rsqrtf(tm / p.d + p.rms_eps);
+      inv_in = rsqrtf(ti / p.d + p.rms_eps);
+      for (int i = threadIdx.x; i < p.d; i += blockDim.x) p.h_norm[i] = p.h_mid[i] * inv_mid;
+    }
+    if (threadIdx.x == 0 && p.norm_scale) *p.norm_scale = 1.f;
+  }
+  const unsigned long long t1 = p.phase_ns ? gtimer() : 0;
+  if (!p.part) {
+  // logits: job q = (which, expert); which 0 = route(h'), 1 = guess(h_in), 2 = early(h', l+1).
+  // Every thread owns a fixed float4 column slice, so all of its loads are independent and
+  // in flight together (the kernel is latency-, not bandwidth-, bound); partial sums are
+  // reduced per job through shared memory in a fixed order.
+  __shared__ float part[3 * EM][kGateThreads / 32];
+  const int nv = p.d / 4;  // float4 columns
+  float accs[3 * EM];
+#pragma unroll
+  for (int q = 0; q < 3 * EM; ++q) accs[q] = 0.f;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    const float4 hm = reinterpret_cast<const float4*>(p.h_mid)[i];
+    const float4 hi = do_guess ? reinterpret_cast<const float4*>(p.h_in)[i] : hm;
+#pragma unroll
+    for (int q = 0; q < 3 * EM; ++q) {
+      const int which = q / EM, e = q % EM;
+      if (e >= p.E) continue;
+      if ((which == 1 && !do_guess) || (which == 2 && !do_prefetch)) continue;
+      const int gl = which == 2 ? p.layer + 1 : p.layer;
+      const float4 a = reinterpret_cast<const float4*>(p.gate_w + (static_cast<size_t>(gl) * p.E + e) * p.d)[i];
+      const float4 b = which == 1 ? hi : hm;
+      float acc = accs[q];
       acc = fmaf(a.x, b.x, acc);
       acc = fmaf(a.y, b.y, acc);
       acc = fmaf(a.z, b.z, acc);
       acc = fmaf(a.w, b.w, acc);
+      accs[q] = acc;
     }
-    acc = warp_sum(acc);
-    if (lane == 0) z[which][e] = acc + p.gate_b[gl * p.E + e];
+  }
+#pragma unroll
+  for (int q = 0; q < 3 * EM; ++q) {
+    const float v = warp_sum(accs[q]);
+    if (lane == 0) part[q][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3 * EM && (threadIdx.x % EM) < p.E) {
+    const int q = threadIdx.x, which = q / EM, e = q % EM;
+    const int gl = which == 2 ? p.layer + 1 : p.layer;
+    float acc = 0.f;
+    for (int w = 0; w < nwarps; ++w) acc += part[q][w];
+    z[which][e] = acc * (which == 1 ? inv_in : inv_mid) + p.gate_b[gl * p.E + e];
+  }
   }
   __syncthreads();
   if (warp != 0) return;
+  const unsigned long long t2 = p.phase_ns ? gtimer() : 0;
 
   const bool valid = lane < p.E;
-  LayerState& S = p.states[p.layer];
+  LayerState& S = sS;
   StepRecord* rec = p.rec;
   // -- route: finiteness (toymoe.py:109-110), softmax over all E (toymoe.py:93-96) --
   const float zr = valid ? z[0][lane] : 0.f;
@@ -328,106 +473,121 @@ __global__ void __launch_bounds__(256) gate_cache_kernel(GateParams p) {
     warp_topk(ze, valid && fe, p.K, pf);
     sort_small(pf, p.K);
   }
-  if (lane != 0) return;
-
-  // -- record --
-  for (int j = 0; j < p.K; ++j) {
-    rec->sel[j] = sel[j];
-    rec->prob[j] = psel[j];
-    rec->acts[j] = acts[j];
-    rec->guess[j] = do_guess ? gs[j] : -1;
-  }
-  rec->rb = rb;
-  rec->ev = ev;
-  rec->flags = flags;
-  if (flags) atomicOr(p.err, static_cast<int>(flags));
-
-  MailRecord* mr = p.mail + (p.seq % kMailRing);
-  int nd = 0, nc = 0, np = 0;
-  if (finite && ok) {
-    S.resident = res_after;
-    S.step = t + 1;
-    int hits = 0;
-    for (int j = 0; j < p.K; ++j) hits += (rb >> acts[j]) & 1u;
-    atomicAdd(&p.stats->hits, static_cast<unsigned long long>(hits));
-    atomicAdd(&p.stats->misses, static_cast<unsigned long long>(p.K - hits));
-    // release buffers of evicted experts (their bytes stay until overwritten)
-    for (int e = 0; e < p.E; ++e)
-      if ((ev >> e) & 1u) {
-        const int b = S.buf_of[e];
-        if (b >= 0) S.buf_policy[b] = 0;
-        S.buf_of[e] = -1;
-      }
-    // misses whose expert was prefetched for exactly this step adopt the staging buffer
+  MailRecord& mr = sM;
+  const unsigned long long t3 = p.phase_ns ? gtimer() : 0;
+  if (lane == 0) {
+    // -- record --
     for (int j = 0; j < p.K; ++j) {
-      const int e = acts[j];
-      if ((rb >> e) & 1u) continue;
-      for (int b = 0; b < p.NB; ++b)
-        if (S.buf_stage_seq[b] == p.seq && S.buf_expert[b] == e && !S.buf_policy[b]) {
-          S.buf_policy[b] = 1;
-          S.buf_of[e] = b;
-          S.buf_stage_seq[b] = -1;
-          mr->demand_expert[nd] = e;
-          mr->demand_buf[nd] = b;
-          mr->demand_adopt[nd] = 1;
-          ++nd;
-          break;
+      rec->sel[j] = sel[j];
+      rec->prob[j] = psel[j];
+      rec->acts[j] = acts[j];
+      rec->guess[j] = do_guess ? gs[j] : -1;
+    }
+    rec->rb = rb;
+    rec->ev = ev;
+    rec->flags = flags;
+    if (flags) atomicOr(p.err, static_cast<int>(flags));
+    int nd = 0, nc = 0, np = 0;
+    if (finite && ok) {
+      S.resident = res_after;
+      S.step = t + 1;
+      int hits = 0;
+      for (int j = 0; j < p.K; ++j) hits += (rb >> acts[j]) & 1u;
+      atomicAdd(&p.stats->hits, static_cast<unsigned long long>(hits));
+      atomicAdd(&p.stats->misses, static_cast<unsigned long long>(p.K - hits));
+      // release buffers of evicted experts (their bytes stay until overwritten)
+      for (int e = 0; e < p.E; ++e)
+        if ((ev >> e) & 1u) {
+          const int b = S.buf_of[e];
+          if (b >= 0) S.buf_policy[b] = 0;
+          S.buf_of[e] = -1;
         }
-    }
-    // the remaining staged buffers of this step were wrong guesses: cancel them
-    for (int b = 0; b < p.NB; ++b)
-      if (S.buf_stage_seq[b] == p.seq) {
-        S.buf_stage_seq[b] = -1;
-        mr->cancel_buf[nc++] = b;
-      }
-    // fresh demand misses take the lowest free buffer
-    for (int j = 0; j < p.K; ++j) {
-      const int e = acts[j];
-      if (((rb >> e) & 1u) || S.buf_of[e] >= 0) continue;
-      int pick = -1;
-      for (int b = 0; b < p.NB && pick < 0; ++b)
-        if (!S.buf_policy[b]) pick = b;
-      S.buf_policy[pick] = 1;
-      S.buf_expert[pick] = e;
-      S.buf_of[e] = pick;
-      mr->demand_expert[nd] = e;
-      mr->demand_buf[nd] = pick;
-      mr->demand_adopt[nd] = 0;
-      ++nd;
-    }
-    // speculative prefetch of layer l+1's guesses that are not resident there
-    if (do_prefetch) {
-      LayerState& S1 = p.states[p.layer + 1];
+      // misses whose expert was prefetched for exactly this step adopt the staging buffer
       for (int j = 0; j < p.K; ++j) {
-        const int g = pf[j];
-        if (g < 0 || g >= p.E || S1.buf_of[g] >= 0) continue;
+        const int e = acts[j];
+        if ((rb >> e) & 1u) continue;
+        for (int b = 0; b < p.NB; ++b)
+          if (S.buf_stage_seq[b] == p.seq && S.buf_expert[b] == e && !S.buf_policy[b]) {
+            S.buf_policy[b] = 1;
+            S.buf_of[e] = b;
+            S.buf_stage_seq[b] = -1;
+            mr.demand_expert[nd] = e;
+            mr.demand_buf[nd] = b;
+            mr.demand_adopt[nd] = 1;
+            ++nd;
+            break;
+          }
+      }
+      // the remaining staged buffers of this step were wrong guesses: cancel them
+      for (int b = 0; b < p.NB; ++b)
+        if (S.buf_stage_seq[b] == p.seq) {
+          S.buf_stage_seq[b] = -1;
+          mr.cancel_buf[nc++] = b;
+        }
+      // fresh demand misses take the lowest free buffer
+      for (int j = 0; j < p.K; ++j) {
+        const int e = acts[j];
+        if (((rb >> e) & 1u) || S.buf_of[e] >= 0) continue;
         int pick = -1;
         for (int b = 0; b < p.NB && pick < 0; ++b)
-          if (!S1.buf_policy[b] && S1.buf_stage_seq[b] != p.seq + 1) pick = b;
-        if (pick < 0) continue;
-        S1.buf_stage_seq[pick] = p.seq + 1;
-        S1.buf_expert[pick] = g;
-        mr->prefetch_expert[np] = g;
-        mr->prefetch_buf[np] = pick;
-        ++np;
+          if (!S.buf_policy[b]) pick = b;
+        S.buf_policy[pick] = 1;
+        S.buf_expert[pick] = e;
+        S.buf_of[e] = pick;
+        mr.demand_expert[nd] = e;
+        mr.demand_buf[nd] = pick;
+        mr.demand_adopt[nd] = 0;
+        ++nd;
+      }
+      // speculative prefetch of layer l+1's guesses that are not resident there
+      if (do_prefetch) {
+        LayerState& S1 = sS1;
+        for (int j = 0; j < p.K; ++j) {
+          const int g = pf[j];
+          if (g < 0 || g >= p.E || S1.buf_of[g] >= 0) continue;
+          int pick = -1;
+          for (int b = 0; b < p.NB && pick < 0; ++b)
+            if (!S1.buf_policy[b] && S1.buf_stage_seq[b] != p.seq + 1) pick = b;
+          if (pick < 0) continue;
+          S1.buf_stage_seq[pick] = p.seq + 1;
+          S1.buf_expert[pick] = g;
+          mr.prefetch_expert[np] = g;
+          mr.prefetch_buf[np] = pick;
+          ++np;
+        }
       }
     }
+    // ring back-pressure: if the host is far behind, make it acknowledge this step
+    mr.seq = p.seq;
+    mr.layer = p.layer;
+    mr.n_demand = nd;
+    mr.n_cancel = nc;
+    mr.n_prefetch = np;
+    mr.need_ack = (p.seq - s_consumed) >= (kMailRing / 2) ? 1 : 0;
   }
-  // ring back-pressure: if the host is far behind, make it acknowledge this step
-  const long long consumed = p.ctl->consumed;
-  const int need_ack = (p.seq - consumed) >= (kMailRing / 2) ? 1 : 0;
-  mr->seq = p.seq;
-  mr->layer = p.layer;
-  mr->n_demand = nd;
-  mr->n_cancel = nc;
-  mr->n_prefetch = np;
-  mr->need_ack = need_ack;
+  __syncwarp();
+  const unsigned long long t4 = p.phase_ns ? gtimer() : 0;
+  // write back the state and post the mail (all lanes, 16-byte stores)
+  copy16(&p.states[p.layer], &sS, sizeof(LayerState), lane, 32);
+  if (do_prefetch) copy16(&p.states[p.layer + 1], &sS1, sizeof(LayerState), lane, 32);
+  MailRecord* dst = p.mail + (p.seq % kMailRing);
+  copy16(dst, &sM, offsetof(MailRecord, ready), lane, 32);
   __threadfence_system();
-  mr->ready = p.seq + 1;
-  p.ctl->gate_done = static_cast<unsigned int>(p.seq + 1);
+  __syncwarp();
+  if (lane == 0) {
+    dst->ready = p.seq + 1;
+    p.ctl->gate_done = static_cast<unsigned int>(p.seq + 1);
+    if (p.phase_ns) {
+      const unsigned long long t5 = gtimer();
+      atomicAdd(&p.phase_ns[0], t1 - t0);
+      atomicAdd(&p.phase_ns[1], t2 - t1);
+      atomicAdd(&p.phase_ns[2], t3 - t2);
+      atomicAdd(&p.phase_ns[3], t4 - t3);
+      atomicAdd(&p.phase_ns[4], t5 - t4);
+      atomicAdd(&p.phase_ns[5], 1ull);
+    }
+  }
 }
-
-
 
 // ---- K3: expert FFN over the selected slots ---------------------------------------------
 struct FfnParams {
@@ -452,7 +612,7 @@ __device__ __forceinline__ bool ffn_phase_match(const FfnParams& p, int j, int* 
 }
 
 // SwiGLU up projection: act[j][r] = silu(w1[r] . x) * (w3[r] . x)
-__global__ void __launch_bounds__(256) swiglu_up_kernel(FfnParams p) {
+static __global__ void __launch_bounds__(256) swiglu_up_kernel(FfnParams p) {
   const int j = blockIdx.y;
   int e;
   if (!ffn_phase_match(p, j, &e)) return;
@@ -473,7 +633,7 @@ __global__ void __launch_bounds__(256) swiglu_up_kernel(FfnParams p) {
 }
 
 // Toy up projection: act[j][r] = tanh(W1t[r] . x)   (toymoe.py:144)
-__global__ void __launch_bounds__(256) toy_up_kernel(FfnParams p) {
+static __global__ void __launch_bounds__(256) toy_up_kernel(FfnParams p) {
   const int j = blockIdx.y;
   int e;
   if (!ffn_phase_match(p, j, &e)) return;
@@ -516,13 +676,13 @@ __global__ void __launch_bounds__(256) down_kernel(FfnParams p) {
 }
 
 // Final layer: h_out = h' + sum_j p_j y_j
-__global__ void finalize_kernel(const float* h_mid, const float* y, const StepRecord* rec, int K,
+static __global__ void finalize_kernel(const float* h_mid, const float* y, const StepRecord* rec, int K,
                                 int d, float* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < d) out[i] = combine_elem(h_mid, y, rec, K, d, i);
 }
 
-__global__ void reset_states_kernel(LayerState* s, int L, int NB) {
+static __global__ void reset_states_kernel(LayerState* s, int L, int NB) {
   const int l = blockIdx.x;
   if (l >= L) return;
   LayerState& S = s[l];

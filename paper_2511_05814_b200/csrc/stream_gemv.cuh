@@ -1,0 +1,413 @@
+// Bulk-copy (TMA engine) streaming GEMV for the bf16 decode path: mixing map (K0),
+// SwiGLU up projection and down projection (K3).
+//
+// Batch-1 decode reads every weight byte exactly once, so these kernels are HBM-bound.
+// Each CTA owns a contiguous band of 8-row blocks of one matrix.  A producer thread streams
+// the band through a ring of shared-memory stages with cp.async.bulk (one bulk copy per
+// row slice, completion counted on an mbarrier, L2 evict-first since nothing re-reads the
+// weights), while 8 consumer warps each reduce one row of the stage against the activation
+// vector kept in shared memory.  Bytes in flight per SM are the ring size (~130-160 KB),
+// independent of register pressure; the grid is sized so every CTA gets the same number of
+// row blocks (HBM, not the SM count, is the bound).
+#pragma once
+#include "engine_kernels.cuh"
+
+namespace moe {
+
+constexpr int kStreamWarps = 8;                       // consumer warps = rows per block
+constexpr int kStreamThreads = (kStreamWarps + 1) * 32; // + one producer warp
+constexpr int kStreamStageBytes = 32 * 1024;
+constexpr int kStreamSmemBudget = 200 * 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// global -> shared bulk copy on the TMA engine, completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kStreamWarps * 32) : "memory");
+}
+
+enum StreamMode { kModeMix = 0, kModeUp = 1, kModeDown = 2 };
+
+struct StreamParams {
+  // geometry
+  int d, f, K, cb, ncb, stages;
+  // MIX
+  const float* x;          // layer-0 token input, else nullptr (then combine prev layer)
+  const float* prev_mid;
+  const float* y;          // previous layer's expert outputs [K][d] (MIX) / output (DOWN)
+  const StepRecord* prev;
+  const uint16_t* M;       // mixing [d][d]
+  float alpha;
+  float* h_in;
+  float* h_mid;
+  // UP / DOWN
+  const float* xin;        // UP: h_norm [d]
+  const StepRecord* rec;
+  const LayerState* state;
+  const char* pool;        // this layer's buffers
+  long long expert_bytes;
+  int phase;
+  int only;                // -1: every expert of the phase; i: just the i-th (ascending id)
+  float* act;              // [K][f]
+  float* yout;             // [K][d]
+  long long* prof_bytes;   // optional: weight bytes this launch streams (profiling)
+  // MIX: per-CTA partial gate logits over the CTA's rows (see GateParams::part)
+  const float* gate_w;     // this layer's gate [E][d]
+  const float* gate_w_next;  // next layer's gate (early speculative guess) or nullptr
+  int E, do_guess;
+  float* part;             // [gridDim.x][3E + 2]
+  // UP: scale applied to xin while staging (1/rms(h') from the gate), or nullptr
+  const float* xscale;
+};
+
+// Which experts this launch covers: (selection slot j, weight block), in ascending expert
+// id.  phase 0 = experts that hit, 1 = experts that missed; `only` >= 0 keeps just the
+// only-th of those (the host orders per-expert launches after that expert's copies).
+__device__ __forceinline__ int stream_active(const StreamParams& p, int* slot, const char** blk) {
+  int n = 0, seen = 0;
+  if (p.rec->flags) return 0;
+  for (int k = 0; k < p.K; ++k) {
+    const int e = p.rec->acts[k];
+    if (e < 0 || e >= kMaxE) continue;
+    const bool hit = (p.rec->rb >> e) & 1u;
+    if ((p.phase == 0) != hit) continue;
+    const int idx = seen++;
+    if (p.only >= 0 && idx != p.only) continue;
+    const int b = p.state->buf_of[e];
+    if (b < 0) continue;
+    int j = 0;
+    while (j < p.K && p.rec->sel[j] != e) ++j;
+    slot[n] = j;
+    blk[n] = p.pool + b * p.expert_bytes;
+    ++n;
+  }
+  return n;
+}
+
+// RPB rows per block, WPR = 8 / RPB warps per row (each reduces a column slice of the row;
+// pairs/quads combine through shared memory in a fixed order).
+template <int MODE, int RPB>
+__global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int NM = MODE == kModeUp ? 2 : 1;  // matrices streamed per row block
+  constexpr int WPR = kStreamWarps / RPB;
+  static_assert(RPB * WPR == kStreamWarps, "RPB must divide the consumer warp count");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int C = MODE == kModeDown ? p.f : p.d;  // row length
+  const int R = MODE == kModeUp ? p.f : p.d;    // rows per matrix
+  const int cb = p.cb, ncb = p.ncb, S = p.stages;
+  const uint32_t slice = static_cast<uint32_t>(cb) * 2;   // bytes per row slice
+  const uint32_t stage_bytes = slice * RPB * NM;
+
+  // ---- which matrix (expert) and which row blocks this CTA owns ----
+  int slot[kMaxK];
+  const char* blk[kMaxK];
+  int n_active = 1;
+  if (MODE != kModeMix) n_active = stream_active(p, slot, blk);
+  if (p.prof_bytes && blockIdx.x == 0 && threadIdx.x == 0)
+    *p.prof_bytes = static_cast<long long>(n_active) * NM * R * C * 2;
+  if (n_active == 0) return;
+  const int a = static_cast<int>((static_cast<long long>(blockIdx.x) * n_active) / gridDim.x);
+  const int c0 = static_cast<int>((static_cast<long long>(a) * gridDim.x + n_active - 1) / n_active);
+  const int c1 = static_cast<int>((static_cast<long long>(a + 1) * gridDim.x + n_active - 1) / n_active);
+  const int nrb = R / RPB;
+  const int my = blockIdx.x - c0, ncta = c1 - c0;
+  const int rb0 = static_cast<int>((static_cast<long long>(my) * nrb) / ncta);
+  const int rb1 = static_cast<int>((static_cast<long long>(my + 1) * nrb) / ncta);
+  const int n_work = (rb1 - rb0) * ncb;
+
+  const uint16_t* W[NM];
+  if constexpr (MODE == kModeMix) {
+    W[0] = p.M;
+  } else if constexpr (MODE == kModeUp) {
+    W[0] = reinterpret_cast<const uint16_t*>(blk[a]);                 // w1 [f][d]
+    W[1] = W[0] + static_cast<size_t>(p.f) * p.d;                      // w3 [f][d]
+  } else {
+    W[0] = reinterpret_cast<const uint16_t*>(blk[a]) + 2 * static_cast<size_t>(p.f) * p.d;  // w2 [d][f]
+  }
+
+  uint8_t* stage_base = smem;
+  float4* pa = reinterpret_cast<float4*>(smem + static_cast<size_t>(S) * stage_bytes);
+  float4* pb = pa + C / 8;
+  float* hs = reinterpret_cast<float*>(pb + C / 8);                 // MIX: layer input
+  float* xch = hs + (MODE == kModeMix ? p.d : 0);                   // [RPB][WPR][NM] partials
+  uint64_t* full = reinterpret_cast<uint64_t*>(xch + 64);
+  uint64_t* empty = full + S;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kStreamWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kStreamWarps) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      for (int it = 0; it < n_work; ++it) {
+        const int s = it % S;
+        if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
+        const int rb = rb0 + it / ncb, c = it % ncb;
+        uint8_t* dst = stage_base + static_cast<size_t>(s) * stage_bytes;
+        mbar_expect_tx(&full[s], stage_bytes);
+#pragma unroll
+        for (int m = 0; m < NM; ++m) {
+          if (ncb == 1) {  // the block's full rows are contiguous: one copy
+            bulk_g2s(dst + m * RPB * slice, W[m] + static_cast<size_t>(rb) * RPB * C,
+                     RPB * slice, &full[s], pol);
+            continue;
+          }
+#pragma unroll
+          for (int r = 0; r < RPB; ++r) {
+            const uint16_t* src = W[m] + static_cast<size_t>(rb * RPB + r) * C +
+                                  static_cast<size_t>(c) * cb;
+            bulk_g2s(dst + (m * RPB + r) * slice, src, slice, &full[s], pol);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: stage the activation vector ----------------
+  if constexpr (MODE == kModeMix) {
+#pragma unroll 4
+    for (int i4 = threadIdx.x; i4 < p.d / 4; i4 += kStreamWarps * 32) {
+      const float4 v = p.x ? reinterpret_cast<const float4*>(p.x)[i4]
+                           : combine4(p.prev_mid, p.y, p.prev, p.K, p.d, i4);
+      reinterpret_cast<float4*>(hs)[i4] = v;
+      if (blockIdx.x == 0) reinterpret_cast<float4*>(p.h_in)[i4] = v;
+    }
+    consumers_sync();
+    stage_planes_n(hs, p.d, pa, pb, kStreamWarps * 32);
+  } else if constexpr (MODE == kModeUp) {
+    stage_planes_n(p.xin, p.d, pa, pb, kStreamWarps * 32);
+    if (p.xscale) {  // RMSNorm applied on the fly: x = h' * (1 / rms(h'))
+      consumers_sync();
+      const float sc = *p.xscale;
+      for (int i = threadIdx.x; i < p.d / 8; i += kStreamWarps * 32) {
+        float4 u = pa[i], v = pb[i];
+        u.x *= sc; u.y *= sc; u.z *= sc; u.w *= sc;
+        v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
+        pa[i] = u;
+        pb[i] = v;
+      }
+    }
+  } else {
+    stage_planes_n(p.act + static_cast<size_t>(slot[a]) * p.f, p.f, pa, pb, kStreamWarps * 32);
+  }
+  consumers_sync();
+
+  const int row_in_block = warp / WPR, part_id = warp % WPR;
+  const int span = cb / WPR;                  // columns this warp reduces per stage
+  const int per_lane = span / 8 / 32;         // uint4 per lane (span multiple of 256)
+  float acc[NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m) acc[m] = 0.f;
+  for (int it = 0; it < n_work; ++it) {
+    const int s = it % S;
+    const int c = it % ncb;
+    mbar_wait(&full[s], (it / S) & 1);
+    const uint8_t* st = stage_base + static_cast<size_t>(s) * stage_bytes;
+    const int col8 = (c * cb + part_id * span) / 8;
+    {
+      const uint4* row0 = reinterpret_cast<const uint4*>(st + row_in_block * slice) + part_id * (span / 8);
+      const uint4* row1 = reinterpret_cast<const uint4*>(st + ((NM - 1) * RPB + row_in_block) * slice) +
+                          part_id * (span / 8);
+      float part0 = 0.f, part1 = 0.f;
+#pragma unroll 4
+      for (int q = 0; q < per_lane; ++q) {
+        const int i = lane + 32 * q;
+        const float4 xa = pa[col8 + i], xb = pb[col8 + i];  // shared by both matrices
+        part0 = dot8_bf16(row0[i], xa, xb, part0);
+        if constexpr (NM == 2) part1 = dot8_bf16(row1[i], xa, xb, part1);
+      }
+      acc[0] += part0;
+      if constexpr (NM == 2) acc[NM - 1] += part1;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (c == ncb - 1) {
+      const int r = (rb0 + it / ncb) * RPB + row_in_block;
+      float v[NM];
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        v[m] = warp_sum(acc[m]);
+        acc[m] = 0.f;
+      }
+      if constexpr (WPR > 1) {
+        // fixed-order combine of the row's column slices (deterministic)
+        if (lane == 0)
+#pragma unroll
+          for (int m = 0; m < NM; ++m) xch[(row_in_block * WPR + part_id) * NM + m] = v[m];
+        asm volatile("bar.sync %0, %1;" ::"r"(2 + row_in_block), "n"(WPR * 32) : "memory");
+        if (part_id == 0 && lane == 0)
+#pragma unroll
+          for (int m = 0; m < NM; ++m) {
+            float t = xch[(row_in_block * WPR) * NM + m];
+            for (int q = 1; q < WPR; ++q) t += xch[(row_in_block * WPR + q) * NM + m];
+            v[m] = t;
+          }
+        asm volatile("bar.sync %0, %1;" ::"r"(2 + row_in_block), "n"(WPR * 32) : "memory");
+      }
+      if (part_id == 0 && lane == 0) {
+        if constexpr (MODE == kModeMix) {
+          p.h_mid[r] = __fadd_rn(hs[r], __fmul_rn(p.alpha, v[0]));
+        } else if constexpr (MODE == kModeUp) {
+          p.act[static_cast<size_t>(slot[a]) * p.f + r] = v[0] / (1.f + expf(-v[0])) * v[NM - 1];
+        } else {
+          p.yout[static_cast<size_t>(slot[a]) * p.d + r] = v[0];
+        }
+      }
+    }
+  }
+  if constexpr (MODE == kModeMix) {
+    if (p.part) {
+      // gate logits fused into the mixing epilogue: this CTA's rows [r0, r1) of
+      //   route  W_l h',  guess  W_l h_in,  early  W_{l+1} h',  and sum h'^2, sum h_in^2
+      consumers_sync();
+      const int r0 = rb0 * RPB, r1 = rb1 * RPB, E = p.E, njob = 3 * E + 2;
+      for (int q = warp; q < njob; q += kStreamWarps) {
+        const int which = q < 3 * E ? q / E : 3, e = q < 3 * E ? q % E : q - 3 * E;
+        float acc = 0.f;
+        if (which == 3) {
+          const float* v = e == 0 ? p.h_mid : hs;
+          for (int r = r0 + lane; r < r1; r += 32) acc = fmaf(v[r], v[r], acc);
+        } else if (!(which == 1 && !p.do_guess) && !(which == 2 && !p.gate_w_next)) {
+          const float* w = (which == 2 ? p.gate_w_next : p.gate_w) + static_cast<size_t>(e) * p.d;
+          const float* v = which == 1 ? hs : p.h_mid;
+          for (int r = r0 + lane; r < r1; r += 32) acc = fmaf(w[r], v[r], acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) p.part[static_cast<size_t>(blockIdx.x) * njob + q] = acc;
+      }
+    }
+  }
+}
+
+// Shared-memory bytes and stage geometry for one stream launch.
+struct StreamGeom {
+  int rpb, cb, ncb, stages;
+  size_t smem;
+};
+
+// Rows per block / column block / ring depth for one mode.  Tuned on B200 with
+// tools/tune_gemv.py: 4 KB+ row slices, 150-200 KB of ring per SM.
+inline StreamGeom stream_geometry_rpb(int mode, int d, int f, int stage_budget, int max_stages,
+                                      int rpb);
+
+inline StreamGeom stream_geometry(int mode, int d, int f, int stage_budget = 0, int max_stages = 6,
+                                  int rpb = 0) {
+  // preferred rows-per-block first, then the always-valid 8 (one warp per row)
+  const int pref = rpb ? rpb : (mode == kModeUp ? 8 : 4);
+  StreamGeom g = stream_geometry_rpb(mode, d, f, stage_budget, max_stages, pref);
+  if (g.ncb == 0 && rpb == 0 && pref != 8) g = stream_geometry_rpb(mode, d, f, stage_budget, max_stages, 8);
+  return g;
+}
+
+inline StreamGeom stream_geometry_rpb(int mode, int d, int f, int stage_budget, int max_stages,
+                                      int rpb) {
+  const int NM = mode == kModeUp ? 2 : 1;
+  const int C = mode == kModeDown ? f : d;
+  if (stage_budget == 0) stage_budget = mode == kModeUp ? 64 * 1024 : 32 * 1024;
+  const int wpr = kStreamWarps / rpb;
+  StreamGeom g{};
+  g.rpb = rpb;
+  // widest column block whose stage fits the budget; each warp's share a multiple of 256
+  g.ncb = 0;
+  for (int n = 1; n <= C / 256; ++n) {
+    if (C % n) continue;
+    const int cb = C / n;
+    if (cb % (256 * wpr)) continue;
+    if (static_cast<long long>(cb) * 2 * rpb * NM <= stage_budget) {
+      g.ncb = n;
+      g.cb = cb;
+      break;
+    }
+  }
+  if (g.ncb == 0) return g;
+  const size_t stage = static_cast<size_t>(g.cb) * 2 * rpb * NM;
+  const size_t fixed = static_cast<size_t>(C) * 4 + (mode == kModeMix ? static_cast<size_t>(d) * 4 : 0) + 64 * 4;
+  if (fixed + 2 * stage + 256 > 227 * 1024) {
+    g.ncb = 0;
+    return g;
+  }
+  int S = static_cast<int>((224 * 1024 - fixed - 256) / stage);
+  S = S < 2 ? 2 : (S > max_stages ? max_stages : S);
+  g.stages = S;
+  g.smem = S * stage + fixed + 2 * S * sizeof(uint64_t);
+  return g;
+}
+
+// Grid: one CTA per SM -- per-SM bulk-copy throughput, not the HBM, limits a partial grid
+// (tools/tune_gemv.py: 74 / 96 / 128 / 148 CTAs -> 3.0 / 3.9 / 5.2 / 5.7 TB/s); a multiple of
+// the expert count so each active expert gets an equal band of CTAs.
+inline int stream_grid(int experts, int sms = 148) { return sms / experts * experts; }
+
+// Launch one stream GEMV with the template instantiation matching the geometry.
+template <int MODE>
+inline cudaError_t launch_stream(const StreamGeom& g, int grid, const StreamParams& sp,
+                                 cudaStream_t s) {
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(stream_gemv_kernel<MODE, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(stream_gemv_kernel<MODE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(stream_gemv_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attrs = true;
+  }
+  StreamParams p = sp;
+  p.cb = g.cb;
+  p.ncb = g.ncb;
+  p.stages = g.stages;
+  if (g.rpb == 8)
+    stream_gemv_kernel<MODE, 8><<<grid, kStreamThreads, g.smem, s>>>(p);
+  else if (g.rpb == 4)
+    stream_gemv_kernel<MODE, 4><<<grid, kStreamThreads, g.smem, s>>>(p);
+  else
+    stream_gemv_kernel<MODE, 2><<<grid, kStreamThreads, g.smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace moe

@@ -27,6 +27,11 @@ from . import _native
 from .errors import ConfigError
 from .policies import OPT, PolicyKind
 
+# Router bias spread of the synthetic Mixtral-shaped models (the reference's `skew` knob).
+# With the RMS-normalised router, 0.25 reproduces the C=4 hit rates the survey / paper report
+# for Mixtral (LRU ~0.55, LFU ~0.58); 1.0 makes routing bias-dominated (hit rate ~0.8).
+DEFAULT_GATE_BIAS_STD = 0.25
+
 
 @dataclass(frozen=True)
 class EngineConfig:
@@ -43,15 +48,17 @@ class EngineConfig:
     renormalize: bool = False            # Mixtral routing (renormalised top-k); ref: False
     record_speculation: bool = True
     max_tokens: int = 4096
-    chunk_bytes: int = 16 << 20
+    chunk_bytes: int = 4 << 20
     prefetch_depth: int = 2
     device: int = 0
+    rms_norm: bool = False               # Mixtral presets: True (RMSNorm before gate/experts)
+    rms_eps: float = 1e-5
 
     @staticmethod
     def mixtral_8x7b(**kw) -> "EngineConfig":
         """Mixtral-8x7B shape (L=32, E=8, K=2, d=4096, f=14336), alpha = 0.1*sqrt(16/d)."""
         base = dict(num_layers=32, num_experts=8, top_k=2, hidden_dim=4096, ffn_dim=14336,
-                    expert_kind="swiglu", mixing_scale=0.1 * math.sqrt(16 / 4096))
+                    expert_kind="swiglu", mixing_scale=0.1 * math.sqrt(16 / 4096), rms_norm=True)
         base.update(kw)
         return EngineConfig(**base)
 
@@ -59,7 +66,7 @@ class EngineConfig:
     def mixtral_8x22b(**kw) -> "EngineConfig":
         """Mixtral-8x22B shape (L=56, E=8, K=2, d=6144, f=16384)."""
         base = dict(num_layers=56, num_experts=8, top_k=2, hidden_dim=6144, ffn_dim=16384,
-                    expert_kind="swiglu", mixing_scale=0.1 * math.sqrt(16 / 6144))
+                    expert_kind="swiglu", mixing_scale=0.1 * math.sqrt(16 / 6144), rms_norm=True)
         base.update(kw)
         return EngineConfig(**base)
 
@@ -87,7 +94,8 @@ class EngineConfig:
             mixing_scale=self.mixing_scale, prefetch=modes[self.prefetch],
             renormalize=int(self.renormalize), record_speculation=int(self.record_speculation),
             max_tokens=self.max_tokens, chunk_bytes=self.chunk_bytes,
-            prefetch_depth=self.prefetch_depth, device=self.device)
+            prefetch_depth=self.prefetch_depth, device=self.device, rms_norm=int(self.rms_norm),
+            rms_eps=self.rms_eps)
 
 
 class OffloadEngine:
@@ -125,9 +133,9 @@ class OffloadEngine:
             pass
 
     # -- weights --
-    def init_random(self, seed: int = 42) -> None:
+    def init_random(self, seed: int = 42, gate_bias_std: float = DEFAULT_GATE_BIAS_STD) -> None:
         """Synthetic Mixtral-shaped bf16 weights from the counter hash."""
-        _native.check(self._lib.moe_engine_init_random(self._h, int(seed)))
+        _native.check(self._lib.moe_engine_init_random(self._h, int(seed), float(gate_bias_std)))
 
     def load_toy_model(self, model) -> None:
         """Upload a ToyMoeModel's weights (reference layout, rounded to f32)."""
@@ -194,6 +202,29 @@ class OffloadEngine:
                                                   _native.stream_ptr(stream)))
         self.tokens_done += T
         return h_out
+
+    def set_mode(self, policy: Optional[PolicyKind] = None, cache_size: Optional[int] = None,
+                 prefetch: Optional[str] = None) -> None:
+        """Switch policy / cache size (<= the allocated one) / prefetch, with cold caches."""
+        import dataclasses
+
+        cfg = dataclasses.replace(
+            self.config, policy=policy or self.config.policy,
+            cache_size=self.config.cache_size if cache_size is None else cache_size,
+            prefetch=self.config.prefetch if prefetch is None else prefetch)
+        c = cfg.to_c()
+        _native.check(self._lib.moe_engine_set_mode(self._h, c.policy, c.decay_factor,
+                                                    c.decay_period, c.cache_size, c.prefetch))
+        self.config = cfg
+
+    def profile(self, enable: bool = True) -> None:
+        """Record CUDA events around every kernel class on the compute stream."""
+        _native.check(self._lib.moe_engine_profile(self._h, int(enable)))
+
+    def kernel_times(self) -> dict:
+        k = _native.KernelTimesC()
+        _native.check(self._lib.moe_engine_kernel_times(self._h, ctypes.byref(k)))
+        return {name: getattr(k, name) for name, _ in _native.KernelTimesC._fields_}
 
     def sync(self) -> None:
         _native.check(self._lib.moe_engine_sync(self._h))

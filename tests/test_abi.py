@@ -40,5 +40,5 @@ def test_invalid_config_is_rejected_before_any_device_work():
 
 def test_engine_struct_layout_matches_header():
     # 8 int32 + double + int64 + float + 4 int32 + (pad) int64 + 2 int32 (moe_engine_config)
-    assert ctypes.sizeof(_native.EngineConfigC) == 88
+    assert ctypes.sizeof(_native.EngineConfigC) == 96
     assert ctypes.sizeof(_native.StatsC) == 12 * 8
