@@ -14,7 +14,9 @@ extern "C" moe_status moe_microbench_gemv(int32_t kernel, int32_t d, int32_t f, 
                                           int32_t stage_kb, int32_t max_stages, int32_t grid,
                                           int32_t rpb, int32_t iters, float* ms_per_iter,
                                           int64_t* bytes_per_iter) {
-  MOE_REQUIRE(kernel >= 0 && kernel <= 5, "kernel must be 0..5");
+  MOE_REQUIRE(kernel >= 0 && kernel <= 8, "kernel must be 0..8");
+  const bool stream_only = kernel >= 6;  // 6/7/8: stream kernels with the compute skipped
+  if (stream_only) kernel -= 6;
   MOE_REQUIRE(experts >= 1 && experts <= 2 && d % 256 == 0 && f % 256 == 0, "bad shape");
   const bool mix = kernel == 0 || kernel == 3;
   const int mode = kernel % 3;
@@ -88,6 +90,7 @@ extern "C" moe_status moe_microbench_gemv(int32_t kernel, int32_t d, int32_t f, 
       sp.only = -1;
       sp.act = act;
       sp.yout = y;
+      sp.stream_only = stream_only ? 1 : 0;
       if (mode == kModeMix)
         launch_stream<kModeMix>(gg, G, sp, 0);
       else if (mode == kModeUp)

@@ -97,6 +97,7 @@ struct StreamParams {
   float* part;             // [gridDim.x][3E + 2]
   // UP: scale applied to xin while staging (1/rms(h') from the gate), or nullptr
   const float* xscale;
+  int stream_only;         // microbenchmark: consumers release stages without computing
 };
 
 // Which experts this launch covers: (selection slot j, weight block), in ascending expert
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
     mbar_wait(&full[s], (it / S) & 1);
     const uint8_t* st = stage_base + static_cast<size_t>(s) * stage_bytes;
     const int col8 = (c * cb + part_id * span) / 8;
-    {
+    if (!p.stream_only) {
       const uint4* row0 = reinterpret_cast<const uint4*>(st + row_in_block * slice) + part_id * (span / 8);
       const uint4* row1 = reinterpret_cast<const uint4*>(st + ((NM - 1) * RPB + row_in_block) * slice) +
                           part_id * (span / 8);

@@ -10,7 +10,8 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2511_05814_b200 import _native  # noqa: E402
 
-NAMES = ["stream-mix", "stream-up", "stream-down", "ldg-mix", "ldg-up", "ldg-down"]
+NAMES = ["stream-mix", "stream-up", "stream-down", "ldg-mix", "ldg-up", "ldg-down",
+         "tma-only-mix", "tma-only-up", "tma-only-down"]
 
 
 def run(kernel, d, f, experts, stage_kb=0, max_stages=6, grid=0, rpb=0, iters=20):
@@ -26,14 +27,12 @@ def run(kernel, d, f, experts, stage_kb=0, max_stages=6, grid=0, rpb=0, iters=20
 def main():
     d, f = 4096, 14336
     configs = []
-    for k in (3, 4, 5):
-        configs.append(dict(kernel=k, d=d, f=f, experts=2))
     for k in (0, 1, 2):
         for ex in ((1, 2) if k else (1,)):
-            configs.append(dict(kernel=k, d=d, f=f, experts=ex))  # engine defaults
-            for rpb in (8, 4, 2):
-                for skb in (32, 64):
-                    configs.append(dict(kernel=k, d=d, f=f, experts=ex, stage_kb=skb, rpb=rpb))
+            configs.append(dict(kernel=k, d=d, f=f, experts=ex))          # engine defaults
+            configs.append(dict(kernel=k + 6, d=d, f=f, experts=ex))      # same, no compute
+            for rpb, skb in ((8, 64), (8, 96), (4, 64), (4, 32), (2, 64), (8, 32)):
+                configs.append(dict(kernel=k + 6, d=d, f=f, experts=ex, stage_kb=skb, rpb=rpb))
     for c in configs:
         try:
             print(json.dumps(run(**c)), flush=True)
