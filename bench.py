@@ -55,7 +55,13 @@ def parse_args():
     p.add_argument("--cpu-sample-tokens", type=int, default=16)
     p.add_argument("--cpu-sample-layers", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--layers", type=int, default=L, help="debug: fewer layers (invalidates the metric)")
+    p.add_argument("--layers", type=int, default=0,
+                   help="fewer layers than the model (invalidates the headline; diagnostics)")
+    p.add_argument("--model", choices=["mixtral_8x7b", "mixtral_8x22b"], default="mixtral_8x7b")
+    p.add_argument("--sweep-cache", default="",
+                   help="e.g. 2,4,6: LFU and LFU+prefetch at each cache size (configs[2])")
+    p.add_argument("--shared-store", action="store_true",
+                   help="host experts in a node-shared segment (automatic when WORLD_SIZE > 1)")
     return p.parse_args()
 
 
@@ -286,34 +292,64 @@ def run_reference(args, world, rank, local):
 
 # ---- our engine ------------------------------------------------------------------------
 
+def parse_variant(v: str, default_c: int):
+    """'lru' | 'lfu' | 'lfu+prefetch' | 'lfu@6' | 'lfu+prefetch@2' -> (policy, C, prefetch)."""
+    from paper_2511_05814_b200.policies import PolicyKind
+
+    name, _, c = v.partition("@")
+    policy = PolicyKind.lfu() if name.startswith("lfu") else PolicyKind.lru()
+    return policy, int(c) if c else default_c, "prefetch" in name
+
+
 def run_ours(args, world, rank, local):
-    import numpy as np
     import torch
 
-    from paper_2511_05814_b200 import _native
+    from paper_2511_05814_b200 import _native, replicas
     from paper_2511_05814_b200.engine import EngineConfig, OffloadEngine, hash_weights, tensor_id
-    from paper_2511_05814_b200.policies import PolicyKind
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    nl = args.layers
+    factory = EngineConfig.mixtral_8x22b if args.model == "mixtral_8x22b" else EngineConfig.mixtral_8x7b
+    variants = [v for v in args.variants.split(",") if v]
+    if args.sweep_cache:
+        variants = [f"{p}@{c}" for c in args.sweep_cache.split(",") for p in ("lfu", "lfu+prefetch")]
+    parsed = [parse_variant(v, args.cache_size) for v in variants]
+    cap_c = max(c for _, c, _ in parsed)
+    want_prefetch = any(pf for _, _, pf in parsed)
+    base_cfg = factory()
+    nl = args.layers or base_cfg.num_layers
+    cfg = factory(num_layers=nl, cache_size=cap_c, prefetch="early" if want_prefetch else "off",
+                  max_tokens=4096, device=local)
+    D, F, EB = cfg.hidden_dim, cfg.ffn_dim, cfg.expert_bytes
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.model == "mixtral_8x7b":
         cpu = cpu_reference_sample(args.seed, args.cpu_sample_tokens, args.cpu_sample_layers)
     pcie_peak = h2d_peak_gbs(dev)
 
-    variants = [v for v in args.variants.split(",") if v]
-    want_prefetch = any("prefetch" in v for v in variants)
-    cfg = EngineConfig.mixtral_8x7b(num_layers=nl, cache_size=args.cache_size,
-                                    policy=PolicyKind.lru(),
-                                    prefetch="early" if want_prefetch else "off",
-                                    max_tokens=4096, device=local)
     t_setup = time.perf_counter()
-    eng = OffloadEngine(cfg)
-    eng.init_random(args.seed)
+    store = None
+    local_rank, local_world = replicas.local_world()
+    if world > 1 or args.shared_store:
+        # one host copy of the experts per node, page-locked by every local replica
+        nbytes = cfg.num_layers * cfg.num_experts * EB
+        name = replicas.store_name(cfg, args.seed, os.environ.get("TORCHELASTIC_RUN_ID", ""))
+        holder = {}
+
+        def fill(st):
+            holder["eng"] = OffloadEngine(cfg, store=st)
+            holder["eng"].init_random(args.seed)
+
+        store = replicas.open_shared_store(name, nbytes, local_rank, lambda: barrier(world), fill)
+        eng = holder.get("eng")
+        if eng is None:
+            eng = OffloadEngine(cfg, store=store)
+            eng.init_random(args.seed, init_experts=False)
+    else:
+        eng = OffloadEngine(cfg)
+        eng.init_random(args.seed)
     t_setup = time.perf_counter() - t_setup
     # independent request stream per rank: token inputs from the counter hash (f32, std 1)
-    base = rank * 1_000_000
+    base = replicas.rank_token_base(rank)
     n_tok = args.warmup + args.steps + args.e2e_steps
     inputs = torch.stack([hash_weights(args.seed, tensor_id(5, base + t), 1.0, D, "f32")
                           for t in range(n_tok)])
@@ -323,10 +359,8 @@ def run_ours(args, world, rank, local):
     ktimes = None
     clocks = None
     e2e = None
-    for v in variants:
-        policy = PolicyKind.lfu() if v.startswith("lfu") else PolicyKind.lru()
-        eng.set_mode(policy=policy, cache_size=args.cache_size,
-                     prefetch="early" if "prefetch" in v else "off")
+    for v, (policy, csize, prefetch) in zip(variants, parsed):
+        eng.set_mode(policy=policy, cache_size=csize, prefetch="early" if prefetch else "off")
         t0_tok = eng.tokens_done
         eng.decode_device(inputs[: args.warmup])
         eng.sync()
@@ -350,7 +384,7 @@ def run_ours(args, world, rank, local):
             sampler.__exit__()
             clocks = sampler.summary()
         barrier(world)
-        ms = max_over_ranks(a.elapsed_time(b), world)
+        tps, ms, total_tok = replicas.reduce_timing(a.elapsed_time(b), args.steps, world)
         eng.sync()
         n1 = _native.kernel_launches()
         s1 = eng.stats()
@@ -364,15 +398,16 @@ def run_ours(args, world, rank, local):
         h2d = s1["h2d_bytes"] - s0["h2d_bytes"]
         busy = s1["copy_busy_ms"] - s0["copy_busy_ms"]
         rec = eng.records(t0_tok + args.warmup, args.steps)
-        total_tok = sum_over_ranks(args.steps, world)
         results[v] = {
-            "tokens_per_s": total_tok / (ms / 1e3),
+            "policy": str(policy), "cache_size": csize, "prefetch": prefetch,
+            "tokens_per_s": tps,
             "ms_per_step": ms / args.steps,
             "hit_rate": hits / max(1, hits + misses),
             "misses_per_token": misses / args.steps,
             "h2d_GBps": h2d / (ms / 1e3) / 1e9,
             "demand_copy_GBps": demand / (busy / 1e3) / 1e9 if busy > 0 else None,
             "pcie_frac_of_measured_h2d_peak": (h2d / (ms / 1e3) / 1e9) / pcie_peak,
+            "pcie_bound_tokens_per_s": pcie_peak * 1e9 / max(1.0, misses / args.steps * EB),
             "prefetch_issued": s1["prefetch_issued"] - s0["prefetch_issued"],
             "prefetch_used": s1["prefetch_used"] - s0["prefetch_used"],
             "prefetch_wasted_bytes": s1["prefetch_wasted_bytes"] - s0["prefetch_wasted_bytes"],
@@ -388,10 +423,14 @@ def run_ours(args, world, rank, local):
             t0 = time.perf_counter()
             for i in range(args.e2e_steps):
                 eng.decode(xs[i: i + 1])
-            dt = max_over_ranks(time.perf_counter() - t0, world)
-            e2e = {"value": sum_over_ranks(args.e2e_steps, world) / dt, "unit": "tokens/s",
+            e_tps, _, _ = replicas.reduce_timing((time.perf_counter() - t0) * 1e3,
+                                                 args.e2e_steps, world)
+            e2e = {"value": e_tps, "unit": "tokens/s",
                    "h2d_bytes_per_step": D * 4, "d2h_bytes_per_step": D * 4}
     eng.close()
+    if store is not None:
+        barrier(world)
+        store.close()
     if rank != 0:
         return
     head = results[variants[0]]
@@ -401,9 +440,9 @@ def run_ours(args, world, rank, local):
     # the all-launch figure (incl. phase launches that found no expert) is reported beside
     ffn_gbs = (ktimes["ffn_active_bytes"] / (ktimes["ffn_active_ms"] / 1e3) / 1e9
                if ktimes["ffn_active_ms"] > 0 else None)
-    ffn_all_gbs = (ktimes["ffn_expert_runs"] * EXPERT_BYTES / (ktimes["ffn_ms"] / 1e3) / 1e9
+    ffn_all_gbs = (ktimes["ffn_expert_runs"] * EB / (ktimes["ffn_ms"] / 1e3) / 1e9
                    if ktimes["ffn_ms"] > 0 else None)
-    traffic = committed_ffn_traffic()
+    traffic = committed_ffn_traffic() if args.model == "mixtral_8x7b" else None
     line = {
         "metric": METRIC,
         "value": head["tokens_per_s"],
@@ -418,13 +457,15 @@ def run_ours(args, world, rank, local):
         "dtype": "bf16",
         "data": "synthetic (counter-hash random-init weights and token inputs)",
         "config": {
-            "workload": "configs[1]: Mixtral-8x7B-shaped bf16 batch-1 decode, LRU cache 4/layer, "
-                        "experts in pinned host DRAM",
-            "model": f"mixtral-8x7b-shape (L={nl},E={E},K={K},d={D},f={F}), random-init",
+            "workload": f"{'configs[4]' if args.model == 'mixtral_8x22b' else 'configs[1]'}: "
+                        f"{args.model}-shaped bf16 batch-1 decode, {variants[0]} cache "
+                        f"{head['cache_size']}/layer, experts in pinned host DRAM",
+            "model": f"{args.model}-shape (L={nl},E={cfg.num_experts},K={cfg.top_k},d={D},f={F}),"
+                     " random-init",
             "global_batch": world, "seq_len": 1, "parallelism": f"replicas x{world}",
-            "cache_size": args.cache_size, "policy": variants[0],
+            "cache_size": head["cache_size"], "policy": variants[0],
             "l2": "inputs larger than L2: each step streams >=23.6 GB of weights through HBM",
-            "setup_s": round(t_setup, 1),
+            "setup_s": round(t_setup, 1), "shared_store": store is not None,
         },
         "hit_rate": head["hit_rate"],
         "variants": results,
@@ -441,7 +482,8 @@ def run_ours(args, world, rank, local):
                                  if ktimes["ffn_active_launches"] else None),
             "achieved_incl_empty_phase_launches": ffn_all_gbs,
             "traffic": traffic.get("dram_bytes_per_expert") if traffic else None,
-            "algorithmic_bytes_per_expert": EXPERT_BYTES,
+            "traffic_unit": "DRAM bytes per expert (ncu, profiles/ncu_ffn_traffic.json)",
+            "algorithmic_bytes_per_expert": EB,
             "peak_source": peaks.get("source", "MEASURED_PEAKS.json hbm_gbs"),
         },
         "kernel_ms_per_step": {k: ktimes[k] / args.steps for k in ("mix_ms", "gate_ms", "ffn_ms",

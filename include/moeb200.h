@@ -153,6 +153,11 @@ typedef struct {
 } moe_stats;
 
 moe_status moe_engine_create(const moe_engine_config* cfg, moe_engine** out);
+/* Same, with a caller-owned host expert store ([L][E][expert] bytes, e.g. a POSIX shared-memory
+ * segment shared by the replicas of one node); the engine page-locks it with cudaHostRegister
+ * and never frees it.  store == NULL allocates a private pinned store. */
+moe_status moe_engine_create_ex(const moe_engine_config* cfg, void* store, int64_t store_bytes,
+                                moe_engine** out);
 moe_status moe_engine_destroy(moe_engine* eng);
 
 /* Dense per-layer weights from host memory, reference layout (toymoe.py:74-83):
@@ -164,8 +169,10 @@ moe_status moe_engine_set_toy_expert_f32(moe_engine* eng, int32_t layer, int32_t
                                          const float* w1, const float* w2);
 /* Synthetic Mixtral-shaped weights from the counter-hash generator (moe_hash_weights).
  * gate_bias_std is the reference's expert-imbalance knob (toymoe `skew`, toymoe.py:75);
- * see DESIGN.md for the value the bench uses. */
-moe_status moe_engine_init_random(moe_engine* eng, uint64_t seed, float gate_bias_std);
+ * see DESIGN.md for the value the bench uses.  init_experts = 0 writes only the device-resident
+ * dense weights (a replica attached to a store its owner already filled). */
+moe_status moe_engine_init_random(moe_engine* eng, uint64_t seed, float gate_bias_std,
+                                  int32_t init_experts);
 /* Host view of one expert block in the pinned store ([w1 | w3 | w2] bf16 or [W1t | W2t] f32). */
 moe_status moe_engine_expert_host_ptr(moe_engine* eng, int32_t layer, int32_t expert,
                                       void** ptr, int64_t* bytes);

@@ -25,7 +25,7 @@ EXPORTED = (
     "moe_last_error", "moe_abi_version", "moe_kernel_launches",
     "moe_replay_policy", "moe_replay_policy_layers", "moe_policy_step",
     "moe_gate_topk_f64", "moe_toy_forward_f64",
-    "moe_engine_create", "moe_engine_destroy", "moe_engine_set_dense_f32",
+    "moe_engine_create", "moe_engine_create_ex", "moe_engine_destroy", "moe_engine_set_dense_f32",
     "moe_engine_set_toy_expert_f32", "moe_engine_init_random", "moe_engine_expert_host_ptr",
     "moe_engine_dense_host", "moe_engine_reset", "moe_engine_decode", "moe_engine_sync",
     "moe_engine_records", "moe_engine_stats", "moe_engine_set_mode", "moe_engine_profile",
@@ -80,7 +80,8 @@ _SIGNATURES = {
     "moe_engine_destroy": ([_P], _I32),
     "moe_engine_set_dense_f32": ([_P, _I32, _P, _P, _P], _I32),
     "moe_engine_set_toy_expert_f32": ([_P, _I32, _I32, _P, _P], _I32),
-    "moe_engine_init_random": ([_P, _U64, _F32], _I32),
+    "moe_engine_init_random": ([_P, _U64, _F32, _I32], _I32),
+    "moe_engine_create_ex": ([ctypes.POINTER(EngineConfigC), _P, _I64, ctypes.POINTER(_P)], _I32),
     "moe_engine_expert_host_ptr": ([_P, _I32, _I32, ctypes.POINTER(_P), ctypes.POINTER(_I64)], _I32),
     "moe_engine_dense_host": ([_P, _I32, _P, _P, _P], _I32),
     "moe_engine_reset": ([_P], _I32),

@@ -51,7 +51,17 @@ struct PinnedStore {
   size_t bytes = 0;
   bool registered = false;
   bool via_alloc = false;
+  bool external = false;  // caller-owned memory (e.g. a shared-memory store), only registered
   double setup_ms = 0;
+
+  moe_status attach(void* p, size_t n) {
+    base = static_cast<char*>(p);
+    bytes = n;
+    external = true;
+    MOE_CUDA(cudaHostRegister(base, n, cudaHostRegisterPortable));
+    registered = true;
+    return MOE_OK;
+  }
 
   moe_status allocate(size_t n) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -85,6 +95,11 @@ struct PinnedStore {
   }
   void release() {
     if (!base) return;
+    if (external) {
+      if (registered) cudaHostUnregister(base);
+      base = nullptr;
+      return;
+    }
     if (via_alloc) {
       cudaFreeHost(base);
     } else {
@@ -150,6 +165,8 @@ struct moe_engine {
   bool debug = getenv("MOE_DEBUG") != nullptr;
   unsigned long long* gate_phase_ns = nullptr;  // MOE_GATE_TIMING: per-phase gate kernel time
   int cap_C = 0;  // policy slots allocated per layer (set_mode may use fewer)
+  void* ext_store = nullptr;  // caller-provided expert store (shared between replicas)
+  int64_t ext_store_bytes = 0;
 
   // kernel profiling (moe_engine_profile): per-layer event sextets, resolved lazily
   bool profiling = false;
@@ -444,6 +461,11 @@ int round8(int x) { return (x + 7) / 8 * 8; }
 extern "C" {
 
 moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) {
+  return moe_engine_create_ex(cfg_in, nullptr, 0, out);
+}
+
+moe_status moe_engine_create_ex(const moe_engine_config* cfg_in, void* store, int64_t store_bytes,
+                                moe_engine** out) {
   MOE_REQUIRE(cfg_in && out, "null argument");
   const moe_engine_config& c = *cfg_in;
   MOE_REQUIRE(c.num_layers >= 1, "num_layers must be >= 1, got %d", c.num_layers);
@@ -491,6 +513,8 @@ moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) 
   g->S = c.prefetch ? c.top_k : 0;
   g->NB = c.cache_size + g->S;
   g->cap_C = c.cache_size;
+  g->ext_store = store;
+  g->ext_store_bytes = store_bytes;
   const moe_status st = create_resources(g);
   if (st != MOE_OK) {
     const std::string msg = moe_last_error();
@@ -557,7 +581,15 @@ moe_status create_resources(moe_engine* g) {
   }
   if (getenv("MOE_GATE_TIMING"))
     TRY(alloc_device(reinterpret_cast<void**>(&g->gate_phase_ns), 8 * sizeof(unsigned long long)));
-  TRY(g->store.allocate(static_cast<size_t>(L) * E * g->expert_bytes));
+  const size_t store_bytes = static_cast<size_t>(L) * E * g->expert_bytes;
+  if (g->ext_store) {
+    MOE_REQUIRE(static_cast<size_t>(g->ext_store_bytes) >= store_bytes,
+                "external expert store holds %lld bytes, the model needs %zu",
+                (long long)g->ext_store_bytes, store_bytes);
+    TRY(g->store.attach(g->ext_store, store_bytes));
+  } else {
+    TRY(g->store.allocate(store_bytes));
+  }
   reset_states_kernel<<<L, 64>>>(g->states, L, g->NB);
   MOE_LAUNCHED();
   MOE_CUDA(cudaDeviceSynchronize());
@@ -656,7 +688,8 @@ moe_status moe_engine_set_toy_expert_f32(moe_engine* g, int32_t layer, int32_t e
   return MOE_OK;
 }
 
-moe_status moe_engine_init_random(moe_engine* g, uint64_t seed, float gate_bias_std) {
+moe_status moe_engine_init_random(moe_engine* g, uint64_t seed, float gate_bias_std,
+                                  int32_t init_experts) {
   MOE_REQUIRE(g, "null engine");
   MOE_REQUIRE(g->bf16, "init_random synthesises Mixtral-shaped (SwiGLU bf16) weights");
   MOE_CUDA(cudaSetDevice(g->device));
@@ -673,10 +706,11 @@ moe_status moe_engine_init_random(moe_engine* g, uint64_t seed, float gate_bias_
     TRY(launch_hash_f32(seed, tensor_id(kTGateB, l, 0, 0), gate_bias_std, E,
                         g->gate_b + static_cast<size_t>(l) * E, s));
   }
-  // experts: generate into a free HBM buffer, then copy down into the pinned store
+  // experts: generate into a free HBM buffer, then copy down into the pinned store (a
+  // replica attached to a shared store leaves this to the store's owner)
   uint16_t* scratch = reinterpret_cast<uint16_t*>(g->pool);
   const long long fd = 1ll * f * d;
-  for (int l = 0; l < L; ++l)
+  for (int l = 0; l < (init_experts ? L : 0); ++l)
     for (int e = 0; e < E; ++e) {
       TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW1), sd, fd, scratch, s));
       TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW3), sd, fd, scratch + fd, s));

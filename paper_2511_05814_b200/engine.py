@@ -101,16 +101,23 @@ class EngineConfig:
 class OffloadEngine:
     """Owns one libmoeb200 engine (one per GPU, driven by one host thread)."""
 
-    def __init__(self, config: EngineConfig):
+    def __init__(self, config: EngineConfig, store=None):
+        """store: optional caller-owned host expert store (replicas.SharedExpertStore) shared by
+        the engines of one node; None allocates a private pinned store."""
         import torch
 
         self.config = config
         self._lib = _native.lib()
         self._dev = torch.device("cuda", config.device)
+        self._store = store
         c = config.to_c()
         handle = ctypes.c_void_p()
         with torch.cuda.device(self._dev):
-            _native.check(self._lib.moe_engine_create(ctypes.byref(c), ctypes.byref(handle)))
+            if store is None:
+                _native.check(self._lib.moe_engine_create(ctypes.byref(c), ctypes.byref(handle)))
+            else:
+                _native.check(self._lib.moe_engine_create_ex(
+                    ctypes.byref(c), store.address, store.nbytes, ctypes.byref(handle)))
         self._h = handle
         self.tokens_done = 0
 
@@ -133,9 +140,12 @@ class OffloadEngine:
             pass
 
     # -- weights --
-    def init_random(self, seed: int = 42, gate_bias_std: float = DEFAULT_GATE_BIAS_STD) -> None:
-        """Synthetic Mixtral-shaped bf16 weights from the counter hash."""
-        _native.check(self._lib.moe_engine_init_random(self._h, int(seed), float(gate_bias_std)))
+    def init_random(self, seed: int = 42, gate_bias_std: float = DEFAULT_GATE_BIAS_STD,
+                    init_experts: bool = True) -> None:
+        """Synthetic Mixtral-shaped bf16 weights from the counter hash.
+        init_experts=False: dense weights only (the shared store's owner wrote the experts)."""
+        _native.check(self._lib.moe_engine_init_random(self._h, int(seed), float(gate_bias_std),
+                                                       int(init_experts)))
 
     def load_toy_model(self, model) -> None:
         """Upload a ToyMoeModel's weights (reference layout, rounded to f32)."""

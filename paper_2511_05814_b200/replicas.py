@@ -1,0 +1,112 @@
+"""Independent decode replicas, one engine per GPU ("replicas only").
+
+Routing and caches never interact across GPUs, so the hot path has no collective; the only
+cross-rank traffic is the bench's timing reduction.  What ranks of one node do share is the
+host expert store: 90 GB (8x7B) or 271 GB (8x22B) per copy does not fit once per GPU in host
+DRAM, so local rank 0 creates a POSIX shared-memory segment, fills it, and every local rank's
+engine page-locks the same pages (moe_engine_create_ex).  The experts are the model's weights,
+identical for every replica; each replica serves its own request stream.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+from dataclasses import dataclass
+from multiprocessing import shared_memory
+from typing import Callable, Optional
+
+TOKENS_PER_RANK_STREAM = 1_000_000  # token-id offset between replicas' synthetic streams
+
+
+def rank_token_base(rank: int) -> int:
+    """First synthetic token index of a replica's request stream (streams never overlap)."""
+    return rank * TOKENS_PER_RANK_STREAM
+
+
+def store_name(config, seed: int, job: str = "") -> str:
+    """Deterministic shm name for a model shape + seed (+ job id, to isolate concurrent jobs)."""
+    key = f"{config.num_layers}x{config.num_experts}x{config.hidden_dim}x{config.ffn_dim}:" \
+          f"{config.expert_kind}:{seed}:{job}"
+    return "moeb200_" + hashlib.sha1(key.encode()).hexdigest()[:16]
+
+
+@dataclass
+class SharedExpertStore:
+    """A named host memory segment holding [L][E][expert] bytes."""
+
+    shm: shared_memory.SharedMemory
+    owner: bool
+
+    @classmethod
+    def create(cls, name: str, nbytes: int) -> "SharedExpertStore":
+        try:  # a stale segment from a killed run
+            old = shared_memory.SharedMemory(name=name)
+            old.close()
+            old.unlink()
+        except FileNotFoundError:
+            pass
+        return cls(shared_memory.SharedMemory(name=name, create=True, size=nbytes), True)
+
+    @classmethod
+    def attach(cls, name: str) -> "SharedExpertStore":
+        return cls(shared_memory.SharedMemory(name=name), False)
+
+    @property
+    def nbytes(self) -> int:
+        return self.shm.size
+
+    @property
+    def address(self) -> int:
+        import ctypes
+
+        return ctypes.addressof(ctypes.c_char.from_buffer(self.shm.buf))
+
+    def close(self) -> None:
+        try:
+            self.shm.close()
+        except BufferError:  # a ctypes view still alive: the mapping dies with the process
+            pass
+        if self.owner:
+            try:
+                self.shm.unlink()
+            except FileNotFoundError:
+                pass
+
+
+def open_shared_store(name: str, nbytes: int, local_rank: int,
+                      barrier: Callable[[], None],
+                      fill: Optional[Callable[[SharedExpertStore], None]] = None):
+    """Local rank 0 creates (and fills) the segment; the others attach after a barrier.
+
+    Returns the store; `fill(store)` runs on the owner before the barrier releases the rest.
+    """
+    if local_rank == 0:
+        store = SharedExpertStore.create(name, nbytes)
+        if fill is not None:
+            fill(store)
+        barrier()
+        return store
+    barrier()
+    return SharedExpertStore.attach(name)
+
+
+def local_world() -> tuple:
+    """(local_rank, local_world_size) from the torch.distributed.run environment."""
+    return int(os.environ.get("LOCAL_RANK", "0")), int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+
+
+def reduce_timing(elapsed_ms: float, tokens: int, world: int):
+    """Whole-job throughput of independent replicas: all tokens / slowest rank's time."""
+    if world == 1:
+        return tokens / (elapsed_ms / 1e3), elapsed_ms, tokens
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if (torch.cuda.is_available() and dist.get_backend() == "nccl") else "cpu"
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    n = torch.tensor([float(tokens)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(n, op=dist.ReduceOp.SUM)
+    ms, total = float(t.item()), int(n.item())
+    return total / (ms / 1e3), ms, total
