@@ -233,6 +233,24 @@ moe_status moe_microbench_gemv(int32_t kernel, int32_t d, int32_t f, int32_t exp
                                int32_t stage_kb, int32_t max_stages, int32_t grid, int32_t rpb,
                                int32_t iters, float* ms_per_iter, int64_t* bytes_per_iter);
 
+/* ---- K4: tcgen05 grouped GEMM (prefill), test / microbenchmark entry points ----------- */
+
+/* Grouped C = A . B^T on the tensor cores (tcgen05.mma 128x256x16, TMA, TMEM accumulators).
+ * A (sum(group_m), K) bf16 row-major, groups stacked in order; B (G*N, K) bf16 row-major,
+ * group g's matrix at rows [g*N, (g+1)*N) (nn.Linear layout); C (sum(group_m), N) f32.
+ * group_m: host array of G row counts (0 allowed).  K % 64 == 0, N % 256 == 0.
+ * Runs `iters` times; ms_per_iter (may be NULL) gets the CUDA-event time per launch. */
+moe_status moe_tc_grouped_gemm_bf16(const uint16_t* A, const uint16_t* B, float* C, int32_t G,
+                                    const int32_t* group_m, int32_t N, int32_t K, int32_t iters,
+                                    float* ms_per_iter, void* stream);
+/* Grouped SwiGLU up projection, the prefill expert's first half:
+ * act = bf16(silu(X . w1^T) * (X . w3^T)); X (sum(group_m), d) bf16; W13 (G, 2f, d) bf16 with
+ * w1 rows [0, f) and w3 rows [f, 2f) per group; act (sum(group_m), f) bf16.
+ * d % 64 == 0, f % 128 == 0. */
+moe_status moe_tc_grouped_swiglu_bf16(const uint16_t* X, const uint16_t* W13, uint16_t* act,
+                                      int32_t G, const int32_t* group_m, int32_t f, int32_t d,
+                                      int32_t iters, float* ms_per_iter, void* stream);
+
 /* ---- synthetic weights (counter hash), shared with oracle/weights.c ---------------- */
 
 /* bf16 bits of element `index` of tensor `tensor_id` for seed `seed`, scaled to unit

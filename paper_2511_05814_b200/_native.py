@@ -31,6 +31,7 @@ EXPORTED = (
     "moe_engine_records", "moe_engine_stats", "moe_engine_set_mode", "moe_engine_profile",
     "moe_engine_kernel_times", "moe_microbench_gemv",
     "moe_hash_weights_bf16", "moe_hash_weights_f32",
+    "moe_tc_grouped_gemm_bf16", "moe_tc_grouped_swiglu_bf16",
 )
 
 
@@ -96,6 +97,8 @@ _SIGNATURES = {
                              ctypes.POINTER(_F32), ctypes.POINTER(_I64)], _I32),
     "moe_hash_weights_bf16": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
     "moe_hash_weights_f32": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
+    "moe_tc_grouped_gemm_bf16": ([_P, _P, _P, _I32, _P, _I32, _I32, _I32, ctypes.POINTER(_F32), _P], _I32),
+    "moe_tc_grouped_swiglu_bf16": ([_P, _P, _P, _I32, _P, _I32, _I32, _I32, ctypes.POINTER(_F32), _P], _I32),
 }
 
 _lib = None
