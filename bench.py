@@ -60,6 +60,10 @@ def parse_args():
     p.add_argument("--model", choices=["mixtral_8x7b", "mixtral_8x22b"], default="mixtral_8x7b")
     p.add_argument("--sweep-cache", default="",
                    help="e.g. 2,4,6: LFU and LFU+prefetch at each cache size (configs[2])")
+    p.add_argument("--prefill-tokens", type=int, default=512,
+                   help="configs[3]: prefill this many tokens (tcgen05 GEMM path), 0 = skip")
+    p.add_argument("--prefill-decode", type=int, default=8,
+                   help="decode tokens timed after the prefill (configs[3] says 256; bounded here)")
     p.add_argument("--shared-store", action="store_true",
                    help="host experts in a node-shared segment (automatic when WORLD_SIZE > 1)")
     return p.parse_args()
@@ -427,7 +431,11 @@ def run_ours(args, world, rank, local):
                                                  args.e2e_steps, world)
             e2e = {"value": e_tps, "unit": "tokens/s",
                    "h2d_bytes_per_step": D * 4, "d2h_bytes_per_step": D * 4}
+    prefill = None
+    if args.prefill_tokens > 0:
+        prefill = run_prefill(args, eng, inputs, base, stream, world, pcie_peak)
     eng.close()
+    gemm_iso = isolated_gemm(D, F) if rank == 0 and args.prefill_tokens > 0 else None
     if store is not None:
         barrier(world)
         store.close()
@@ -495,7 +503,111 @@ def run_ours(args, world, rank, local):
     }
     if cpu:
         line["speedup_vs_cpu_port"] = head["tokens_per_s"] / cpu["value"]
+    if prefill:
+        tf_peak = float(peaks.get("bf16_tflops", 1590.0))
+        for rec in [prefill["gemm"]] + ([gemm_iso] if gemm_iso else []):
+            rec["tensor_frac"] = rec["tflops"] / tf_peak
+            rec["hbm_frac"] = rec["algorithmic_GBps"] / hbm_peak
+            rec["bound"] = "tensor" if rec["tensor_frac"] >= rec["hbm_frac"] else "hbm"
+            rec["peaks"] = {"bf16_tflops": tf_peak, "hbm_gbs": hbm_peak,
+                            "source": peaks.get("source", "MEASURED_PEAKS.json")}
+        prefill["gemm_isolated"] = gemm_iso
+        line["prefill"] = prefill
     print(json.dumps(line), flush=True)
+
+
+def run_prefill(args, eng, inputs, base, stream, world, pcie_peak):
+    """configs[3]: cold LRU C=4 cache, prefill P tokens as one batch (mixing map and SwiGLU
+    experts as tcgen05 grouped GEMMs, one H2D load per needed expert per layer), then decode."""
+    import torch
+
+    from paper_2511_05814_b200.engine import hash_weights, tensor_id
+    from paper_2511_05814_b200.policies import PolicyKind
+
+    P, Dd = args.prefill_tokens, inputs.shape[1]
+    X = torch.stack([hash_weights(args.seed, tensor_id(5, base + 100000 + t), 1.0, Dd, "f32")
+                     for t in range(P)])
+    eng.set_mode(policy=PolicyKind.lru(), cache_size=args.cache_size, prefetch="off")
+    eng.profile(True)
+    k0, s0 = eng.kernel_times(), eng.stats()
+    barrier(world)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    eng.prefill_device(X)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms_p = max_over_ranks(a.elapsed_time(b), world)
+    eng.sync()
+    k1, s1 = eng.kernel_times(), eng.stats()
+    eng.profile(False)
+    k = {n: k1[n] - k0[n] for n in k1}
+    nbytes = s1["prefill_bytes"] - s0["prefill_bytes"]
+    hits, misses = s1["hits"] - s0["hits"], s1["misses"] - s0["misses"]
+    out = {
+        "workload": f"configs[3]: prefill {P} tokens (one batch) + decode, LRU cache "
+                    f"{args.cache_size}/layer, cold start",
+        "prefill_tokens": P, "prefill_ms": ms_p,
+        "prefill_tokens_per_s": sum_over_ranks(P / (ms_p / 1e3), world),
+        "prefill_hit_rate": hits / max(1, hits + misses),
+        "h2d_GB": nbytes / 1e9, "h2d_GBps": nbytes / (ms_p / 1e3) / 1e9,
+        "pcie_frac_of_measured_h2d_peak": nbytes / (ms_p / 1e3) / 1e9 / pcie_peak,
+        "gemm": {"kernel": "tc::grouped_gemm_kernel (tcgen05.mma 128x256x16, TMA, TMEM; mix + "
+                           "SwiGLU up + split-K down), live in the prefill",
+                 "launches": k["gemm_launches"], "ms": k["gemm_ms"],
+                 "tflops": k["gemm_flops"] / (k["gemm_ms"] / 1e3) / 1e12 if k["gemm_ms"] else None,
+                 "algorithmic_GBps": k["gemm_bytes"] / (k["gemm_ms"] / 1e3) / 1e9 if k["gemm_ms"] else None,
+                 "share_of_prefill": k["gemm_ms"] / ms_p},
+    }
+    if args.prefill_decode > 0:
+        xs = inputs[: args.prefill_decode]
+        h0 = eng.stats()
+        a.record(stream)
+        eng.decode_device(xs)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms_d = max_over_ranks(a.elapsed_time(b), world)
+        h1 = eng.stats()
+        dh, dm = h1["hits"] - h0["hits"], h1["misses"] - h0["misses"]
+        out["decode_after_prefill"] = {"tokens": args.prefill_decode,
+                                       "tokens_per_s": args.prefill_decode / (ms_d / 1e3),
+                                       "hit_rate": dh / max(1, dh + dm)}
+    return out
+
+
+def isolated_gemm(Dd, Ff):
+    """K4 alone: the 8 experts of one layer resident in HBM, 128 token rows each (512 tokens x
+    top-2): grouped SwiGLU up (w1|w3) then grouped down, CUDA events per launch."""
+    import ctypes
+
+    import torch
+
+    from paper_2511_05814_b200 import _native
+
+    lib = _native.lib()
+    G, m = 8, 128
+    gm = (ctypes.c_int32 * G)(*([m] * G))
+    X = torch.randn(G * m, Dd, device="cuda").bfloat16()
+    W13 = (torch.randn(G, 2 * Ff, Dd, device="cuda") / Dd ** 0.5).bfloat16()
+    act = torch.empty(G * m, Ff, device="cuda", dtype=torch.bfloat16)
+    W2 = (torch.randn(G * Dd, Ff, device="cuda") / Ff ** 0.5).bfloat16()
+    out = torch.empty(G * m, Dd, device="cuda", dtype=torch.float32)
+    ms_u, ms_d = ctypes.c_float(0), ctypes.c_float(0)
+    _native.check(lib.moe_tc_grouped_swiglu_bf16(X.data_ptr(), W13.data_ptr(), act.data_ptr(), G, gm,
+                                                 Ff, Dd, 6, ctypes.byref(ms_u), _native.stream_ptr()))
+    _native.check(lib.moe_tc_grouped_gemm_bf16(act.data_ptr(), W2.data_ptr(), out.data_ptr(), G, gm,
+                                               Dd, Ff, 1, 6, ctypes.byref(ms_d), _native.stream_ptr()))
+    torch.cuda.synchronize()
+    rows = G * m
+    flops = 2.0 * rows * 2 * Ff * Dd + 2.0 * rows * Ff * Dd
+    nbytes = G * 3 * Ff * Dd * 2 + rows * Dd * 2 + 2 * rows * Ff * 2 + rows * Dd * 4
+    ms = ms_u.value + ms_d.value
+    del X, W13, act, W2, out
+    torch.cuda.empty_cache()
+    return {"kernel": "tc::grouped_gemm_kernel isolated: 8 resident experts x 128 rows, SwiGLU up + "
+                      "down (2 launches, weights 2.82 GB > L2)",
+            "up_ms": ms_u.value, "down_ms": ms_d.value, "ms": ms,
+            "tflops": flops / (ms / 1e3) / 1e12, "algorithmic_GBps": nbytes / (ms / 1e3) / 1e9}
 
 
 def main():

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define MOE_ABI_VERSION 1
+#define MOE_ABI_VERSION 2
 
 typedef int32_t moe_status;
 enum {
@@ -150,6 +150,9 @@ typedef struct {
   int64_t prefetch_wasted_bytes; /* bytes of prefetch chunks for guesses that were wrong */
   int64_t expert_bytes;     /* bytes of one expert block */
   double copy_busy_ms;      /* copy-stream busy time for demand transfers (events) */
+  int64_t prefill_tokens;   /* tokens processed by moe_engine_prefill */
+  int64_t prefill_bytes;    /* bytes copied host->device by prefill (one load per needed expert
+                               per layer; included in h2d_bytes) */
 } moe_stats;
 
 moe_status moe_engine_create(const moe_engine_config* cfg, moe_engine** out);
@@ -198,6 +201,12 @@ typedef struct {
   double ffn_active_ms;     /* device time of the FFN launches that processed >= 1 expert */
   int64_t ffn_active_bytes; /* weight bytes those launches streamed (device-counted) */
   int64_t ffn_active_launches;
+  /* prefill: tcgen05 grouped GEMM launches (mix, SwiGLU up, down) */
+  double gemm_ms;           /* summed CUDA-event time of the GEMM launches */
+  int64_t gemm_launches;
+  double gemm_flops;        /* algorithmic FLOPs of those launches (2*m*n*k per group) */
+  int64_t gemm_bytes;       /* algorithmic bytes: weights + activations read + outputs written */
+  double prefill_ms;        /* whole-prefill device time (first kernel to last, per call, summed) */
 } moe_kernel_times;
 moe_status moe_engine_profile(moe_engine* eng, int32_t enable);
 /* Resolves outstanding events (synchronises) and returns the running totals. */
@@ -207,6 +216,18 @@ moe_status moe_engine_kernel_times(moe_engine* eng, moe_kernel_times* out);
  * Token t's step records go to ring position (tokens_done + t) % max_tokens. */
 moe_status moe_engine_decode(moe_engine* eng, const float* h_in_dev, int64_t T,
                              float* h_out_dev, void* stream);
+
+/* Prefill T tokens as one batch (layer-major): for each layer, the mixing map for all T rows
+ * on the tensor cores, the gate for every token, the cache policy replayed over the T steps in
+ * token order (so step records, hit/miss/evict traces and the final cache state equal those of
+ * T decode steps), one H2D load of every needed expert that is not resident, and the SwiGLU
+ * experts as tcgen05 grouped GEMMs over the token groups.  Activations enter the GEMMs in bf16
+ * (the decode path keeps them f32), so outputs agree with decode within the bf16 tolerance.
+ * SwiGLU engines only; T <= max_tokens; hidden_dim % 256 == 0, ffn_dim % 128 == 0.
+ * h_in_dev / h_out_dev as for moe_engine_decode.  Replaces run_model's token loop
+ * (toymoe.py:175-185) for a batch of independent tokens. */
+moe_status moe_engine_prefill(moe_engine* eng, const float* h_in_dev, int64_t T,
+                              float* h_out_dev, void* stream);
 
 /* Block until the engine's outstanding work is complete; reports MOE_NONFINITE if any
  * gate produced non-finite logits since the last call. */
@@ -239,10 +260,12 @@ moe_status moe_microbench_gemv(int32_t kernel, int32_t d, int32_t f, int32_t exp
  * A (sum(group_m), K) bf16 row-major, groups stacked in order; B (G*N, K) bf16 row-major,
  * group g's matrix at rows [g*N, (g+1)*N) (nn.Linear layout); C (sum(group_m), N) f32.
  * group_m: host array of G row counts (0 allowed).  K % 64 == 0, N % 256 == 0.
+ * splits > 1: split-K; C then holds `splits` planes (splits, sum(group_m), N) whose sum is the
+ * product (each plane one contiguous k-range; 1 <= splits <= K/64).
  * Runs `iters` times; ms_per_iter (may be NULL) gets the CUDA-event time per launch. */
 moe_status moe_tc_grouped_gemm_bf16(const uint16_t* A, const uint16_t* B, float* C, int32_t G,
-                                    const int32_t* group_m, int32_t N, int32_t K, int32_t iters,
-                                    float* ms_per_iter, void* stream);
+                                    const int32_t* group_m, int32_t N, int32_t K, int32_t splits,
+                                    int32_t iters, float* ms_per_iter, void* stream);
 /* Grouped SwiGLU up projection, the prefill expert's first half:
  * act = bf16(silu(X . w1^T) * (X . w3^T)); X (sum(group_m), d) bf16; W13 (G, 2f, d) bf16 with
  * w1 rows [0, f) and w3 rows [f, 2f) per group; act (sum(group_m), f) bf16.

@@ -215,6 +215,66 @@ class MixtralRef:
         return np.stack(outs) if outs else np.zeros((0, self.d)), acts
 
 
+def bf16_round(a) -> np.ndarray:
+    """Round to bf16 (nearest even) through f32, returned widened to f32: the engine's
+    __floats2bfloat162_rn on an f32 value."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    r = (u + np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))) & np.uint32(0xFFFF0000)
+    return r.astype(np.uint32).view(np.float32)
+
+
+def mixtral_prefill(ref: "MixtralRef", X: np.ndarray, return_gaps: bool = False):
+    """Batched prefill restated (moe_engine_prefill): every layer over all T tokens, with the
+    engine's operand roundings -- the mixing GEMM reads bf16(x), the experts read
+    bf16(h' / rms(h')) and the down projection bf16(silu(w1 x) * w3 x) -- and everything else
+    in fp64.  Routing / guesses as MixtralRef.forward (toymoe.py:99-115, 178-180).
+    Returns (outputs (T, d), acts (T, L, K) sorted, guessed (T, L-1, K) sorted[, gaps (T, L)]),
+    gaps = k-th minus (k+1)-th logit, for near-tie accounting."""
+    assert ref.layout == "ref"
+    T, d = X.shape
+    L, E, K = len(ref.layers), ref.E, ref.K
+    x = X.astype(np.float64)
+    acts = np.zeros((T, L, K), np.int64)
+    guessed = np.zeros((T, max(L - 1, 0), K), np.int64)
+    gaps = np.zeros((T, L))
+    for i, l in enumerate(ref.layers):
+        M, gw, gb = ref.dense(l)
+        if i >= 1:
+            xn = np.stack([ref._norm(r) for r in x])
+            zg = xn @ gw + gb
+            guessed[:, i - 1] = np.sort(np.stack([np.lexsort((np.arange(E), -z))[:K] for z in zg]), axis=1)
+        h = x + ref.alpha * (bf16_round(x).astype(np.float64) @ M)
+        hn = np.stack([ref._norm(r) for r in h])
+        z = hn @ gw + gb
+        if not np.isfinite(z).all():
+            raise FloatingPointError("gate logits are not finite")
+        sel = np.stack([np.lexsort((np.arange(E), -zt))[:K] for zt in z])
+        zs = -np.sort(-z, axis=1)
+        gaps[:, i] = zs[:, K - 1] - zs[:, K] if K < E else np.inf
+        p = np.stack([softmax(zt) for zt in z])
+        w = np.take_along_axis(p, sel, 1)
+        if ref.renormalize:
+            w = w / w.sum(1, keepdims=True)
+        an = bf16_round(hn).astype(np.float64)
+        y = np.zeros((T, K, d))
+        for e in range(E):
+            rows, slots = np.nonzero(sel == e)
+            if rows.size == 0:
+                continue
+            w1, w3, w2 = ref.expert(l, e)
+            a1, a3 = an[rows] @ w1, an[rows] @ w3
+            act = bf16_round(a1 / (1.0 + np.exp(-a1)) * a3).astype(np.float64)
+            y[rows, slots] = act @ w2
+        out = h.copy()
+        for j in range(K):
+            out = out + w[:, j:j + 1] * y[:, j]
+        acts[:, i] = np.sort(sel, axis=1)
+        x = out
+    if return_gaps:
+        return x, acts, guessed, gaps
+    return x, acts, guessed
+
+
 def replay_layers(acts: np.ndarray, E: int, C: int, policy: int, df=1.0, dp=1):
     """Per-layer replay of a (T, L, K) activation grid with the C oracle."""
     T, L, K = acts.shape

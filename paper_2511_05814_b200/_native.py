@@ -27,7 +27,7 @@ EXPORTED = (
     "moe_gate_topk_f64", "moe_toy_forward_f64",
     "moe_engine_create", "moe_engine_create_ex", "moe_engine_destroy", "moe_engine_set_dense_f32",
     "moe_engine_set_toy_expert_f32", "moe_engine_init_random", "moe_engine_expert_host_ptr",
-    "moe_engine_dense_host", "moe_engine_reset", "moe_engine_decode", "moe_engine_sync",
+    "moe_engine_dense_host", "moe_engine_reset", "moe_engine_decode", "moe_engine_prefill", "moe_engine_sync",
     "moe_engine_records", "moe_engine_stats", "moe_engine_set_mode", "moe_engine_profile",
     "moe_engine_kernel_times", "moe_microbench_gemv",
     "moe_hash_weights_bf16", "moe_hash_weights_f32",
@@ -53,7 +53,8 @@ class StatsC(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in (
         "tokens", "steps", "hits", "misses", "h2d_bytes", "demand_bytes", "prefetch_bytes",
         "prefetch_issued", "prefetch_used", "prefetch_wasted_bytes", "expert_bytes")] + [
-        ("copy_busy_ms", ctypes.c_double)]
+        ("copy_busy_ms", ctypes.c_double), ("prefill_tokens", ctypes.c_int64),
+        ("prefill_bytes", ctypes.c_int64)]
 
 
 class KernelTimesC(ctypes.Structure):
@@ -61,7 +62,9 @@ class KernelTimesC(ctypes.Structure):
         (n, ctypes.c_int64) for n in ("mix_launches", "gate_launches", "ffn_launches",
                                       "finalize_launches", "ffn_expert_runs")] + [
         ("ffn_active_ms", ctypes.c_double), ("ffn_active_bytes", ctypes.c_int64),
-        ("ffn_active_launches", ctypes.c_int64)]
+        ("ffn_active_launches", ctypes.c_int64), ("gemm_ms", ctypes.c_double),
+        ("gemm_launches", ctypes.c_int64), ("gemm_flops", ctypes.c_double),
+        ("gemm_bytes", ctypes.c_int64), ("prefill_ms", ctypes.c_double)]
 
 
 _P = ctypes.c_void_p
@@ -87,6 +90,7 @@ _SIGNATURES = {
     "moe_engine_dense_host": ([_P, _I32, _P, _P, _P], _I32),
     "moe_engine_reset": ([_P], _I32),
     "moe_engine_decode": ([_P, _P, _I64, _P, _P], _I32),
+    "moe_engine_prefill": ([_P, _P, _I64, _P, _P], _I32),
     "moe_engine_sync": ([_P], _I32),
     "moe_engine_records": ([_P, _I64, _I64, _P, _P, _P, _P, _P], _I32),
     "moe_engine_stats": ([_P, ctypes.POINTER(StatsC)], _I32),
@@ -97,7 +101,7 @@ _SIGNATURES = {
                              ctypes.POINTER(_F32), ctypes.POINTER(_I64)], _I32),
     "moe_hash_weights_bf16": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
     "moe_hash_weights_f32": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
-    "moe_tc_grouped_gemm_bf16": ([_P, _P, _P, _I32, _P, _I32, _I32, _I32, ctypes.POINTER(_F32), _P], _I32),
+    "moe_tc_grouped_gemm_bf16": ([_P, _P, _P, _I32, _P, _I32, _I32, _I32, _I32, ctypes.POINTER(_F32), _P], _I32),
     "moe_tc_grouped_swiglu_bf16": ([_P, _P, _P, _I32, _P, _I32, _I32, _I32, ctypes.POINTER(_F32), _P], _I32),
 }
 

@@ -17,168 +17,10 @@
 // measured to stall copies queued behind them on this driver; every dependency here is
 // CUDA-visible.)  While it waits for the next decision
 // the thread trickles speculative-prefetch chunks onto the copy stream.
-#include "engine_kernels.cuh"
 #include "hash.cuh"
 #include "stream_gemv.cuh"
 
-#include <sys/mman.h>
-#include <unistd.h>
-
-#include <algorithm>
-#include <array>
-#include <chrono>
-#include <cmath>
-#include <cstdlib>
-#include <cstring>
-#include <deque>
-#include <mutex>
-#include <thread>
-#include <vector>
-
-namespace moe {
-
-moe_status launch_hash_bf16(uint64_t seed, uint64_t tid, float std, long long n, uint16_t* out,
-                            cudaStream_t s);
-moe_status launch_hash_f32(uint64_t seed, uint64_t tid, float std, long long n, float* out,
-                           cudaStream_t s);
-
-// ---- pinned host store ------------------------------------------------------------------
-// Default: cudaHostAlloc (portable).  MOE_PIN_MODE=register: anonymous mapping with
-// transparent huge pages, first-touched by all host threads in parallel, then
-// cudaHostRegister (faster to set up for the 90 GB Mixtral-8x7B store).
-struct PinnedStore {
-  char* base = nullptr;
-  size_t bytes = 0;
-  bool registered = false;
-  bool via_alloc = false;
-  bool external = false;  // caller-owned memory (e.g. a shared-memory store), only registered
-  double setup_ms = 0;
-
-  moe_status attach(void* p, size_t n) {
-    base = static_cast<char*>(p);
-    bytes = n;
-    external = true;
-    MOE_CUDA(cudaHostRegister(base, n, cudaHostRegisterPortable));
-    registered = true;
-    return MOE_OK;
-  }
-
-  moe_status allocate(size_t n) {
-    const auto t0 = std::chrono::steady_clock::now();
-    bytes = n;
-    const char* mode = getenv("MOE_PIN_MODE");
-    if (!(mode && strcmp(mode, "register") == 0)) {
-      via_alloc = true;
-      MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&base), n, cudaHostAllocPortable));
-    } else {
-      void* p = mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
-      if (p == MAP_FAILED) {
-        set_error("mmap of %zu bytes for the expert store failed", n);
-        return MOE_OOM;
-      }
-      base = static_cast<char*>(p);
-      madvise(base, n, MADV_HUGEPAGE);
-      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-      const size_t per = ((n + hw - 1) / hw + 4095) & ~size_t(4095);
-      std::vector<std::thread> th;
-      for (unsigned i = 0; i < hw; ++i)
-        th.emplace_back([this, i, per] {
-          const size_t lo = i * per, hi = std::min(bytes, lo + per);
-          for (size_t o = lo; o < hi; o += 4096) base[o] = 0;
-        });
-      for (auto& x : th) x.join();
-      MOE_CUDA(cudaHostRegister(base, n, cudaHostRegisterPortable));
-      registered = true;
-    }
-    setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    return MOE_OK;
-  }
-  void release() {
-    if (!base) return;
-    if (external) {
-      if (registered) cudaHostUnregister(base);
-      base = nullptr;
-      return;
-    }
-    if (via_alloc) {
-      cudaFreeHost(base);
-    } else {
-      if (registered) cudaHostUnregister(base);
-      munmap(base, bytes);
-    }
-    base = nullptr;
-  }
-};
-
-struct PrefetchJob {
-  int layer, buf, expert;
-  long long next_chunk, n_chunks;
-  bool cancelled, adopted;
-};
-
-}  // namespace moe
-
-using namespace moe;
-
-struct moe_engine {
-  moe_engine_config cfg{};
-  int d = 0, dpad = 0, f = 0, NB = 0, S = 0;
-  bool bf16 = false;
-  long long expert_bytes = 0;
-  int device = 0;
-
-  // device memory
-  char* pool = nullptr;          // [L][NB][expert_bytes]
-  void* mixing = nullptr;        // [L][dpad][dpad] (bf16 or f32), device layout
-  float* gate_w = nullptr;       // [L][E][dpad]
-  float* gate_b = nullptr;       // [L][E]
-  LayerState* states = nullptr;  // [L]
-  StepRecord* ring = nullptr;    // [max_tokens][L]
-  float *h_in = nullptr, *h_mid = nullptr, *h_norm = nullptr, *y = nullptr, *act = nullptr;
-  float* gate_part = nullptr;   // [148][3E + 2] partial gate logits from the mixing GEMV
-  float* norm_scale = nullptr;  // 1 / rms(h') of the current layer
-  float *x_pad = nullptr, *out_pad = nullptr;  // padded token staging when d % 8 != 0
-  int* err = nullptr;
-  DeviceStats* dstats = nullptr;
-
-  // mapped pinned memory shared with the device
-  MailRecord* mail_h = nullptr;
-  MailRecord* mail_d = nullptr;
-  HostControl* ctl_h = nullptr;
-  HostControl* ctl_d = nullptr;
-
-  PinnedStore store;
-  cudaStream_t copy_stream = nullptr;
-
-  // forwarder state (driven by the thread calling decode)
-  long long next_mail = 0;    // first mail seq not yet forwarded
-  long long tokens_done = 0;  // absolute tokens enqueued
-  std::deque<PrefetchJob> jobs;
-  std::deque<cudaEvent_t> prefetch_inflight;  // one event per prefetch chunk in flight
-  std::vector<cudaEvent_t> sync_events;       // free list (timing disabled)
-  std::vector<cudaEvent_t> order_events;      // ring of events ordering phase 1 after copies
-  size_t order_next = 0;
-  std::mutex stats_mu;
-  moe_stats st{};
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_events;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> free_events;
-  bool debug = getenv("MOE_DEBUG") != nullptr;
-  unsigned long long* gate_phase_ns = nullptr;  // MOE_GATE_TIMING: per-phase gate kernel time
-  int cap_C = 0;  // policy slots allocated per layer (set_mode may use fewer)
-  void* ext_store = nullptr;  // caller-provided expert store (shared between replicas)
-  int64_t ext_store_bytes = 0;
-
-  // kernel profiling (moe_engine_profile): per-layer event sextets, resolved lazily
-  bool profiling = false;
-  std::vector<cudaEvent_t> prof_free;
-  std::vector<std::array<cudaEvent_t, 3>> prof_pending;  // before mix, after mix, after gate
-  std::vector<std::array<cudaEvent_t, 2>> prof_ffn;      // around each expert-FFN launch group
-  long long* prof_bytes_dev = nullptr;                    // per FFN launch: bytes streamed
-  static constexpr int kProfSlots = 1 << 16;
-  std::vector<std::array<cudaEvent_t, 2>> prof_final;
-  std::vector<int> prof_pending_k;
-  moe_kernel_times ktimes{};
-};
+#include "engine_impl.h"
 
 namespace {
 
@@ -624,6 +466,7 @@ moe_status moe_engine_destroy(moe_engine* g) {
   for (auto& a : g->prof_ffn)
     for (auto e : a) cudaEventDestroy(e);
   if (g->prof_bytes_dev) cudaFree(g->prof_bytes_dev);
+  if (g->pf) prefill_release(g->pf);
   if (g->gate_phase_ns) {
     unsigned long long h[8] = {};
     cudaMemcpy(h, g->gate_phase_ns, sizeof(h), cudaMemcpyDeviceToHost);

@@ -136,4 +136,75 @@ __device__ __forceinline__ bool warp_policy_step(WarpCacheState<EPL>& st, int E,
   return ok;
 }
 
+// Single-thread form of warp_policy_step for E <= EM experts held in registers (fully
+// unrolled): the same decisions, bit for bit (same keys, same tie-breaks, same fp64 freq
+// arithmetic), without the warp reductions -- for long sequential replays where one step's
+// shuffle latency would dominate (the prefill replays T steps per layer).  LRU / LFU /
+// LFU-aged (OPT needs the future and stays on the warp path).
+template <int EM>
+struct ScalarCacheState {
+  uint32_t resident;
+  double freq[EM];
+  long long last_touch[EM];
+};
+
+template <int EM>
+__device__ __forceinline__ bool scalar_policy_step(ScalarCacheState<EM>& st, int E, int C,
+                                                   int policy, double decay_factor,
+                                                   long long decay_period, long long t,
+                                                   const uint8_t* act, int K, uint32_t& rb,
+                                                   uint32_t& ev) {
+  if (policy == MOE_P_LFU_AGED && t > 0 && (t % decay_period) == 0) {
+#pragma unroll
+    for (int e = 0; e < EM; ++e) st.freq[e] *= decay_factor;
+  }
+  uint32_t in_act = 0;
+  int n_miss = 0;
+  for (int j = 0; j < K; ++j) {
+    const int e = act[j];
+    in_act |= 1u << e;
+    if (!((st.resident >> e) & 1u)) ++n_miss;
+  }
+  rb = st.resident;
+  ev = 0;
+  const int need = __popc(st.resident) + n_miss - C;
+  bool ok = true;
+  for (int r = 0; r < need; ++r) {
+    const uint32_t cand = st.resident & ~in_act;
+    if (!cand) {
+      ok = false;
+      break;
+    }
+    int best = -1;
+    uint64_t bf = ~0ull, bl = ~0ull;
+#pragma unroll
+    for (int e = 0; e < EM; ++e) {
+      if (e >= E || !((cand >> e) & 1u)) continue;
+      const uint64_t lk = static_cast<uint64_t>(st.last_touch[e] + kTouchBias);
+      const uint64_t fk = (policy == MOE_P_LFU || policy == MOE_P_LFU_AGED)
+                              ? static_cast<uint64_t>(__double_as_longlong(st.freq[e]))
+                              : 0ull;
+      // strict '<' in ascending e: the lowest id wins ties (kernels.py:109-131)
+      if (fk < bf || (fk == bf && lk < bl)) {
+        bf = fk;
+        bl = lk;
+        best = e;
+      }
+    }
+    st.resident &= ~(1u << best);
+    ev |= 1u << best;
+  }
+  for (int j = 0; j < K; ++j) {
+    const int e = act[j];
+#pragma unroll
+    for (int q = 0; q < EM; ++q)
+      if (q == e) {
+        st.freq[q] += 1.0;
+        st.last_touch[q] = t;
+      }
+    st.resident |= 1u << e;
+  }
+  return ok;
+}
+
 }  // namespace moe

@@ -1,6 +1,7 @@
 // Host side of the tcgen05 grouped GEMM (K4): tensor-map construction and the test /
 // microbenchmark entry points.  The prefill path (prefill.cu) launches the same kernel with
 // device-prepared tile tables.
+#define MOE_TC_GEMM_KERNEL
 #include "tc_gemm.h"
 
 #include <mutex>
@@ -47,15 +48,15 @@ moe_status make_tmap_bf16(CUtensorMap* map, const void* base, long long rows, lo
   return MOE_OK;
 }
 
-moe_status launch_grouped(const CUtensorMap& a, const CUtensorMap& b, const Params& p, int grid,
-                          cudaStream_t s) {
+moe_status launch_grouped(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
+                          const Params& p, int grid, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     MOE_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   SMEM_BYTES));
     attr = true;
   }
-  grouped_gemm_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(a, b, p);
+  grouped_gemm_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(a, b0, b1, p);
   MOE_LAUNCHED();
   return MOE_OK;
 }
@@ -118,7 +119,7 @@ moe_status run_plan(const HostPlan& hp, const CUtensorMap& ta, const CUtensorMap
   p.groups = reinterpret_cast<const tc::Group*>(base);
   p.tiles = reinterpret_cast<const tc::Tile*>(base + gbytes);
   p.n_tiles = reinterpret_cast<const int*>(base + gbytes + tbytes);
-  if (grid <= 0) grid = std::max(1, std::min(nt, tc::sm_count()));
+  if (grid <= 0) grid = std::max(1, std::min(nt * std::max(1, p.splits), tc::sm_count()));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (ms) {
     MOE_CUDA(cudaEventCreate(&e0));
@@ -127,7 +128,7 @@ moe_status run_plan(const HostPlan& hp, const CUtensorMap& ta, const CUtensorMap
   moe_status st = MOE_OK;
   for (int i = 0; i < iters && st == MOE_OK; ++i) {
     if (ms && i == (iters > 1 ? 1 : 0)) cudaEventRecord(e0, s);
-    st = tc::launch_grouped(ta, tb, p, grid, s);
+    st = tc::launch_grouped(ta, tb, tb, p, grid, s);
   }
   if (ms) {
     cudaEventRecord(e1, s);
@@ -149,11 +150,12 @@ moe_status run_plan(const HostPlan& hp, const CUtensorMap& ta, const CUtensorMap
 extern "C" {
 
 moe_status moe_tc_grouped_gemm_bf16(const uint16_t* A, const uint16_t* B, float* C, int32_t G,
-                                    const int32_t* group_m, int32_t N, int32_t K, int32_t iters,
-                                    float* ms_per_iter, void* stream) {
+                                    const int32_t* group_m, int32_t N, int32_t K, int32_t splits,
+                                    int32_t iters, float* ms_per_iter, void* stream) {
   MOE_REQUIRE(A && B && C && group_m && G >= 1, "null argument");
   MOE_REQUIRE(K % tc::BK == 0 && K >= tc::BK, "K must be a positive multiple of 64, got %d", K);
   MOE_REQUIRE(N % tc::BN == 0 && N >= tc::BN, "N must be a positive multiple of 256, got %d", N);
+  MOE_REQUIRE(splits >= 1 && splits <= K / tc::BK, "splits must be in [1, K/64], got %d", splits);
   long long rows = 0;
   for (int g = 0; g < G; ++g) {
     MOE_REQUIRE(group_m[g] >= 0, "negative group size");
@@ -172,6 +174,8 @@ moe_status moe_tc_grouped_gemm_bf16(const uint16_t* A, const uint16_t* B, float*
   p.N = N;
   p.epi = tc::kEpiStoreF32;
   p.c = C;
+  p.splits = splits;
+  p.split_stride = rows * N;
   return run_plan(hp, ta, tb, p, 0, std::max(1, iters), s, ms_per_iter);
 }
 

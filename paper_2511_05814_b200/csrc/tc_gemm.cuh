@@ -43,6 +43,7 @@ struct Group {
   int m;       // rows in the group
   int b_row0;  // first B row (N index 0); SwiGLU: first w1 row
   int b_row1;  // SwiGLU: first w3 row; otherwise unused
+  int b_map;   // which B tensor map holds the group's matrix (0 or 1)
 };
 
 struct Tile {
@@ -64,6 +65,11 @@ struct Params {
   uint16_t* act;       // kEpiSwiGLU: [rows][N] bf16
   const int* row_map;  // kEpiScatter: A row -> output row
   float* y;            // kEpiScatter: [out rows][N]
+  // split-K (kEpiStoreF32 / kEpiScatter): tile list walked `splits` times, split s reducing
+  // k-blocks [s*nk/splits, (s+1)*nk/splits) into its own output plane c/y + s*split_stride;
+  // the consumer sums the planes in split order (deterministic, no atomics)
+  int splits;
+  long long split_stride;
 };
 
 __device__ __forceinline__ float silu_mul(float a1, float a3) {
@@ -75,9 +81,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
+#ifdef MOE_TC_GEMM_KERNEL  // defined by tc_gemm.cu only: the one TU that owns the kernel
 __global__ void __launch_bounds__(THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                        const __grid_constant__ CUtensorMap tmap_b, Params p) {
+                        const __grid_constant__ CUtensorMap tmap_b0,
+                        const __grid_constant__ CUtensorMap tmap_b1, Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;                        // [STAGES][A_STAGE]
@@ -86,7 +94,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ uint32_t tmem_base_s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntiles = *p.n_tiles;
+  const int nbase = *p.n_tiles;
+  const int splits = p.splits > 1 ? p.splits : 1;
+  const int ntiles = nbase * splits;
   const int nk = p.K / BK;
 
   if (threadIdx.x == 0) {
@@ -102,7 +112,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
-    tma_prefetch_desc(&tmap_b);
+    tma_prefetch_desc(&tmap_b0);
+    tma_prefetch_desc(&tmap_b1);
   }
   if (warp == 2) tmem_alloc<TMEM_COLS>(&tmem_base_s);
   tc_fence_before();
@@ -117,9 +128,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint64_t pol_b = evict_first_policy();  // weights: streamed
       int it = 0;
       for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-        const Tile t = p.tiles[ti];
+        const Tile t = p.tiles[ti % nbase];
+        const int sp = ti / nbase;
+        const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
         const Group g = p.groups[t.group];
         const int arow = g.a_row0 + t.m0;
+        const void* tmap_b = g.b_map ? static_cast<const void*>(&tmap_b1) : static_cast<const void*>(&tmap_b0);
         int brow0, brow1;
         if (p.epi == kEpiSwiGLU) {
           brow0 = g.b_row0 + t.n0;
@@ -128,13 +142,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           brow0 = g.b_row0 + t.n0;
           brow1 = brow0 + BN / 2;
         }
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           mbar_expect_tx(&full[s], STAGE_BYTES);
           tma_load_2d(sa + s * A_STAGE, &tmap_a, &full[s], kb * BK, arow, pol_a);
-          tma_load_2d(sb + s * B_STAGE, &tmap_b, &full[s], kb * BK, brow0, pol_b);
-          tma_load_2d(sb + s * B_STAGE + B_STAGE / 2, &tmap_b, &full[s], kb * BK, brow1, pol_b);
+          tma_load_2d(sb + s * B_STAGE, tmap_b, &full[s], kb * BK, brow0, pol_b);
+          tma_load_2d(sb + s * B_STAGE + B_STAGE / 2, tmap_b, &full[s], kb * BK, brow1, pol_b);
         }
       }
     }
@@ -148,7 +162,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int sp = ti / nbase;
+        const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&full[s], (it / STAGES) & 1);
           tc_fence_after();
@@ -156,7 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
             umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                      (kb | k) != 0);
+                      (kb > kb0 || k > 0) ? 1u : 0u);
           umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
         umma_commit(&tfull[acc]);  // accumulator complete
@@ -169,7 +185,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     int lt = 0;
     for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++lt) {
       const int acc = lt & 1;
-      const Tile t = p.tiles[ti];
+      const Tile t = p.tiles[ti % nbase];
+      const long long plane = static_cast<long long>(ti / nbase) * p.split_stride;
       const Group g = p.groups[t.group];
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
@@ -205,12 +222,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float* res = nullptr;
         if (valid) {
           if (p.epi == kEpiStoreF32) {
-            out = p.c + static_cast<size_t>(arow) * p.N + t.n0;
+            out = p.c + plane + static_cast<size_t>(arow) * p.N + t.n0;
           } else if (p.epi == kEpiMix) {
             out = p.h_mid + static_cast<size_t>(arow) * p.N + t.n0;
             res = p.x + static_cast<size_t>(arow) * p.N + t.n0;
           } else {
-            out = p.y + static_cast<size_t>(p.row_map[arow]) * p.N + t.n0;
+            out = p.y + plane + static_cast<size_t>(p.row_map[arow]) * p.N + t.n0;
           }
         }
 #pragma unroll 1
@@ -251,6 +268,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_fence_after();
   if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem_base);
 }
+#endif  // MOE_TC_GEMM_KERNEL
 
 }  // namespace tc
 }  // namespace moe

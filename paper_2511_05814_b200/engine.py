@@ -213,6 +213,35 @@ class OffloadEngine:
         self.tokens_done += T
         return h_out
 
+    def prefill_device(self, h_in, h_out=None, stream=None):
+        """Enqueue a batched prefill of h_in (T, d) float32 CUDA tensor (tensor-core GEMMs,
+        one H2D load per needed expert per layer); returns h_out without syncing.  Step
+        records / cache traces equal those of decoding the same T tokens."""
+        import torch
+
+        d = self.config.hidden_dim
+        if h_in.dtype != torch.float32 or h_in.device.type != "cuda" or h_in.dim() != 2 or h_in.shape[1] != d:
+            raise ConfigError(f"h_in must be a (T, {d}) float32 CUDA tensor")
+        h_in = h_in.contiguous()
+        T = h_in.shape[0]
+        if h_out is None:
+            h_out = torch.empty_like(h_in)
+        _native.check(self._lib.moe_engine_prefill(self._h, h_in.data_ptr(), T, h_out.data_ptr(),
+                                                   _native.stream_ptr(stream)))
+        self.tokens_done += T
+        return h_out
+
+    def prefill(self, h_in) -> np.ndarray:
+        """Public prefill: host (T, d) array in, host (T, d) float32 out (copies included)."""
+        import torch
+
+        x = torch.as_tensor(np.ascontiguousarray(h_in, dtype=np.float32))
+        x = x.pin_memory().to(self._dev, non_blocking=True)
+        y = self.prefill_device(x)
+        out = y.cpu().numpy()
+        self.sync()
+        return out
+
     def set_mode(self, policy: Optional[PolicyKind] = None, cache_size: Optional[int] = None,
                  prefetch: Optional[str] = None) -> None:
         """Switch policy / cache size (<= the allocated one) / prefetch, with cold caches."""

@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_channel():
     lib = _native.load_library()
-    assert lib.moe_abi_version() == 1
+    assert lib.moe_abi_version() == 2
     assert isinstance(lib.moe_last_error(), bytes)
 
 
@@ -41,4 +41,7 @@ def test_invalid_config_is_rejected_before_any_device_work():
 def test_engine_struct_layout_matches_header():
     # 8 int32 + double + int64 + float + 4 int32 + (pad) int64 + 2 int32 (moe_engine_config)
     assert ctypes.sizeof(_native.EngineConfigC) == 96
-    assert ctypes.sizeof(_native.StatsC) == 12 * 8
+    # 11 int64 + double + 2 int64 (moe_stats)
+    assert ctypes.sizeof(_native.StatsC) == 14 * 8
+    # 4 double + 5 int64 + double + 2 int64 + double + int64 + double + int64 + double
+    assert ctypes.sizeof(_native.KernelTimesC) == 17 * 8

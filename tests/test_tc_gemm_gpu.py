@@ -13,15 +13,16 @@ from paper_2511_05814_b200 import _native
 pytestmark = pytest.mark.gpu
 
 
-def _gemm(A, B, G, gm, N, K, iters=1):
+def _gemm(A, B, G, gm, N, K, iters=1, splits=1):
     lib = _native.lib()
-    C = torch.full((A.shape[0], N), float("nan"), device="cuda", dtype=torch.float32)
+    C = torch.full((splits, A.shape[0], N), float("nan"), device="cuda", dtype=torch.float32)
     gm_c = (ctypes.c_int32 * G)(*gm)
     ms = ctypes.c_float(0)
     _native.check(lib.moe_tc_grouped_gemm_bf16(A.data_ptr(), B.data_ptr(), C.data_ptr(), G, gm_c,
-                                               N, K, iters, ctypes.byref(ms), _native.stream_ptr()))
+                                               N, K, splits, iters, ctypes.byref(ms),
+                                               _native.stream_ptr()))
     torch.cuda.synchronize()
-    return C, ms.value
+    return C.sum(0), ms.value
 
 
 def _ref(A, B, gm, N):
@@ -43,6 +44,17 @@ def test_grouped_gemm_matches_torch(gm, N, K):
     ref = _ref(A, B, gm, N)
     err = (C - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-3, err
+
+
+@pytest.mark.parametrize("splits", [2, 3, 9])
+def test_split_k_planes_sum_to_the_product(splits):
+    gm, N, K = [128, 5, 200], 512, 14 * 64
+    g = torch.Generator(device="cuda").manual_seed(splits)
+    A = torch.randn(sum(gm), K, device="cuda", generator=g).bfloat16()
+    B = torch.randn(len(gm) * N, K, device="cuda", generator=g).bfloat16()
+    C, _ = _gemm(A, B, len(gm), gm, N, K, splits=splits)
+    ref = _ref(A, B, gm, N)
+    assert (C - ref).abs().max().item() / ref.abs().max().item() < 1e-3
 
 
 def test_grouped_swiglu_matches_torch():
@@ -74,8 +86,15 @@ def test_gemm_rate_mixtral_expert_shape():
     gm, N, K = [128] * 8, 4096, 14336
     A = torch.randn(sum(gm), K, device="cuda").bfloat16()
     B = torch.randn(8 * N, K, device="cuda").bfloat16()
-    _, ms = _gemm(A, B, 8, gm, N, K, iters=5)
     flops = 2.0 * sum(gm) * N * K
-    bytes_ = B.numel() * 2 + A.numel() * 2 + sum(gm) * N * 4
-    print(f"grouped down-proj GEMM: {ms:.3f} ms, {flops / ms / 1e9:.1f} TFLOP/s, {bytes_ / ms / 1e6:.1f} GB/s")
-    assert flops / ms / 1e9 > 100
+    for splits in (1, 2, 4):
+        _, ms = _gemm(A, B, 8, gm, N, K, iters=5, splits=splits)
+        bytes_ = B.numel() * 2 + A.numel() * 2 + splits * sum(gm) * N * 4
+        print(f"grouped down-proj GEMM splits={splits}: {ms:.3f} ms, {flops / ms / 1e9:.1f} TFLOP/s, "
+              f"{bytes_ / ms / 1e6:.1f} GB/s")
+        assert flops / ms / 1e9 > 100
+    # one expert (the prefill's per-expert launch): 16 tiles, split-K fills the SMs
+    for splits in (1, 9):
+        _, ms = _gemm(A[:128], B[:N], 1, [128], N, K, iters=5, splits=splits)
+        bytes_ = N * K * 2 + 128 * K * 2 + splits * 128 * N * 4
+        print(f"one-expert down-proj splits={splits}: {ms:.3f} ms, {bytes_ / ms / 1e6:.1f} GB/s")
