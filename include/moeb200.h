@@ -274,6 +274,29 @@ moe_status moe_tc_grouped_swiglu_bf16(const uint16_t* X, const uint16_t* W13, ui
                                       int32_t G, const int32_t* group_m, int32_t f, int32_t d,
                                       int32_t iters, float* ms_per_iter, void* stream);
 
+/* ---- trace / event-log JSONL (host only, no CUDA) ------------------------------------ */
+
+/* A formatted document owned by the library (moe_text_free). */
+typedef struct moe_text moe_text;
+const char* moe_text_data(const moe_text* doc);
+int64_t moe_text_size(const moe_text* doc);
+void moe_text_free(moe_text* doc);
+
+/* traces.write_trace (traces.py:267-312), byte for byte.  kind 0: ActivationTrace, grid_a
+ * (T, L, K) int64 sorted rows; kind 1: SpeculationTrace, grid_g = guessed and grid_a = actual,
+ * both (T, L-1, K).  Formatted on all host threads for long traces. */
+moe_status moe_format_trace(int32_t kind, int32_t num_layers, int32_t num_experts, int32_t top_k,
+                            int64_t T, const int64_t* grid_a, const int64_t* grid_g,
+                            moe_text** doc);
+/* simulate.write_event_log (simulate.py:187-226) of a columnar CacheEventLog: layers[n_layers]
+ * (log.layers), activated (n_layers, T, K) int64, resident_before / evicted (n_layers, T, E)
+ * uint8; policy is str(PolicyKind) (e.g. "lru", "lfu-aged:0.5:16"). */
+moe_status moe_format_event_log(const char* policy, int32_t cache_size, int32_t num_layers,
+                                int32_t num_experts, int32_t top_k, int64_t warmup_tokens,
+                                int32_t n_layers, const int32_t* layers, int64_t T,
+                                const int64_t* activated, const uint8_t* resident_before,
+                                const uint8_t* evicted, moe_text** doc);
+
 /* ---- synthetic weights (counter hash), shared with oracle/weights.c ---------------- */
 
 /* bf16 bits of element `index` of tensor `tensor_id` for seed `seed`, scaled to unit

@@ -32,6 +32,7 @@ EXPORTED = (
     "moe_engine_kernel_times", "moe_microbench_gemv",
     "moe_hash_weights_bf16", "moe_hash_weights_f32",
     "moe_tc_grouped_gemm_bf16", "moe_tc_grouped_swiglu_bf16",
+    "moe_text_data", "moe_text_size", "moe_text_free", "moe_format_trace", "moe_format_event_log",
 )
 
 
@@ -102,6 +103,12 @@ _SIGNATURES = {
     "moe_hash_weights_bf16": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
     "moe_hash_weights_f32": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
     "moe_tc_grouped_gemm_bf16": ([_P, _P, _P, _I32, _P, _I32, _I32, _I32, _I32, ctypes.POINTER(_F32), _P], _I32),
+    "moe_text_data": ([_P], ctypes.c_void_p),
+    "moe_text_size": ([_P], _I64),
+    "moe_text_free": ([_P], None),
+    "moe_format_trace": ([_I32, _I32, _I32, _I32, _I64, _P, _P, ctypes.POINTER(_P)], _I32),
+    "moe_format_event_log": ([ctypes.c_char_p, _I32, _I32, _I32, _I32, _I64, _I32, _P, _I64, _P, _P,
+                              _P, ctypes.POINTER(_P)], _I32),
     "moe_tc_grouped_swiglu_bf16": ([_P, _P, _P, _I32, _P, _I32, _I32, _I32, ctypes.POINTER(_F32), _P], _I32),
 }
 
@@ -159,6 +166,15 @@ def stream_ptr(stream=None) -> int:
 
     s = stream if stream is not None else torch.cuda.current_stream()
     return int(s.cuda_stream)
+
+
+def take_text(handle) -> bytes:
+    """Copy a library-owned moe_text into Python bytes and free it."""
+    lib_ = load_library()
+    try:
+        return ctypes.string_at(lib_.moe_text_data(handle), lib_.moe_text_size(handle))
+    finally:
+        lib_.moe_text_free(handle)
 
 
 def kernel_launches() -> int:

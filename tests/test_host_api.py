@@ -260,3 +260,50 @@ def test_exhaustive_lru_lfu_small_alphabet_oracle():
                 for t, (before, evicted) in enumerate(straight([[a] for a in assignment], C, pol)):
                     assert np.flatnonzero(rb[t]).tolist() == before
                     assert np.flatnonzero(ev[t]).tolist() == evicted
+
+
+def _ref_dump(obj):
+    import json
+
+    return json.dumps(obj, separators=(",", ":"))
+
+
+def test_native_jsonl_long_traces_match_json_dumps():
+    """Long traces go through the multi-threaded native path (> 64K lines): same bytes as the
+    reference writers' json.dumps (traces.py:267-312, simulate.py:187-226) restated here."""
+    import numpy as np
+
+    from paper_2511_05814_b200.simulate import CacheEventLog, SimConfig, format_event_log
+    from paper_2511_05814_b200.traces import ActivationTrace, ModelShape, SpeculationTrace, format_trace
+
+    rng = np.random.default_rng(5)
+    T, L, E, K = 3000, 32, 8, 2
+    acts = np.sort(np.stack([rng.permutation(E)[:K] for _ in range(T * L)]), axis=1).reshape(T, L, K)
+    shape = ModelShape(L, E, K)
+    want = [_ref_dump({"kind": "activation", "num_layers": L, "num_experts": E, "top_k": K})]
+    want += [_ref_dump({"t": t, "l": l, "a": acts[t, l].tolist()}) for t in range(T) for l in range(L)]
+    assert format_trace(ActivationTrace(shape, acts)) == ("\n".join(want) + "\n").encode()
+    g = np.sort(np.stack([rng.permutation(E)[:K] for _ in range(T * (L - 1))]), axis=1).reshape(T, L - 1, K)
+    want = [_ref_dump({"kind": "speculation", "num_layers": L, "num_experts": E, "top_k": K})]
+    want += [_ref_dump({"t": t, "l": j + 1, "g": g[t, j].tolist(), "a": acts[t, j + 1].tolist()})
+             for t in range(T) for j in range(L - 1)]
+    sp = SpeculationTrace(shape, g, np.ascontiguousarray(acts[:, 1:]))
+    assert format_trace(sp) == ("\n".join(want) + "\n").encode()
+    rb = (rng.random((L, T, E)) < 0.5).astype(np.uint8)
+    ev = (rng.random((L, T, E)) < 0.2).astype(np.uint8)
+    layers = tuple(range(L))
+    log = CacheEventLog(config=SimConfig(policy=PolicyKind.parse("lfu-aged:0.5:16"), cache_size=4,
+                                         warmup_tokens=7),
+                        shape=shape, layers=layers,
+                        activated={l: np.ascontiguousarray(acts[:, l]) for l in layers},
+                        resident_before={l: rb[l] for l in layers},
+                        evicted={l: ev[l] for l in layers}, num_tokens=T)
+    want = [_ref_dump({"kind": "events", "policy": "lfu-aged:0.5:16", "cache_size": 4,
+                       "num_layers": L, "num_experts": E, "top_k": K, "warmup_tokens": 7})]
+    for t in range(T):
+        for l in layers:
+            a = set(acts[t, l].tolist())
+            r = set(np.flatnonzero(rb[l, t]).tolist())
+            want.append(_ref_dump({"t": t, "l": l, "cached": sorted(r), "hit": sorted(a & r),
+                                   "miss": sorted(a - r), "evict": sorted(np.flatnonzero(ev[l, t]).tolist())}))
+    assert format_event_log(log) == ("\n".join(want) + "\n").encode()
