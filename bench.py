@@ -64,6 +64,9 @@ def parse_args():
                    help="configs[3]: prefill this many tokens (tcgen05 GEMM path), 0 = skip")
     p.add_argument("--prefill-decode", type=int, default=8,
                    help="decode tokens timed after the prefill (configs[3] says 256; bounded here)")
+    p.add_argument("--trace-variants", default="zipf:1.0",
+                   help="trace-driven decode (SURVEY 8f.3): comma list of zipf:<skew> / "
+                        "markov:<repeat_prob>; LRU and LFU on each; '' = skip")
     p.add_argument("--shared-store", action="store_true",
                    help="host experts in a node-shared segment (automatic when WORLD_SIZE > 1)")
     return p.parse_args()
@@ -431,6 +434,7 @@ def run_ours(args, world, rank, local):
                                                  args.e2e_steps, world)
             e2e = {"value": e_tps, "unit": "tokens/s",
                    "h2d_bytes_per_step": D * 4, "d2h_bytes_per_step": D * 4}
+    trace_driven = run_trace_driven(args, eng, inputs, stream, world) if args.trace_variants else None
     prefill = None
     if args.prefill_tokens > 0:
         prefill = run_prefill(args, eng, inputs, base, stream, world, pcie_peak)
@@ -503,6 +507,8 @@ def run_ours(args, world, rank, local):
     }
     if cpu:
         line["speedup_vs_cpu_port"] = head["tokens_per_s"] / cpu["value"]
+    if trace_driven:
+        line["trace_driven"] = trace_driven
     if prefill:
         tf_peak = float(peaks.get("bf16_tflops", 1590.0))
         for rec in [prefill["gemm"]] + ([gemm_iso] if gemm_iso else []):
@@ -514,6 +520,47 @@ def run_ours(args, world, rank, local):
         prefill["gemm_isolated"] = gemm_iso
         line["prefill"] = prefill
     print(json.dumps(line), flush=True)
+
+
+def run_trace_driven(args, eng, inputs, stream, world):
+    """Decode with routing taken from a synthetic activation trace (gen_zipf / gen_markov, the
+    reference's workload generators) instead of the gate: LRU vs LFU at the bench's cache size
+    with real transfers (the paper's expert-imbalance study at Mixtral scale)."""
+    import torch
+
+    from paper_2511_05814_b200.policies import PolicyKind
+    from paper_2511_05814_b200.traces import ModelShape
+    from paper_2511_05814_b200.tracegen import MarkovParams, ZipfParams, gen_markov, gen_zipf
+
+    cfg = eng.config
+    shape = ModelShape(cfg.num_layers, cfg.num_experts, cfg.top_k)
+    n = args.warmup + args.steps
+    out = {}
+    for spec in args.trace_variants.split(","):
+        kind, _, val = spec.partition(":")
+        v = float(val) if val else (1.0 if kind == "zipf" else 0.3)
+        zp = ZipfParams(shape, n, skew_exponent=v if kind == "zipf" else 1.0, seed=args.seed)
+        tr = gen_zipf(zp) if kind == "zipf" else gen_markov(MarkovParams(shape, n, v, zp, seed=args.seed))
+        for pol in ("lru", "lfu"):
+            eng.set_mode(policy=PolicyKind.parse(pol), cache_size=args.cache_size, prefetch="off")
+            eng.decode_device(inputs[: args.warmup], routing=tr.activations[: args.warmup])
+            eng.sync()
+            s0 = eng.stats()
+            barrier(world)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            eng.decode_device(inputs[args.warmup: n], routing=tr.activations[args.warmup: n])
+            b.record(stream)
+            torch.cuda.synchronize()
+            eng.sync()
+            ms = max_over_ranks(a.elapsed_time(b), world)
+            s1 = eng.stats()
+            hits, misses = s1["hits"] - s0["hits"], s1["misses"] - s0["misses"]
+            out[f"{spec}/{pol}"] = {"tokens_per_s": args.steps / (ms / 1e3),
+                                    "hit_rate": hits / max(1, hits + misses),
+                                    "misses_per_token": misses / args.steps}
+    return out
 
 
 def run_prefill(args, eng, inputs, base, stream, world, pcie_peak):

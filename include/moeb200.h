@@ -229,6 +229,17 @@ moe_status moe_engine_decode(moe_engine* eng, const float* h_in_dev, int64_t T,
 moe_status moe_engine_prefill(moe_engine* eng, const float* h_in_dev, int64_t T,
                               float* h_out_dev, void* stream);
 
+/* Trace-driven routing: as moe_engine_decode / moe_engine_prefill, but step
+ * (t, l) activates the K experts routing_dev[(t * L + l) * K + 0..K) (int32, device; e.g. an
+ * ActivationTrace from gen_zipf / gen_markov or a recorded trace) instead of the gate's top-k.
+ * The gate's softmax still weights them; caches, transfers and the FFN run as usual, so the
+ * event log equals the reference's simulate() of that trace.  Ids out of range or repeated in
+ * a step flag the step (moe_engine_sync -> MOE_INVALID_CONFIG). */
+moe_status moe_engine_decode_routed(moe_engine* eng, const float* h_in_dev, int64_t T,
+                                    float* h_out_dev, const int32_t* routing_dev, void* stream);
+moe_status moe_engine_prefill_routed(moe_engine* eng, const float* h_in_dev, int64_t T,
+                                     float* h_out_dev, const int32_t* routing_dev, void* stream);
+
 /* Block until the engine's outstanding work is complete; reports MOE_NONFINITE if any
  * gate produced non-finite logits since the last call. */
 moe_status moe_engine_sync(moe_engine* eng);
@@ -273,6 +284,19 @@ moe_status moe_tc_grouped_gemm_bf16(const uint16_t* A, const uint16_t* B, float*
 moe_status moe_tc_grouped_swiglu_bf16(const uint16_t* X, const uint16_t* W13, uint16_t* act,
                                       int32_t G, const int32_t* group_m, int32_t f, int32_t d,
                                       int32_t iters, float* ms_per_iter, void* stream);
+
+/* ---- synthetic routing workloads (tracegen) ---------------------------------------------- */
+
+/* kernels.sample_zipf_layer for all L layers at once (kernels.py:150-184): weights (L, E) f64,
+ * uniforms (L, T, K) f64 (the reference's per-layer rng.random((T, K)) draws, tracegen.py:86),
+ * out (T, L, K) int64 rows ascending.  Device pointers; E <= 64. */
+moe_status moe_sample_zipf(const double* weights_dev, int32_t L, int32_t E, int64_t T, int32_t K,
+                           const double* uniforms_dev, int64_t* out_dev, void* stream);
+/* kernels.sample_markov_layer for all L layers (kernels.py:187-232): u_retain / u_draw
+ * (L, T, K) f64 (tracegen.py:104-105), out (T, L, K) int64. */
+moe_status moe_sample_markov(const double* weights_dev, int32_t L, int32_t E, int64_t T, int32_t K,
+                             double repeat_prob, const double* u_retain_dev,
+                             const double* u_draw_dev, int64_t* out_dev, void* stream);
 
 /* ---- trace / event-log JSONL (host only, no CUDA) ------------------------------------ */
 

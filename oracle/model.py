@@ -283,3 +283,64 @@ def replay_layers(acts: np.ndarray, E: int, C: int, policy: int, df=1.0, dp=1):
     for l in range(L):
         rb[l], ev[l] = replay_policy(np.ascontiguousarray(acts[:, l, :]), E, C, policy, df, dp)
     return rb, ev
+
+
+def sample_layer(weights, T, K, uniforms, repeat_prob=None, u_retain=None):
+    """ORACLE restatement of kernels.sample_zipf_layer (kernels.py:150-184) and, with
+    repeat_prob / u_retain, sample_markov_layer (kernels.py:187-232): sequential renormalised
+    draws without replacement, plain-Python fp64 loops in the reference's order."""
+    E = len(weights)
+    out = np.zeros((T, K), np.int64)
+    for t in range(T):
+        avail = [True] * E
+        filled = 0
+        if repeat_prob is not None and t > 0:
+            for j in range(K):
+                prev = int(out[t - 1, j])
+                if u_retain[t, j] < repeat_prob:
+                    out[t, filled] = prev
+                    avail[prev] = False
+                    filled += 1
+        draws = 0
+        while filled < K:
+            total = 0.0
+            for e in range(E):
+                if avail[e]:
+                    total += float(weights[e])
+            x = float(uniforms[t, draws]) * total
+            acc, chosen = 0.0, -1
+            for e in range(E):
+                if avail[e]:
+                    acc += float(weights[e])
+                    if x < acc:
+                        chosen = e
+                        break
+            if chosen == -1:
+                chosen = max(e for e in range(E) if avail[e])
+            out[t, filled] = chosen
+            avail[chosen] = False
+            filled += 1
+            draws += 1
+        out[t] = np.sort(out[t])
+    return out
+
+
+def gen_trace(kind, L, E, K, T, skew, per_layer_permutation, repeat_prob, seed):
+    """ORACLE restatement of tracegen.gen_zipf / gen_markov (tracegen.py:65-112), same RNG
+    draw order, sampling by sample_layer.  Returns acts (T, L, K)."""
+    rng = np.random.default_rng(seed)
+    rank_w = np.arange(1, E + 1, dtype=np.float64) ** (-skew)
+    weights = np.empty((L, E))
+    shared = rng.permutation(E)
+    for l in range(L):
+        perm = rng.permutation(E) if per_layer_permutation else shared
+        weights[l, perm] = rank_w
+    acts = np.zeros((T, L, K), np.int64)
+    for l in range(L):
+        if kind == "zipf":
+            acts[:, l] = sample_layer(weights[l], T, K, rng.random((T, K)))
+        else:
+            ur = rng.random((T, K))
+            ud = rng.random((T, K))
+            acts[:, l] = sample_layer(weights[l], T, K, ud, repeat_prob, ur)
+    return acts

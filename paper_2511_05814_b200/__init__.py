@@ -40,6 +40,7 @@ from .toymoe import (
     run_model,
     speculate_next,
 )
+from .tracegen import MarkovParams, ZipfParams, gen_markov, gen_zipf, repeat_rate
 from .engine import EngineConfig, OffloadEngine
 
 __version__ = "0.1.0"

@@ -33,6 +33,7 @@ EXPORTED = (
     "moe_hash_weights_bf16", "moe_hash_weights_f32",
     "moe_tc_grouped_gemm_bf16", "moe_tc_grouped_swiglu_bf16",
     "moe_text_data", "moe_text_size", "moe_text_free", "moe_format_trace", "moe_format_event_log",
+    "moe_sample_zipf", "moe_sample_markov", "moe_engine_decode_routed", "moe_engine_prefill_routed",
 )
 
 
@@ -103,6 +104,10 @@ _SIGNATURES = {
     "moe_hash_weights_bf16": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
     "moe_hash_weights_f32": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
     "moe_tc_grouped_gemm_bf16": ([_P, _P, _P, _I32, _P, _I32, _I32, _I32, _I32, ctypes.POINTER(_F32), _P], _I32),
+    "moe_sample_zipf": ([_P, _I32, _I32, _I64, _I32, _P, _P, _P], _I32),
+    "moe_sample_markov": ([_P, _I32, _I32, _I64, _I32, _F64, _P, _P, _P, _P], _I32),
+    "moe_engine_decode_routed": ([_P, _P, _I64, _P, _P, _P], _I32),
+    "moe_engine_prefill_routed": ([_P, _P, _I64, _P, _P, _P], _I32),
     "moe_text_data": ([_P], ctypes.c_void_p),
     "moe_text_size": ([_P], _I64),
     "moe_text_free": ([_P], None),

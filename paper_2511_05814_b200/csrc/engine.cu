@@ -608,6 +608,11 @@ moe_status moe_engine_reset(moe_engine* g) {
 
 moe_status moe_engine_decode(moe_engine* g, const float* h_in_dev, int64_t T, float* h_out_dev,
                              void* stream) {
+  return moe_engine_decode_routed(g, h_in_dev, T, h_out_dev, nullptr, stream);
+}
+
+moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_t T,
+                                    float* h_out_dev, const int32_t* routing_dev, void* stream) {
   MOE_REQUIRE(g, "null engine");
   MOE_REQUIRE(T >= 0, "negative token count");
   MOE_CUDA(cudaSetDevice(g->device));
@@ -768,7 +773,8 @@ moe_status moe_engine_decode(moe_engine* g, const float* h_in_dev, int64_t T, fl
                     c.cache_size + (c.prefetch ? g->S : 0), c.policy, c.decay_factor, c.decay_period, c.record_speculation,
                     c.prefetch, c.renormalize, seq, g->states, trec + l, g->mail_d,
                     g->ctl_d, g->err, g->dstats, c.rms_norm, c.rms_eps, g->h_norm,
-                    g->gate_phase_ns, g->bf16 ? g->gate_part : nullptr, grid_mix, g->norm_scale};
+                    g->gate_phase_ns, g->bf16 ? g->gate_part : nullptr, grid_mix, g->norm_scale,
+                    routing_dev ? routing_dev + (static_cast<size_t>(t) * L + l) * K : nullptr};
       if (c.num_experts <= 8)
         gate_cache_kernel<8><<<1, kGateThreads, 0, s>>>(gp);
       else
@@ -856,6 +862,10 @@ moe_status moe_engine_sync(moe_engine* g) {
     if (h & 1) {
       set_error("gate logits are not finite");
       return MOE_NONFINITE;
+    }
+    if (h & 4) {
+      set_error("routed activations out of range or repeated within a step");
+      return MOE_INVALID_CONFIG;
     }
     set_error("cache policy found no eviction candidate");
     return MOE_INVALID_CONFIG;

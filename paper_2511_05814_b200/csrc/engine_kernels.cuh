@@ -246,6 +246,7 @@ struct GateParams {
   const float* part;
   int nparts;
   float* norm_scale;       // out: 1/rms(h') (or 1) for the up projection's input staging
+  const int32_t* forced;   // trace-driven routing: this step's K ids, or nullptr (gate top-k)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -287,6 +288,22 @@ __device__ __forceinline__ void copy16(void* dst, const void* src, int n, int ti
   int4* d = static_cast<int4*>(dst);
   const int4* s = static_cast<const int4*>(src);
   for (int i = tid; i < n / 16; i += nthreads) d[i] = s[i];
+}
+
+// Trace-driven routing: the step's K expert ids come from a caller-supplied activation trace
+// (ActivationTrace row, ascending) instead of the gate's top-k; the gate's softmax still
+// weights them.  Returns false for ids out of range or repeated (the step is then flagged).
+__device__ __forceinline__ bool load_forced(const int32_t* forced, int K, int E, int* sel) {
+  uint32_t seen = 0;
+  bool ok = true;
+  for (int j = 0; j < K; ++j) {
+    const int e = forced[j];
+    const bool in = e >= 0 && e < E && e < 32;
+    ok = ok && in && !((seen >> (in ? e : 0)) & 1u);
+    if (in) seen |= 1u << e;
+    sel[j] = in ? e : 0;
+  }
+  return ok;
 }
 
 constexpr int kGateThreads = 512;  // d=4096: two float4 columns per thread, loads all in flight
@@ -427,7 +444,14 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
   const float ez = valid ? expf(zr - m) : 0.f;
   const float sum = warp_sum(ez);
   const float prob = ez / sum;
-  warp_topk(zr, valid && finite, p.K, sel);
+  bool routed_ok = true;
+  if (p.forced) {
+    routed_ok = load_forced(p.forced, p.K, p.E, sel);
+    if (!routed_ok) flags |= 4u;
+  } else {
+    warp_topk(zr, valid && finite, p.K, sel);
+  }
+  const bool go = finite && routed_ok;
   float psel[kMaxK];
   float ssel = 0.f;
   for (int j = 0; j < p.K; ++j) {
@@ -447,7 +471,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
   const long long t = S.step;
   uint32_t rbb = 0, evb = 0;
   bool ok = true;
-  if (finite) {
+  if (go) {
     ok = warp_policy_step<1>(st, p.E, p.C, p.policy, p.decay_factor, p.decay_period, t,
                              [&](int j) { return static_cast<long long>(acts[j]); }, p.K,
                              [&](int) { return 0ll; }, rbb, evb);
@@ -457,7 +481,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
   const uint32_t rb = __ballot_sync(FULL, rbb & 1u) & emask;
   const uint32_t ev = __ballot_sync(FULL, evb & 1u) & emask;
   const uint32_t res_after = __ballot_sync(FULL, st.resident & 1u) & emask;
-  if (valid && finite) {
+  if (valid && go) {
     S.freq[lane] = st.freq[0];
     S.last_touch[lane] = st.last_touch[0];
   }
@@ -488,7 +512,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
     rec->flags = flags;
     if (flags) atomicOr(p.err, static_cast<int>(flags));
     int nd = 0, nc = 0, np = 0;
-    if (finite && ok) {
+    if (go && ok) {
       S.resident = res_after;
       S.step = t + 1;
       int hits = 0;

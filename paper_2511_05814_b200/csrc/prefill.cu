@@ -185,6 +185,12 @@ using namespace moe;
 
 extern "C" moe_status moe_engine_prefill(moe_engine* g, const float* h_in_dev, int64_t T64,
                                          float* h_out_dev, void* stream) {
+  return moe_engine_prefill_routed(g, h_in_dev, T64, h_out_dev, nullptr, stream);
+}
+
+extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in_dev, int64_t T64,
+                                                float* h_out_dev, const int32_t* routing_dev,
+                                                void* stream) {
   MOE_REQUIRE(g, "null engine");
   MOE_REQUIRE(g->bf16, "prefill runs the SwiGLU (bf16) engine; the toy engine decodes token by token");
   const moe_engine_config& c = g->cfg;
@@ -283,7 +289,8 @@ extern "C" moe_status moe_engine_prefill(moe_engine* g, const float* h_in_dev, i
     // ---- gate, one warp per token ----
     PfGateParams gp{pf->x, pf->hm, g->gate_w + static_cast<size_t>(l) * E * d,
                     g->gate_b + static_cast<size_t>(l) * E, g->ring, tok0, c.max_tokens, L, l, T, d,
-                    E, K, c.record_speculation, c.renormalize, c.rms_norm, c.rms_eps, pf->inv, g->err};
+                    E, K, c.record_speculation, c.renormalize, c.rms_norm, c.rms_eps, pf->inv, g->err,
+                    routing_dev};
     if (E <= 8)
       pf_gate_kernel<8><<<T, 256, 0, s>>>(gp);
     else

@@ -95,6 +95,7 @@ struct PfGateParams {
   float rms_eps;
   float* inv;           // [T] 1/rms(h') (1 without RMSNorm)
   int* err;
+  const int32_t* forced;  // trace-driven routing: (T, L, K) ids, or nullptr
 };
 
 // One CTA per token: every thread owns a fixed slice of the row (all its loads in flight
@@ -169,7 +170,11 @@ __global__ void __launch_bounds__(256) pf_gate_kernel(PfGateParams p) {
   const float ez = valid ? expf(zr - m) : 0.f;
   const float prob = ez / warp_sum(ez);
   int sel[kMaxK], acts[kMaxK], gs[kMaxK];
-  warp_topk(zr, valid && finite, p.K, sel);
+  bool routed_ok = true;
+  if (p.forced)
+    routed_ok = load_forced(p.forced + (static_cast<size_t>(t) * p.L + p.layer) * p.K, p.K, p.E, sel);
+  else
+    warp_topk(zr, valid && finite, p.K, sel);
   float psel[kMaxK], ssel = 0.f;
   for (int j = 0; j < p.K; ++j) {
     psel[j] = __shfl_sync(FULL, prob, sel[j] & 31);
@@ -193,8 +198,9 @@ __global__ void __launch_bounds__(256) pf_gate_kernel(PfGateParams p) {
     }
     rec->rb = 0;
     rec->ev = 0;
-    rec->flags = finite ? 0u : 1u;
-    if (!finite) atomicOr(p.err, 1);
+    const uint32_t fl = (finite ? 0u : 1u) | (routed_ok ? 0u : 4u);
+    rec->flags = fl;
+    if (fl) atomicOr(p.err, static_cast<int>(fl));
     p.inv[t] = inv_mid;
   }
 }

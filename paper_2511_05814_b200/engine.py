@@ -197,8 +197,25 @@ class OffloadEngine:
         """Cold caches (policies.warm_state) for every layer."""
         _native.check(self._lib.moe_engine_reset(self._h))
 
-    def decode_device(self, h_in, h_out=None, stream=None):
-        """Enqueue decode of h_in (T, d) float32 CUDA tensor; returns h_out without syncing."""
+    def _routing(self, routing, T):
+        """(T, L, K) expert ids (ActivationTrace, numpy or torch) -> int32 CUDA tensor."""
+        import torch
+
+        if routing is None:
+            return None
+        if hasattr(routing, "activations"):
+            routing = routing.activations
+        cfg = self.config
+        r = routing if torch.is_tensor(routing) else torch.from_numpy(np.array(routing, dtype=np.int32))
+        if tuple(r.shape) != (T, cfg.num_layers, cfg.top_k):
+            raise ConfigError(f"routing must be (T, L, K) = ({T}, {cfg.num_layers}, {cfg.top_k}), "
+                              f"got {tuple(r.shape)}")
+        return r.to(device=self._dev, dtype=torch.int32).contiguous()
+
+    def decode_device(self, h_in, h_out=None, stream=None, routing=None):
+        """Enqueue decode of h_in (T, d) float32 CUDA tensor; returns h_out without syncing.
+        routing: optional (T, L, K) activation trace that replaces the gate's top-k
+        (trace-driven mode: caches, transfers and FFN run as usual)."""
         import torch
 
         d = self.config.hidden_dim
@@ -208,12 +225,15 @@ class OffloadEngine:
         T = h_in.shape[0]
         if h_out is None:
             h_out = torch.empty_like(h_in)
-        _native.check(self._lib.moe_engine_decode(self._h, h_in.data_ptr(), T, h_out.data_ptr(),
-                                                  _native.stream_ptr(stream)))
+        r = self._routing(routing, T)
+        _native.check(self._lib.moe_engine_decode_routed(
+            self._h, h_in.data_ptr(), T, h_out.data_ptr(), r.data_ptr() if r is not None else None,
+            _native.stream_ptr(stream)))
+        self._keep = r  # the device routing must outlive the enqueued work
         self.tokens_done += T
         return h_out
 
-    def prefill_device(self, h_in, h_out=None, stream=None):
+    def prefill_device(self, h_in, h_out=None, stream=None, routing=None):
         """Enqueue a batched prefill of h_in (T, d) float32 CUDA tensor (tensor-core GEMMs,
         one H2D load per needed expert per layer); returns h_out without syncing.  Step
         records / cache traces equal those of decoding the same T tokens."""
@@ -226,18 +246,21 @@ class OffloadEngine:
         T = h_in.shape[0]
         if h_out is None:
             h_out = torch.empty_like(h_in)
-        _native.check(self._lib.moe_engine_prefill(self._h, h_in.data_ptr(), T, h_out.data_ptr(),
-                                                   _native.stream_ptr(stream)))
+        r = self._routing(routing, T)
+        _native.check(self._lib.moe_engine_prefill_routed(
+            self._h, h_in.data_ptr(), T, h_out.data_ptr(), r.data_ptr() if r is not None else None,
+            _native.stream_ptr(stream)))
+        self._keep = r
         self.tokens_done += T
         return h_out
 
-    def prefill(self, h_in) -> np.ndarray:
+    def prefill(self, h_in, routing=None) -> np.ndarray:
         """Public prefill: host (T, d) array in, host (T, d) float32 out (copies included)."""
         import torch
 
         x = torch.as_tensor(np.ascontiguousarray(h_in, dtype=np.float32))
         x = x.pin_memory().to(self._dev, non_blocking=True)
-        y = self.prefill_device(x)
+        y = self.prefill_device(x, routing=routing)
         out = y.cpu().numpy()
         self.sync()
         return out
@@ -268,13 +291,14 @@ class OffloadEngine:
     def sync(self) -> None:
         _native.check(self._lib.moe_engine_sync(self._h))
 
-    def decode(self, h_in) -> np.ndarray:
-        """Public decode: host (T, d) array in, host (T, d) float32 out (copies included)."""
+    def decode(self, h_in, routing=None) -> np.ndarray:
+        """Public decode: host (T, d) array in, host (T, d) float32 out (copies included).
+        routing: optional (T, L, K) activation trace (trace-driven mode)."""
         import torch
 
         x = torch.as_tensor(np.ascontiguousarray(h_in, dtype=np.float32))
         x = x.pin_memory().to(self._dev, non_blocking=True)
-        y = self.decode_device(x)
+        y = self.decode_device(x, routing=routing)
         out = y.cpu().numpy()
         self.sync()
         return out

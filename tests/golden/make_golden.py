@@ -11,6 +11,7 @@ It imports moesim from /root/reference/pkg/src (read-only; numba's cache is redi
   toy_t1_1024.npz      the same config at T=1024: activations, guesses + event-log digests
   toy_small.npz        small run_model configs (incl. the reference's straight-line case)
   forward_cases.npz    forward_token / gate_select outputs on random small models
+  tracegen.npz         gen_zipf / gen_markov traces (tracegen.py:78-112) for a set of params
   manifest.json        sha256 of every artefact + versions used
 """
 
@@ -171,13 +172,46 @@ def forward_cases(manifest):
     manifest["forward_cases.npz"] = {"cases": 6}
 
 
+# (kind, L, E, K, T, skew, per_layer_permutation, repeat_prob, seed)
+TRACEGEN = [
+    ("zipf", 4, 8, 2, 300, 1.0, True, 0.0, 0), ("zipf", 32, 8, 2, 200, 1.2, True, 0.0, 42),
+    ("zipf", 3, 8, 2, 100, 0.0, True, 0.0, 1), ("zipf", 2, 16, 4, 150, 2.5, False, 0.0, 7),
+    ("zipf", 2, 5, 5, 40, 1.0, True, 0.0, 3), ("zipf", 2, 8, 2, 0, 1.0, True, 0.0, 3),
+    ("markov", 4, 8, 2, 300, 1.0, True, 0.3, 0), ("markov", 32, 8, 2, 200, 1.2, True, 0.6, 42),
+    ("markov", 3, 8, 2, 100, 1.0, True, 1.0, 5), ("markov", 3, 8, 2, 100, 1.0, True, 0.0, 5),
+    ("markov", 2, 16, 4, 120, 0.5, False, 0.45, 9), ("markov", 2, 6, 6, 30, 1.0, True, 0.5, 2),
+]
+
+
+def tracegen_cases(manifest):
+    from moesim.tracegen import MarkovParams, ZipfParams, gen_markov, gen_zipf
+
+    rows = {}
+    for i, (kind, L, E, K, T, skew, perm, rp, seed) in enumerate(TRACEGEN):
+        shape = ModelShape(L, E, K)
+        zp = ZipfParams(shape, T, skew_exponent=skew, per_layer_permutation=perm, seed=seed)
+        if kind == "zipf":
+            tr = gen_zipf(zp)
+        else:
+            tr = gen_markov(MarkovParams(shape, T, repeat_prob=rp, base=zp, seed=seed))
+        rows[f"acts_{i}"] = tr.activations
+    np.savez_compressed(OUT / "tracegen.npz", **rows)
+    manifest["tracegen.npz"] = {"cases": [list(c) for c in TRACEGEN]}
+
+
 def main():
     manifest = {"numpy": np.__version__, "moesim": moesim.__version__, "backend": kernels.BACKEND}
+    if sys.argv[1:] == ["--only", "tracegen"]:
+        manifest = json.loads((OUT / "manifest.json").read_text())
+        tracegen_cases(manifest)
+        (OUT / "manifest.json").write_text(json.dumps(manifest, indent=1, sort_keys=True) + "\n")
+        return
     policy_streams(manifest)
     toy_t1(manifest)
     toy_t1_1024(manifest)
     toy_small(manifest)
     forward_cases(manifest)
+    tracegen_cases(manifest)
     (OUT / "manifest.json").write_text(json.dumps(manifest, indent=1, sort_keys=True) + "\n")
     print(json.dumps({k: v for k, v in manifest.items() if k.startswith("toy_t1")}, indent=1))
 
