@@ -493,6 +493,11 @@ def run_ours(args, world, rank, local):
             "bytes_per_launch": (ktimes["ffn_active_bytes"] / ktimes["ffn_active_launches"]
                                  if ktimes["ffn_active_launches"] else None),
             "achieved_incl_empty_phase_launches": ffn_all_gbs,
+            "achieved_in_kernel": (ktimes["ffn_active_bytes"] / (ktimes["ffn_kernel_ms"] / 1e3) / 1e9
+                                   if ktimes.get("ffn_kernel_ms") else None),
+            "in_kernel_note": "globaltimer span first CTA start -> last CTA end per launch; the "
+                              "CUDA-event span adds launch / front-end latency (~20 us per launch "
+                              "live, with the copy engine busy)",
             "traffic": traffic.get("dram_bytes_per_expert") if traffic else None,
             "traffic_unit": "DRAM bytes per expert (ncu, profiles/ncu_ffn_traffic.json)",
             "algorithmic_bytes_per_expert": EB,

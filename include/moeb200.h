@@ -207,6 +207,9 @@ typedef struct {
   double gemm_flops;        /* algorithmic FLOPs of those launches (2*m*n*k per group) */
   int64_t gemm_bytes;       /* algorithmic bytes: weights + activations read + outputs written */
   double prefill_ms;        /* whole-prefill device time (first kernel to last, per call, summed) */
+  double ffn_kernel_ms;     /* in-kernel span (globaltimer, first CTA start -> last CTA end) of
+                               the FFN launches that processed >= 1 expert: excludes launch
+                               latency and the host-side gaps the events see */
 } moe_kernel_times;
 moe_status moe_engine_profile(moe_engine* eng, int32_t enable);
 /* Resolves outstanding events (synchronises) and returns the running totals. */

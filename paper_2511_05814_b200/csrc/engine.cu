@@ -261,19 +261,29 @@ void resolve_profile(moe_engine* g) {
     k.ffn_expert_runs += g->prof_pending_k[i];
     for (int q = 0; q < 3; ++q) g->prof_free.push_back(e[q]);
   }
-  std::vector<long long> bytes(g->prof_ffn.size(), 0);
-  if (g->bf16 && g->prof_bytes_dev && !bytes.empty())
-    cudaMemcpy(bytes.data(), g->prof_bytes_dev, sizeof(long long) * bytes.size(),
+  std::vector<long long> slots(4 * g->prof_ffn.size(), 0);
+  if (g->bf16 && g->prof_bytes_dev && !slots.empty()) {
+    cudaMemcpy(slots.data(), g->prof_bytes_dev, sizeof(long long) * slots.size(),
                cudaMemcpyDeviceToHost);
+    cudaMemset(g->prof_bytes_dev, 0, sizeof(long long) * slots.size());
+  }
+  std::vector<long long> bytes(g->prof_ffn.size(), 0);
+  for (size_t i = 0; i < bytes.size(); ++i) bytes[i] = slots[4 * i];
+  static const bool dump = getenv("MOE_PROF_DUMP") != nullptr;
   for (size_t i = 0; i < g->prof_ffn.size(); ++i) {
     auto& e = g->prof_ffn[i];
     const float ms = elapsed(e[0], e[1]);
+    if (dump)
+      fprintf(stderr, "[moe-prof] ffn %zu %.4f ms %lld B kernel %.4f ms\n", i, ms, (long long)bytes[i],
+              slots.empty() ? 0.0 : (slots[4 * i + 2] - (0x7fffffffffffffffll - slots[4 * i + 1])) / 1e6);
     k.ffn_ms += ms;
     k.ffn_launches += 1;
     if (!g->bf16 || bytes[i] > 0) {
       k.ffn_active_ms += ms;
       k.ffn_active_bytes += bytes[i];
       k.ffn_active_launches += 1;
+      const long long t0 = 0x7fffffffffffffffll - slots[4 * i + 1], t1 = slots[4 * i + 2];
+      if (g->bf16 && slots[4 * i + 1] > 0 && t1 > t0) k.ffn_kernel_ms += (t1 - t0) / 1e6;
     }
     g->prof_free.push_back(e[0]);
     g->prof_free.push_back(e[1]);
@@ -650,10 +660,12 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
   const int grid_mix = stream_grid(1), grid_ffn = stream_grid(K);
   // one expert-FFN launch group: phase 0 = hits, 1 = misses; only = -1 all, i = i-th miss
   if (g->profiling && !g->prof_bytes_dev)
-    MOE_CUDA(cudaMalloc(&g->prof_bytes_dev, sizeof(long long) * moe_engine::kProfSlots));
+    MOE_CUDA(cudaMalloc(&g->prof_bytes_dev, 4 * sizeof(long long) * moe_engine::kProfSlots));
+  if (g->profiling && g->prof_ffn.empty())
+    MOE_CUDA(cudaMemsetAsync(g->prof_bytes_dev, 0, 4 * sizeof(long long) * moe_engine::kProfSlots, s));
   auto prof_slot = [&]() -> long long* {
     if (!g->profiling || g->prof_ffn.size() >= static_cast<size_t>(moe_engine::kProfSlots)) return nullptr;
-    return g->prof_bytes_dev + g->prof_ffn.size();
+    return g->prof_bytes_dev + 4 * g->prof_ffn.size();
   };
   auto prof_begin = [&](std::array<cudaEvent_t, 2>& ev) -> moe_status {
     if (g->profiling) {

@@ -48,7 +48,8 @@ struct StreamParams {
   int only;                // -1: every expert of the phase; i: just the i-th (ascending id)
   float* act;              // [K][f]
   float* yout;             // [K][d]
-  long long* prof_bytes;   // optional: weight bytes this launch streams (profiling)
+  long long* prof_bytes;   // optional profiling slot [4]: weight bytes this launch streams,
+                           // max(LLONG_MAX - CTA start ns), max(consumer end ns) (globaltimer)
   // MIX: per-CTA partial gate logits over the CTA's rows (see GateParams::part)
   const float* gate_w;     // this layer's gate [E][d]
   const float* gate_w_next;  // next layer's gate (early speculative guess) or nullptr
@@ -103,8 +104,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
   const char* blk[kMaxK];
   int n_active = 1;
   if (MODE != kModeMix) n_active = stream_active(p, slot, blk);
-  if (p.prof_bytes && blockIdx.x == 0 && threadIdx.x == 0)
-    *p.prof_bytes = static_cast<long long>(n_active) * NM * R * C * 2;
+  if (p.prof_bytes && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&p.prof_bytes[1], 0x7fffffffffffffffll - static_cast<long long>(t));
+    if (blockIdx.x == 0) p.prof_bytes[0] = static_cast<long long>(n_active) * NM * R * C * 2;
+    if (n_active == 0) atomicMax(&p.prof_bytes[2], static_cast<long long>(t));
+  }
   if (n_active == 0) return;
   const int a = static_cast<int>((static_cast<long long>(blockIdx.x) * n_active) / gridDim.x);
   const int c0 = static_cast<int>((static_cast<long long>(a) * gridDim.x + n_active - 1) / n_active);
@@ -284,6 +290,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
         if (lane == 0) p.part[static_cast<size_t>(blockIdx.x) * njob + q] = acc;
       }
     }
+  }
+  if (p.prof_bytes && lane == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&p.prof_bytes[2], static_cast<long long>(t));
   }
 }
 

@@ -43,5 +43,5 @@ def test_engine_struct_layout_matches_header():
     assert ctypes.sizeof(_native.EngineConfigC) == 96
     # 11 int64 + double + 2 int64 (moe_stats)
     assert ctypes.sizeof(_native.StatsC) == 14 * 8
-    # 4 double + 5 int64 + double + 2 int64 + double + int64 + double + int64 + double
-    assert ctypes.sizeof(_native.KernelTimesC) == 17 * 8
+    # 4 double + 5 int64 + double + 2 int64 + double + int64 + double + int64 + 2 double
+    assert ctypes.sizeof(_native.KernelTimesC) == 18 * 8
