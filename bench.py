@@ -67,6 +67,8 @@ def parse_args():
     p.add_argument("--trace-variants", default="zipf:1.0",
                    help="trace-driven decode (SURVEY 8f.3): comma list of zipf:<skew> / "
                         "markov:<repeat_prob>; LRU and LFU on each; '' = skip")
+    p.add_argument("--tiny-tokens", type=int, default=1024,
+                   help="configs[0]: tiny toy-MoE decode (L=4,E=8,K=2,d=256), LRU C=2; 0 = skip")
     p.add_argument("--shared-store", action="store_true",
                    help="host experts in a node-shared segment (automatic when WORLD_SIZE > 1)")
     return p.parse_args()
@@ -440,6 +442,7 @@ def run_ours(args, world, rank, local):
         prefill = run_prefill(args, eng, inputs, base, stream, world, pcie_peak)
     eng.close()
     gemm_iso = isolated_gemm(D, F) if rank == 0 and args.prefill_tokens > 0 else None
+    tiny = run_tiny(args) if rank == 0 and world == 1 and args.tiny_tokens > 0 else None
     if store is not None:
         barrier(world)
         store.close()
@@ -514,6 +517,8 @@ def run_ours(args, world, rank, local):
         line["speedup_vs_cpu_port"] = head["tokens_per_s"] / cpu["value"]
     if trace_driven:
         line["trace_driven"] = trace_driven
+    if tiny:
+        line["tiny"] = tiny
     if prefill:
         tf_peak = float(peaks.get("bf16_tflops", 1590.0))
         for rec in [prefill["gemm"]] + ([gemm_iso] if gemm_iso else []):
@@ -525,6 +530,67 @@ def run_ours(args, world, rank, local):
         prefill["gemm_isolated"] = gemm_iso
         line["prefill"] = prefill
     print(json.dumps(line), flush=True)
+
+
+def run_tiny(args):
+    """configs[0]: the reference's own tiny config (ToyModelConfig(ModelShape(4, 8, 2), d=256,
+    alpha=0.1, seed=42), T tokens, LRU cache 2/layer) through the engine (toy tanh experts, f32),
+    beside the reference algorithm on the host (oracle port of toymoe.run_model + the policy
+    replay, numpy fp64).  Latency-bound: reported as tokens/s, us/token and launches/token,
+    with the engine's activation trace checked against the oracle's."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from oracle.model import replay_layers
+    from paper_2511_05814_b200 import _native
+    from paper_2511_05814_b200.engine import EngineConfig, OffloadEngine
+    from paper_2511_05814_b200.policies import PolicyKind
+    from paper_2511_05814_b200.toymoe import ToyModelConfig, ToyMoeModel
+    from paper_2511_05814_b200.traces import ModelShape
+
+    Lt, Et, Kt, dt, T = 4, 8, 2, 256, args.tiny_tokens
+    cfg = ToyModelConfig(ModelShape(Lt, Et, Kt), hidden_dim=dt, mixing_scale=0.1, seed=42, tokens=T)
+    model, rng = ToyMoeModel.build(cfg)
+    inputs = rng.standard_normal((T, dt))
+    ecfg = EngineConfig(num_layers=Lt, num_experts=Et, top_k=Kt, hidden_dim=dt, expert_kind="toy_tanh",
+                        cache_size=2, policy=PolicyKind.lru(), mixing_scale=0.1, max_tokens=T + 64)
+    stream = torch.cuda.current_stream()
+    with OffloadEngine(ecfg) as eng:
+        eng.load_toy_model(model)
+        x = torch.from_numpy(inputs.astype(np.float32)).cuda()
+        eng.decode_device(x[:16])            # warm-up
+        eng.sync()
+        eng.reset()
+        n0 = _native.kernel_launches()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        eng.decode_device(x)
+        b.record(stream)
+        torch.cuda.synchronize()
+        eng.sync()
+        ms = a.elapsed_time(b)
+        launches = _native.kernel_launches() - n0
+        rec = eng.records(16, T)
+        eng.reset()
+        t0 = time.perf_counter()
+        eng.decode(inputs[:64].astype(np.float32))   # public API, host arrays, synced
+        e2e_tps = 64 / (time.perf_counter() - t0)
+    w = oracle.toy_weights(Lt, Et, dt, 1.0, 42, T)
+    t0 = time.perf_counter()
+    acts, _, _ = oracle.toy_run_model(Lt, Et, Kt, dt, 0.1, 1.0, 42, T, weights=w)
+    replay_layers(acts, Et, 2, 0)
+    cpu_s = time.perf_counter() - t0
+    return {"workload": "configs[0]: tiny MoE (4 layers, 8 experts top-2, d=256) decode, LRU cache "
+                        "2/layer (toy tanh experts, f32 on the GPU)",
+            "tokens": T, "tokens_per_s": T / (ms / 1e3), "us_per_token": ms * 1e3 / T,
+            "launches_per_token": launches / T, "e2e_tokens_per_s": e2e_tps,
+            "trace_equals_oracle": bool(np.array_equal(rec["acts"], acts)),
+            "cpu_baseline": {"value": T / cpu_s, "unit": "tokens/s", "cores": os.cpu_count(),
+                             "kind": "port",
+                             "sample": f"oracle toy_run_model (numpy fp64, toymoe.py:159-190) + "
+                                       f"policy replay, {T} tokens"}}
 
 
 def run_trace_driven(args, eng, inputs, stream, world):

@@ -45,6 +45,13 @@ enum { MOE_P_LRU = 0, MOE_P_LFU = 1, MOE_P_LFU_AGED = 2, MOE_P_OPT = 3 };
  * SWIGLU the Mixtral-shaped north-star expert (w2 . (silu(w1 h) * w3 h)). */
 enum { MOE_EXPERT_TOY_TANH_F32 = 0, MOE_EXPERT_SWIGLU_BF16 = 1 };
 
+/* Transfer engines.  COPY_ENGINE: the device posts its decision to a mapped
+ * mailbox and the host forwards cudaMemcpyAsync on a copy stream (peak link bandwidth, one host
+ * round trip per layer).  SM: a fetch kernel reads the missed experts from the mapped pinned
+ * store itself (no host in the loop; ~15 % below the copy engine's bandwidth).  AUTO: SM for
+ * experts <= 16 MiB (latency-bound), the copy engine otherwise; prefetch needs the copy engine. */
+enum { MOE_TRANSFER_AUTO = 0, MOE_TRANSFER_COPY_ENGINE = 1, MOE_TRANSFER_SM = 2 };
+
 /* Speculative prefetch issue point. */
 enum {
   MOE_PREFETCH_OFF = 0,
@@ -136,6 +143,7 @@ typedef struct {
                              Mixtral; keeps the SwiGLU residual stream finite.  0: reference
                              toy semantics (no norm, toymoe.py:138-146). */
   float rms_eps;          /* RMSNorm epsilon (Mixtral: 1e-5) */
+  int32_t transfer;       /* MOE_TRANSFER_*: how missed experts reach HBM */
 } moe_engine_config;
 
 typedef struct {

@@ -19,6 +19,7 @@ MOE_OK, MOE_INVALID_CONFIG, MOE_NONFINITE, MOE_CUDA_ERROR, MOE_OOM = range(5)
 P_LRU, P_LFU, P_LFU_AGED, P_OPT = range(4)
 EXPERT_TOY_TANH_F32, EXPERT_SWIGLU_BF16 = 0, 1
 PREFETCH_OFF, PREFETCH_EARLY = 0, 1
+TRANSFER_AUTO, TRANSFER_COPY_ENGINE, TRANSFER_SM = 0, 1, 2
 
 # Every exported symbol, as declared in include/moeb200.h (checked by the CPU test suite).
 EXPORTED = (
@@ -48,6 +49,7 @@ class EngineConfigC(ctypes.Structure):
         ("record_speculation", ctypes.c_int32), ("max_tokens", ctypes.c_int32),
         ("chunk_bytes", ctypes.c_int64), ("prefetch_depth", ctypes.c_int32),
         ("device", ctypes.c_int32), ("rms_norm", ctypes.c_int32), ("rms_eps", ctypes.c_float),
+        ("transfer", ctypes.c_int32),
     ]
 
 

@@ -343,6 +343,10 @@ moe_status moe_engine_create_ex(const moe_engine_config* cfg_in, void* store, in
   MOE_REQUIRE(c.expert_kind != MOE_EXPERT_SWIGLU_BF16 ||
                   (c.hidden_dim % 8 == 0 && c.ffn_dim >= 8 && c.ffn_dim % 8 == 0),
               "SwiGLU experts need hidden_dim and ffn_dim multiples of 8");
+  MOE_REQUIRE(c.transfer >= MOE_TRANSFER_AUTO && c.transfer <= MOE_TRANSFER_SM,
+              "unknown transfer mode %d", c.transfer);
+  MOE_REQUIRE(!(c.transfer == MOE_TRANSFER_SM && c.prefetch),
+              "speculative prefetch runs on the copy engine (transfer=SM has no staging path)");
   MOE_REQUIRE(c.cache_size + (c.prefetch ? c.top_k : 0) <= kMaxBuf,
               "cache_size + staging buffers must be <= %d", kMaxBuf);
 
@@ -362,6 +366,8 @@ moe_status moe_engine_create_ex(const moe_engine_config* cfg_in, void* store, in
     g->f = g->dpad;
     g->expert_bytes = 2ll * g->dpad * g->dpad * 4;
   }
+  g->sm_transfer = c.transfer == MOE_TRANSFER_SM ||
+                   (c.transfer == MOE_TRANSFER_AUTO && !c.prefetch && g->expert_bytes <= (16ll << 20));
   g->S = c.prefetch ? c.top_k : 0;
   g->NB = c.cache_size + g->S;
   g->cap_C = c.cache_size;
@@ -414,6 +420,7 @@ moe_status create_resources(moe_engine* g) {
   memset(g->ctl_h, 0, sizeof(HostControl));
   MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g->ctl_d), g->ctl_h, 0));
   MOE_CUDA(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+
   // every event the forwarder will need, created up front (no allocation on the hot path)
   for (int i = 0; i < 64; ++i) {
     cudaEvent_t e = nullptr;
@@ -441,6 +448,11 @@ moe_status create_resources(moe_engine* g) {
     TRY(g->store.attach(g->ext_store, store_bytes));
   } else {
     TRY(g->store.allocate(store_bytes));
+  }
+  {
+    void* dp = nullptr;
+    MOE_CUDA(cudaHostGetDevicePointer(&dp, g->store.base, 0));
+    g->store_dev = static_cast<const char*>(dp);
   }
   reset_states_kernel<<<L, 64>>>(g->states, L, g->NB);
   MOE_LAUNCHED();
@@ -477,6 +489,11 @@ moe_status moe_engine_destroy(moe_engine* g) {
     for (auto e : a) cudaEventDestroy(e);
   if (g->prof_bytes_dev) cudaFree(g->prof_bytes_dev);
   if (g->pf) prefill_release(g->pf);
+  if (g->graph_exec) cudaGraphExecDestroy(g->graph_exec);
+  if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
+  for (void* p : {static_cast<void*>(g->cursor), static_cast<void*>(g->cur_rec), static_cast<void*>(g->x_cur),
+                  static_cast<void*>(g->out_cur), static_cast<void*>(g->x_stage), static_cast<void*>(g->out_stage)})
+    if (p) cudaFree(p);
   if (g->gate_phase_ns) {
     unsigned long long h[8] = {};
     cudaMemcpy(h, g->gate_phase_ns, sizeof(h), cudaMemcpyDeviceToHost);
@@ -493,6 +510,7 @@ moe_status moe_engine_destroy(moe_engine* g) {
   if (g->mail_h) cudaFreeHost(g->mail_h);
   if (g->ctl_h) cudaFreeHost(g->ctl_h);
   if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
+
   g->store.release();
   delete g;
   return MOE_OK;
@@ -735,11 +753,13 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
     MOE_LAUNCHED();
     return MOE_OK;
   };
-  for (int64_t t = 0; t < T; ++t) {
-    const long long tok = g->tokens_done + t;
-    StepRecord* trec = g->ring + (tok % c.max_tokens) * L;
-    const float* x = h_in_dev + t * d;
-    if (D != d) {
+  // One token through all layers.  Graph mode (fixed = true): token-invariant pointers --
+  // the input in x_cur, records in cur_rec, the output in out_cur -- so the sequence can be
+  // captured once and replayed (token_begin / token_end move them to / from the rings).
+  auto run_token = [&](long long tok, int64_t t, bool fixed) -> moe_status {
+    StepRecord* trec = fixed ? g->cur_rec : g->ring + (tok % c.max_tokens) * L;
+    const float* x = fixed ? g->x_cur : h_in_dev + t * d;
+    if (!fixed && D != d) {
       MOE_CUDA(cudaMemcpyAsync(g->x_pad, x, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
       x = g->x_pad;
     }
@@ -783,7 +803,8 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       if (g->profiling) MOE_CUDA(cudaEventRecord(pe[1], s));
       GateParams gp{hm, g->h_in, g->gate_w, g->gate_b, l, L, c.num_experts, K, D, c.cache_size,
                     c.cache_size + (c.prefetch ? g->S : 0), c.policy, c.decay_factor, c.decay_period, c.record_speculation,
-                    c.prefetch, c.renormalize, seq, g->states, trec + l, g->mail_d,
+                    c.prefetch, c.renormalize, seq, g->states, trec + l,
+                    g->sm_transfer ? nullptr : g->mail_d,
                     g->ctl_d, g->err, g->dstats, c.rms_norm, c.rms_eps, g->h_norm,
                     g->gate_phase_ns, g->bf16 ? g->gate_part : nullptr, grid_mix, g->norm_scale,
                     routing_dev ? routing_dev + (static_cast<size_t>(t) * L + l) * K : nullptr};
@@ -796,8 +817,37 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       FfnParams fp{(c.rms_norm && !g->bf16) ? g->h_norm : hm, trec + l, g->states + l,
                    g->pool + static_cast<long long>(l) * g->NB * g->expert_bytes, g->expert_bytes,
                    D, g->f, K, 0, g->act, g->y};
-      // phase 0: experts that hit run while the misses are fetched
       std::array<cudaEvent_t, 2> fev{};
+      if (g->sm_transfer) {
+        // device-driven: the SMs fetch the missed experts, then one FFN pass over all K
+        FetchParams fp2{trec + l, g->states + l,
+                        g->store_dev + static_cast<long long>(l) * c.num_experts * g->expert_bytes,
+                        g->pool + static_cast<long long>(l) * g->NB * g->expert_bytes, g->expert_bytes,
+                        K, g->dstats};
+        const long long n16 = g->expert_bytes / 16;
+        const int fgrid = static_cast<int>(std::max(1ll, std::min<long long>(296, (K * n16 + 4095) / 4096)));
+        // (a side-stream fork of the fetch beside the hits' FFN was measured: no gain on the
+        // latency-bound small configs -- the critical path keeps one up/down after the fetch)
+        fetch_kernel<<<fgrid, 512, 0, s>>>(fp2);
+        MOE_LAUNCHED();
+        fp.phase = 2;
+        TRY(prof_begin(fev));
+        TRY(launch_ffn(fp, -1));
+        TRY(prof_end(fev));
+        TRY(prof_begin(fev));
+        TRY(launch_down(fp, -1));
+        TRY(prof_end(fev));
+        if (g->profiling) {
+          g->prof_pending.push_back(pe);
+          g->prof_pending_k.push_back(K);
+        }
+        continue;
+      }
+      if (fixed) {
+        set_error("graph capture of a copy-engine step");
+        return MOE_INVALID_CONFIG;
+      }
+      // phase 0: experts that hit run while the misses are fetched
       TRY(prof_begin(fev));
       TRY(launch_ffn(fp, -1));
       TRY(prof_end(fev));
@@ -842,8 +892,8 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
         g->prof_pending_k.push_back(K);
       }
     }
-    float* out = h_out_dev + t * d;
-    float* dst = D != d ? g->out_pad : out;
+    float* out = fixed ? g->out_cur : h_out_dev + t * d;
+    float* dst = (!fixed && D != d) ? g->out_pad : out;
     std::array<cudaEvent_t, 2> fe{};
     if (g->profiling) {
       fe = {take_prof_event(g), take_prof_event(g)};
@@ -856,8 +906,73 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       MOE_CUDA(cudaEventRecord(fe[1], s));
       g->prof_final.push_back(fe);
     }
-    if (D != d)
+    if (!fixed && D != d)
       MOE_CUDA(cudaMemcpyAsync(out, g->out_pad, sizeof(float) * d, cudaMemcpyDeviceToDevice, s));
+    return MOE_OK;
+  };
+
+  const bool graph = g->sm_transfer && !g->profiling && !routing_dev && !g->no_graph && T >= 1;
+  if (graph && !g->cursor) {
+    const size_t rows = static_cast<size_t>(c.max_tokens) * D;
+    TRY(alloc_device(reinterpret_cast<void**>(&g->cursor), sizeof(long long)));
+    TRY(alloc_device(reinterpret_cast<void**>(&g->cur_rec), sizeof(StepRecord) * L));
+    TRY(alloc_device(reinterpret_cast<void**>(&g->x_cur), sizeof(float) * D));
+    TRY(alloc_device(reinterpret_cast<void**>(&g->out_cur), sizeof(float) * D));
+    TRY(alloc_device(reinterpret_cast<void**>(&g->x_stage), sizeof(float) * rows));
+    TRY(alloc_device(reinterpret_cast<void**>(&g->out_stage), sizeof(float) * rows));
+    MOE_CUDA(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+  }
+  if (!graph) {
+    for (int64_t t = 0; t < T; ++t) TRY(run_token(g->tokens_done + t, t, false));
+  } else {
+    if (!g->graph_exec) {
+      // capture one token on a private stream; kernels counted per replay below
+      const uint64_t n0 = launch_counter().load();
+      cudaStream_t user = s;
+      s = g->cap_stream;
+      MOE_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      token_begin_kernel<<<1, 256, 0, s>>>(g->cursor, g->x_stage, c.max_tokens, D, g->x_cur);
+      MOE_LAUNCHED();
+      const moe_status st = run_token(0, 0, true);
+      token_end_kernel<<<1, 256, 0, s>>>(g->cursor, g->cur_rec, g->ring, g->out_cur, g->out_stage,
+                                         c.max_tokens, L, D);
+      MOE_LAUNCHED();
+      cudaGraph_t graph_obj = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(s, &graph_obj);
+      s = user;
+      if (st != MOE_OK) {
+        if (graph_obj) cudaGraphDestroy(graph_obj);
+        return st;
+      }
+      MOE_CUDA(ce);
+      MOE_CUDA(cudaGraphInstantiate(&g->graph_exec, graph_obj, 0));
+      cudaGraphDestroy(graph_obj);
+      g->graph_kernels = launch_counter().load() - n0;
+      launch_counter().fetch_sub(g->graph_kernels);
+    }
+    // per chunk of <= max_tokens tokens: stage the inputs into the ring rows, replay the token
+    // graph once per token, collect the outputs from the ring rows
+    const long long cap = c.max_tokens, t0 = g->tokens_done;
+    set_cursor_kernel<<<1, 1, 0, s>>>(g->cursor, t0);
+    MOE_LAUNCHED();
+    for (long long done = 0; done < T;) {
+      const long long chunk = std::min<long long>(T - done, cap);
+      for (long long k = 0; k < chunk;) {
+        const long long pos = (t0 + done + k) % cap, n = std::min<long long>(chunk - k, cap - pos);
+        MOE_CUDA(cudaMemcpy2DAsync(g->x_stage + pos * D, sizeof(float) * D, h_in_dev + (done + k) * d,
+                                   sizeof(float) * d, sizeof(float) * d, n, cudaMemcpyDeviceToDevice, s));
+        k += n;
+      }
+      for (long long i = 0; i < chunk; ++i) MOE_CUDA(cudaGraphLaunch(g->graph_exec, s));
+      launch_counter().fetch_add(g->graph_kernels * chunk);
+      for (long long k = 0; k < chunk;) {
+        const long long pos = (t0 + done + k) % cap, n = std::min<long long>(chunk - k, cap - pos);
+        MOE_CUDA(cudaMemcpy2DAsync(h_out_dev + (done + k) * d, sizeof(float) * d, g->out_stage + pos * D,
+                                   sizeof(float) * D, sizeof(float) * d, n, cudaMemcpyDeviceToDevice, s));
+        k += n;
+      }
+      done += chunk;
+    }
   }
   g->tokens_done += T;
   return MOE_OK;
@@ -932,6 +1047,10 @@ moe_status moe_engine_set_mode(moe_engine* g, int32_t policy, double decay_facto
   MOE_REQUIRE(prefetch == MOE_PREFETCH_OFF || (prefetch == MOE_PREFETCH_EARLY && g->S > 0),
               "prefetch needs staging buffers: create the engine with prefetch enabled");
   TRY(moe_engine_reset(g));
+  if (g->graph_exec) {  // kernel parameters (policy, cache size) are baked into the graph
+    cudaGraphExecDestroy(g->graph_exec);
+    g->graph_exec = nullptr;
+  }
   g->cfg.policy = policy;
   g->cfg.decay_factor = decay_factor;
   g->cfg.decay_period = decay_period;
@@ -967,6 +1086,8 @@ moe_status moe_engine_stats(moe_engine* g, moe_stats* out) {
   *out = g->st;
   out->hits = static_cast<int64_t>(ds.hits);
   out->misses = static_cast<int64_t>(ds.misses);
+  out->demand_bytes += static_cast<int64_t>(ds.fetched_bytes);
+  out->h2d_bytes += static_cast<int64_t>(ds.fetched_bytes);
   out->tokens = g->tokens_done;
   out->steps = g->tokens_done * g->cfg.num_layers;
   out->expert_bytes = g->expert_bytes;

@@ -39,7 +39,7 @@ struct PinnedStore {
     base = static_cast<char*>(p);
     bytes = n;
     external = true;
-    MOE_CUDA(cudaHostRegister(base, n, cudaHostRegisterPortable));
+    MOE_CUDA(cudaHostRegister(base, n, cudaHostRegisterPortable | cudaHostRegisterMapped));
     registered = true;
     return MOE_OK;
   }
@@ -50,7 +50,8 @@ struct PinnedStore {
     const char* mode = getenv("MOE_PIN_MODE");
     if (!(mode && strcmp(mode, "register") == 0)) {
       via_alloc = true;
-      MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&base), n, cudaHostAllocPortable));
+      MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&base), n,
+                             cudaHostAllocPortable | cudaHostAllocMapped));
     } else {
       void* p = mmap(nullptr, n, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
       if (p == MAP_FAILED) {
@@ -68,7 +69,7 @@ struct PinnedStore {
           for (size_t o = lo; o < hi; o += 4096) base[o] = 0;
         });
       for (auto& x : th) x.join();
-      MOE_CUDA(cudaHostRegister(base, n, cudaHostRegisterPortable));
+      MOE_CUDA(cudaHostRegister(base, n, cudaHostRegisterPortable | cudaHostRegisterMapped));
       registered = true;
     }
     setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -132,6 +133,17 @@ struct moe_engine {
   HostControl* ctl_d = nullptr;
 
   PinnedStore store;
+  const char* store_dev = nullptr;  // device view of the store (SM transfer)
+  bool sm_transfer = false;
+  // token graph (SM transfer): one token captured once, replayed per token
+  bool no_graph = getenv("MOE_NO_GRAPH") != nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  uint64_t graph_kernels = 0;
+  cudaStream_t cap_stream = nullptr;
+  long long* cursor = nullptr;        // absolute index of the token the graph processes next
+  StepRecord* cur_rec = nullptr;      // [L] records of the token in flight
+  float *x_cur = nullptr, *out_cur = nullptr;       // [D]
+  float *x_stage = nullptr, *out_stage = nullptr;   // [max_tokens][D] rings
   cudaStream_t copy_stream = nullptr;
 
   // forwarder state (driven by the thread calling decode)

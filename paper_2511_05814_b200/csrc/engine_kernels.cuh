@@ -54,6 +54,7 @@ static_assert(sizeof(LayerState) % 16 == 0, "layer state is copied with 16-byte 
 
 struct DeviceStats {
   unsigned long long hits, misses;
+  unsigned long long fetched_bytes;  // SM transfer mode: bytes read from the host store
 };
 
 // Mapped pinned control block shared by the device and the host forwarder.
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
   // stage the cache state in shared memory (its latency overlaps the logits below)
   copy16(&sS, &p.states[p.layer], sizeof(LayerState), threadIdx.x, blockDim.x);
   if (do_prefetch) copy16(&sS1, &p.states[p.layer + 1], sizeof(LayerState), threadIdx.x, blockDim.x);
-  if (threadIdx.x == 0) s_consumed = p.ctl->consumed;
+  if (threadIdx.x == 0) s_consumed = p.mail ? p.ctl->consumed : 0;
   // RMSNorm scales of h' (route, early guess, experts) and of h_in (reference guess)
   float inv_mid = 1.f, inv_in = 1.f;
   const int njob = 3 * p.E + 2;
@@ -382,45 +383,25 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
   const unsigned long long t1 = p.phase_ns ? gtimer() : 0;
   if (!p.part) {
   // logits: job q = (which, expert); which 0 = route(h'), 1 = guess(h_in), 2 = early(h', l+1).
-  // Every thread owns a fixed float4 column slice, so all of its loads are independent and
-  // in flight together (the kernel is latency-, not bandwidth-, bound); partial sums are
-  // reduced per job through shared memory in a fixed order.
-  __shared__ float part[3 * EM][kGateThreads / 32];
+  // One warp per job (16 warps, 3E jobs): coalesced row loads, one shuffle reduction per job
+  // -- the latency of a handful of dependent steps instead of 3E sequential reductions.
   const int nv = p.d / 4;  // float4 columns
-  float accs[3 * EM];
-#pragma unroll
-  for (int q = 0; q < 3 * EM; ++q) accs[q] = 0.f;
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-    const float4 hm = reinterpret_cast<const float4*>(p.h_mid)[i];
-    const float4 hi = do_guess ? reinterpret_cast<const float4*>(p.h_in)[i] : hm;
-#pragma unroll
-    for (int q = 0; q < 3 * EM; ++q) {
-      const int which = q / EM, e = q % EM;
-      if (e >= p.E) continue;
-      if ((which == 1 && !do_guess) || (which == 2 && !do_prefetch)) continue;
-      const int gl = which == 2 ? p.layer + 1 : p.layer;
-      const float4 a = reinterpret_cast<const float4*>(p.gate_w + (static_cast<size_t>(gl) * p.E + e) * p.d)[i];
-      const float4 b = which == 1 ? hi : hm;
-      float acc = accs[q];
-      acc = fmaf(a.x, b.x, acc);
-      acc = fmaf(a.y, b.y, acc);
-      acc = fmaf(a.z, b.z, acc);
-      acc = fmaf(a.w, b.w, acc);
-      accs[q] = acc;
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 3 * EM; ++q) {
-    const float v = warp_sum(accs[q]);
-    if (lane == 0) part[q][warp] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x < 3 * EM && (threadIdx.x % EM) < p.E) {
-    const int q = threadIdx.x, which = q / EM, e = q % EM;
+  for (int q = warp; q < 3 * p.E; q += nwarps) {
+    const int which = q / p.E, e = q % p.E;
+    if ((which == 1 && !do_guess) || (which == 2 && !do_prefetch)) continue;
     const int gl = which == 2 ? p.layer + 1 : p.layer;
+    const float4* w = reinterpret_cast<const float4*>(p.gate_w + (static_cast<size_t>(gl) * p.E + e) * p.d);
+    const float4* v = reinterpret_cast<const float4*>(which == 1 ? p.h_in : p.h_mid);
     float acc = 0.f;
-    for (int w = 0; w < nwarps; ++w) acc += part[q][w];
-    z[which][e] = acc * (which == 1 ? inv_in : inv_mid) + p.gate_b[gl * p.E + e];
+    for (int i = lane; i < nv; i += 32) {
+      const float4 a4 = w[i], b4 = v[i];
+      acc = fmaf(a4.x, b4.x, acc);
+      acc = fmaf(a4.y, b4.y, acc);
+      acc = fmaf(a4.z, b4.z, acc);
+      acc = fmaf(a4.w, b4.w, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) z[which][e] = acc * (which == 1 ? inv_in : inv_mid) + p.gate_b[gl * p.E + e];
   }
   }
   __syncthreads();
@@ -594,13 +575,18 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
   // write back the state and post the mail (all lanes, 16-byte stores)
   copy16(&p.states[p.layer], &sS, sizeof(LayerState), lane, 32);
   if (do_prefetch) copy16(&p.states[p.layer + 1], &sS1, sizeof(LayerState), lane, 32);
-  MailRecord* dst = p.mail + (p.seq % kMailRing);
-  copy16(dst, &sM, offsetof(MailRecord, ready), lane, 32);
-  __threadfence_system();
+  // copy-engine transfer: post the decision to the host forwarder (SM transfer: no host)
+  MailRecord* dst = p.mail ? p.mail + (p.seq % kMailRing) : nullptr;
+  if (dst) {
+    copy16(dst, &sM, offsetof(MailRecord, ready), lane, 32);
+    __threadfence_system();
+  }
   __syncwarp();
   if (lane == 0) {
-    dst->ready = p.seq + 1;
-    p.ctl->gate_done = static_cast<unsigned int>(p.seq + 1);
+    if (dst) {
+      dst->ready = p.seq + 1;
+      p.ctl->gate_done = static_cast<unsigned int>(p.seq + 1);
+    }
     if (p.phase_ns) {
       const unsigned long long t5 = gtimer();
       atomicAdd(&p.phase_ns[0], t1 - t0);
@@ -621,7 +607,7 @@ struct FfnParams {
   const char* pool;          // this layer's buffers: pool + b * expert_bytes
   long long expert_bytes;
   int d, f, K;
-  int phase;                 // 0: experts that hit (resident before), 1: misses
+  int phase;                 // 0: experts that hit (resident before), 1: misses, 2: all
   float* act;                // [K][f]
   float* y;                  // [K][d]
 };
@@ -632,7 +618,60 @@ __device__ __forceinline__ bool ffn_phase_match(const FfnParams& p, int j, int* 
   if (e < 0 || e >= kMaxE || p.rec->flags) return false;  // failed gate: nothing to run
   if (p.state->buf_of[e] < 0) return false;
   const bool hit = (p.rec->rb >> e) & 1u;
-  return (p.phase == 0) == hit;
+  return p.phase == 2 || (p.phase == 0) == hit;
+}
+
+// ---- SM transfer: missed experts copied from the mapped pinned store by the SMs ----------
+// (device-driven: no host round trip per layer; for small experts, where latency dominates)
+struct FetchParams {
+  const StepRecord* rec;
+  const LayerState* state;   // buf_of after this step's policy decision
+  const char* store;         // device view of this layer's host experts [E][expert_bytes]
+  char* pool;                // this layer's HBM buffers
+  long long expert_bytes;    // multiple of 16
+  int K;
+  DeviceStats* stats;
+};
+
+static __global__ void __launch_bounds__(512) fetch_kernel(FetchParams p) {
+  if (p.rec->flags) return;
+  // the step's missed experts as one flat range of 16-byte words, so every PCIe read of the
+  // step is in flight together (8 per thread before its stores)
+  const char* src[kMaxK];
+  char* dst[kMaxK];
+  int misses = 0;
+  for (int j = 0; j < p.K; ++j) {
+    const int e = p.rec->acts[j];
+    if (e < 0 || e >= kMaxE || ((p.rec->rb >> e) & 1u)) continue;
+    const int b = p.state->buf_of[e];
+    if (b < 0) continue;
+    src[misses] = p.store + e * p.expert_bytes;
+    dst[misses] = p.pool + b * p.expert_bytes;
+    ++misses;
+  }
+  if (!misses) return;
+  const long long per = p.expert_bytes / 16, n16 = per * misses;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 7 * stride < n16; i += 8 * stride) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const long long k = i + u * stride, m = k / per;
+      v[u] = ld_stream(reinterpret_cast<const uint4*>(src[m]) + (k - m * per));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const long long k = i + u * stride, m = k / per;
+      reinterpret_cast<uint4*>(dst[m])[k - m * per] = v[u];
+    }
+  }
+  for (; i < n16; i += stride) {
+    const long long m = i / per;
+    reinterpret_cast<uint4*>(dst[m])[i - m * per] = ld_stream(reinterpret_cast<const uint4*>(src[m]) + (i - m * per));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(&p.stats->fetched_bytes, static_cast<unsigned long long>(misses) * p.expert_bytes);
 }
 
 // SwiGLU up projection: act[j][r] = silu(w1[r] . x) * (w3[r] . x)
@@ -704,6 +743,25 @@ static __global__ void finalize_kernel(const float* h_mid, const float* y, const
                                 int d, float* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < d) out[i] = combine_elem(h_mid, y, rec, K, d, i);
+}
+
+// ---- token graph plumbing: move the token in flight between the rings and the fixed buffers
+static __global__ void set_cursor_kernel(long long* cursor, long long v) { *cursor = v; }
+
+static __global__ void token_begin_kernel(const long long* cursor, const float* x_stage, int cap,
+                                          int D, float* x_cur) {
+  const float* src = x_stage + (*cursor % cap) * D;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) x_cur[i] = src[i];
+}
+
+static __global__ void token_end_kernel(long long* cursor, const StepRecord* cur_rec,
+                                        StepRecord* ring, const float* out_cur, float* out_stage,
+                                        int cap, int L, int D) {
+  const long long row = *cursor % cap;
+  copy16(ring + row * L, cur_rec, static_cast<int>(sizeof(StepRecord)) * L, threadIdx.x, blockDim.x);
+  for (int i = threadIdx.x; i < D; i += blockDim.x) out_stage[row * D + i] = out_cur[i];
+  __syncthreads();
+  if (threadIdx.x == 0) *cursor += 1;
 }
 
 static __global__ void reset_states_kernel(LayerState* s, int L, int NB) {

@@ -70,7 +70,7 @@ __device__ __forceinline__ int stream_active(const StreamParams& p, int* slot, c
     const int e = p.rec->acts[k];
     if (e < 0 || e >= kMaxE) continue;
     const bool hit = (p.rec->rb >> e) & 1u;
-    if ((p.phase == 0) != hit) continue;
+    if (p.phase != 2 && (p.phase == 0) != hit) continue;
     const int idx = seen++;
     if (p.only >= 0 && idx != p.only) continue;
     const int b = p.state->buf_of[e];

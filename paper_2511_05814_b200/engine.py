@@ -53,6 +53,7 @@ class EngineConfig:
     device: int = 0
     rms_norm: bool = False               # Mixtral presets: True (RMSNorm before gate/experts)
     rms_eps: float = 1e-5
+    transfer: str = "auto"               # "auto" | "copy_engine" | "sm" (see moeb200.h)
 
     @staticmethod
     def mixtral_8x7b(**kw) -> "EngineConfig":
@@ -86,6 +87,10 @@ class EngineConfig:
         modes = {"off": _native.PREFETCH_OFF, "early": _native.PREFETCH_EARLY}
         if self.prefetch not in modes:
             raise ConfigError(f"unknown prefetch mode {self.prefetch!r}")
+        transfers = {"auto": _native.TRANSFER_AUTO, "copy_engine": _native.TRANSFER_COPY_ENGINE,
+                     "sm": _native.TRANSFER_SM}
+        if self.transfer not in transfers:
+            raise ConfigError(f"unknown transfer mode {self.transfer!r}")
         code, df, dp = self.policy.device_params()
         return _native.EngineConfigC(
             num_layers=self.num_layers, num_experts=self.num_experts, top_k=self.top_k,
@@ -95,7 +100,7 @@ class EngineConfig:
             renormalize=int(self.renormalize), record_speculation=int(self.record_speculation),
             max_tokens=self.max_tokens, chunk_bytes=self.chunk_bytes,
             prefetch_depth=self.prefetch_depth, device=self.device, rms_norm=int(self.rms_norm),
-            rms_eps=self.rms_eps)
+            rms_eps=self.rms_eps, transfer=transfers[self.transfer])
 
 
 class OffloadEngine:

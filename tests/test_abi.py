@@ -38,10 +38,26 @@ def test_invalid_config_is_rejected_before_any_device_work():
     assert st == _native.MOE_INVALID_CONFIG
 
 
-def test_engine_struct_layout_matches_header():
-    # 8 int32 + double + int64 + float + 4 int32 + (pad) int64 + 2 int32 (moe_engine_config)
-    assert ctypes.sizeof(_native.EngineConfigC) == 96
-    # 11 int64 + double + 2 int64 (moe_stats)
-    assert ctypes.sizeof(_native.StatsC) == 14 * 8
-    # 4 double + 5 int64 + double + 2 int64 + double + int64 + double + int64 + 2 double
-    assert ctypes.sizeof(_native.KernelTimesC) == 18 * 8
+def test_engine_struct_layout_matches_header(tmp_path):
+    """Every ctypes mirror has the C header's size and field offsets (compiled with gcc)."""
+    import subprocess
+
+    structs = {"moe_engine_config": _native.EngineConfigC, "moe_stats": _native.StatsC,
+               "moe_kernel_times": _native.KernelTimesC}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{ROOT / "include" / "moeb200.h"}"',
+             "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')
+        for f, _ in cls._fields_:
+            lines.append(f'  printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], check=True, capture_output=True,
+                                                         text=True).stdout.splitlines())
+    for cname, cls in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for f, _ in cls._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(cls, f).offset, f"{cname}.{f}"

@@ -9,7 +9,7 @@ ARCH="-gencode arch=compute_100a,code=sm_100a"
 FLAGS="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr ${MOE_NVCC_EXTRA:-}"
 mkdir -p build
 objs=(); pids=()
-newest_hdr=$(ls -t $SRC/*.cuh include/*.h | head -1)
+newest_hdr=$(ls -t $SRC/*.cuh $SRC/*.h include/*.h | head -1)
 for f in $SRC/*.cu; do
   o=build/$(basename "$f" .cu).o
   objs+=("$o")
