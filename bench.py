@@ -58,6 +58,9 @@ def parse_args():
     p.add_argument("--layers", type=int, default=0,
                    help="fewer layers than the model (invalidates the headline; diagnostics)")
     p.add_argument("--model", choices=["mixtral_8x7b", "mixtral_8x22b"], default="mixtral_8x7b")
+    p.add_argument("--store-layers", type=int, default=-1,
+                   help="host expert store depth; -1 = all layers if they fit in 85%% of host RAM, "
+                        "else as many as fit (deeper layers alias l %% S; SURVEY H5)")
     p.add_argument("--sweep-cache", default="",
                    help="e.g. 2,4,6: LFU and LFU+prefetch at each cache size (configs[2])")
     p.add_argument("--prefill-tokens", type=int, default=512,
@@ -196,6 +199,16 @@ def measured_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+def host_available_bytes() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 1 << 62
+
+
 def h2d_peak_gbs(dev) -> float:
     """Copy-engine H2D peak: 1 GiB pinned -> device, best of 5 (CUDA events)."""
     import torch
@@ -327,8 +340,21 @@ def run_ours(args, world, rank, local):
     want_prefetch = any(pf for _, _, pf in parsed)
     base_cfg = factory()
     nl = args.layers or base_cfg.num_layers
+    store_layers = args.store_layers
+    if store_layers < 0:
+        per_layer = base_cfg.num_experts * base_cfg.expert_bytes
+        avail = host_available_bytes()
+        store_layers = 0 if nl * per_layer <= 0.85 * avail else max(1, int(0.85 * avail // per_layer))
+    # HBM: per-layer pool of C policy + S staging buffers; deeper models stage 1 guess per layer
+    import torch as _t
+    hbm = _t.cuda.get_device_properties(local).total_memory
+    dense = nl * (2 * base_cfg.hidden_dim ** 2 + 4 * base_cfg.num_experts * base_cfg.hidden_dim)
+    pf_bufs = 0
+    if want_prefetch and nl * (cap_c + base_cfg.top_k) * base_cfg.expert_bytes + dense > 0.9 * hbm:
+        pf_bufs = 1
     cfg = factory(num_layers=nl, cache_size=cap_c, prefetch="early" if want_prefetch else "off",
-                  max_tokens=4096, device=local)
+                  max_tokens=4096, device=local, store_layers=store_layers,
+                  prefetch_buffers=pf_bufs)
     D, F, EB = cfg.hidden_dim, cfg.ffn_dim, cfg.expert_bytes
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.model == "mixtral_8x7b":
@@ -340,7 +366,7 @@ def run_ours(args, world, rank, local):
     local_rank, local_world = replicas.local_world()
     if world > 1 or args.shared_store:
         # one host copy of the experts per node, page-locked by every local replica
-        nbytes = cfg.num_layers * cfg.num_experts * EB
+        nbytes = cfg.host_store_layers * cfg.num_experts * EB
         name = replicas.store_name(cfg, args.seed, os.environ.get("TORCHELASTIC_RUN_ID", ""))
         holder = {}
 
@@ -481,6 +507,8 @@ def run_ours(args, world, rank, local):
             "cache_size": head["cache_size"], "policy": variants[0],
             "l2": "inputs larger than L2: each step streams >=23.6 GB of weights through HBM",
             "setup_s": round(t_setup, 1), "shared_store": store is not None,
+            "host_store_layers": cfg.host_store_layers,
+            "prefetch_buffers_per_layer": (cfg.prefetch_buffers or cfg.top_k) if want_prefetch else 0,
         },
         "hit_rate": head["hit_rate"],
         "variants": results,

@@ -144,6 +144,12 @@ typedef struct {
                              toy semantics (no norm, toymoe.py:138-146). */
   float rms_eps;          /* RMSNorm epsilon (Mixtral: 1e-5) */
   int32_t transfer;       /* MOE_TRANSFER_*: how missed experts reach HBM */
+  int32_t store_layers;   /* host expert store depth: 0 = num_layers.  S < num_layers aliases
+                             layer l's experts to store layer l % S (synthetic models deeper
+                             than host RAM holds, e.g. Mixtral-8x22B's 271 GB on a 196 GB
+                             host); HBM caches, routing and transfers stay per layer. */
+  int32_t prefetch_buffers; /* staging buffers per layer with prefetch on: 0 = top_k; fewer
+                               fit deeper models in HBM (prefetch then covers the best guesses) */
 } moe_engine_config;
 
 typedef struct {

@@ -109,12 +109,13 @@ class MixtralRef:
 
     def __init__(self, L, E, K, d, f, alpha, seed=42, layout="ref", threads=None,
                  layers=None, renormalize=False, rms_norm=False, rms_eps=1e-5,
-                 gate_bias_std=0.25):
+                 gate_bias_std=0.25, store_layers=0):
         self.L, self.E, self.K, self.d, self.f = L, E, K, d, f
         self.alpha, self.seed, self.layout, self.threads = alpha, seed, layout, threads
         self.renormalize = renormalize
         self.rms_norm, self.rms_eps = rms_norm, rms_eps
         self.gate_bias_std = gate_bias_std
+        self.store_layers = store_layers if store_layers > 0 else L  # engine store aliasing
         self.dtype = np.float64 if layout == "ref" else np.float32
         self.layers = list(range(L)) if layers is None else list(layers)
         self._dense = {}
@@ -140,6 +141,7 @@ class MixtralRef:
         return self._dense[l]
 
     def expert(self, l, e):
+        l = l % self.store_layers  # layer l's experts live in store layer l % S
         if (l, e) not in self._experts:
             d, f = self.d, self.f
             self._experts[(l, e)] = (self._matrix(_tid(4, l, e, 1), _std(d), f, d),

@@ -49,7 +49,8 @@ class EngineConfigC(ctypes.Structure):
         ("record_speculation", ctypes.c_int32), ("max_tokens", ctypes.c_int32),
         ("chunk_bytes", ctypes.c_int64), ("prefetch_depth", ctypes.c_int32),
         ("device", ctypes.c_int32), ("rms_norm", ctypes.c_int32), ("rms_eps", ctypes.c_float),
-        ("transfer", ctypes.c_int32),
+        ("transfer", ctypes.c_int32), ("store_layers", ctypes.c_int32),
+        ("prefetch_buffers", ctypes.c_int32),
     ]
 
 

@@ -34,8 +34,7 @@ moe_status create_resources(moe_engine* g);
 
 moe_status issue_copy(moe_engine* g, int layer, int buf, int expert, long long off, long long n) {
   char* dst = g->pool + (static_cast<long long>(layer) * g->NB + buf) * g->expert_bytes + off;
-  const char* src =
-      g->store.base + (static_cast<long long>(layer) * g->cfg.num_experts + expert) * g->expert_bytes + off;
+  const char* src = g->store_block(layer, expert) + off;
   MOE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, g->copy_stream));
   return MOE_OK;
 }
@@ -343,10 +342,12 @@ moe_status moe_engine_create_ex(const moe_engine_config* cfg_in, void* store, in
   MOE_REQUIRE(c.expert_kind != MOE_EXPERT_SWIGLU_BF16 ||
                   (c.hidden_dim % 8 == 0 && c.ffn_dim >= 8 && c.ffn_dim % 8 == 0),
               "SwiGLU experts need hidden_dim and ffn_dim multiples of 8");
+  MOE_REQUIRE(c.store_layers >= 0, "store_layers must be >= 0");
   MOE_REQUIRE(c.transfer >= MOE_TRANSFER_AUTO && c.transfer <= MOE_TRANSFER_SM,
               "unknown transfer mode %d", c.transfer);
   MOE_REQUIRE(!(c.transfer == MOE_TRANSFER_SM && c.prefetch),
               "speculative prefetch runs on the copy engine (transfer=SM has no staging path)");
+  MOE_REQUIRE(c.prefetch_buffers >= 0, "prefetch_buffers must be >= 0");
   MOE_REQUIRE(c.cache_size + (c.prefetch ? c.top_k : 0) <= kMaxBuf,
               "cache_size + staging buffers must be <= %d", kMaxBuf);
 
@@ -368,7 +369,8 @@ moe_status moe_engine_create_ex(const moe_engine_config* cfg_in, void* store, in
   }
   g->sm_transfer = c.transfer == MOE_TRANSFER_SM ||
                    (c.transfer == MOE_TRANSFER_AUTO && !c.prefetch && g->expert_bytes <= (16ll << 20));
-  g->S = c.prefetch ? c.top_k : 0;
+  g->S = c.prefetch ? (c.prefetch_buffers > 0 ? std::min(c.prefetch_buffers, c.top_k) : c.top_k) : 0;
+  g->SL = c.store_layers > 0 ? std::min(c.store_layers, c.num_layers) : c.num_layers;
   g->NB = c.cache_size + g->S;
   g->cap_C = c.cache_size;
   g->ext_store = store;
@@ -440,7 +442,7 @@ moe_status create_resources(moe_engine* g) {
   }
   if (getenv("MOE_GATE_TIMING"))
     TRY(alloc_device(reinterpret_cast<void**>(&g->gate_phase_ns), 8 * sizeof(unsigned long long)));
-  const size_t store_bytes = static_cast<size_t>(L) * E * g->expert_bytes;
+  const size_t store_bytes = static_cast<size_t>(g->SL) * E * g->expert_bytes;
   if (g->ext_store) {
     MOE_REQUIRE(static_cast<size_t>(g->ext_store_bytes) >= store_bytes,
                 "external expert store holds %lld bytes, the model needs %zu",
@@ -547,7 +549,7 @@ moe_status moe_engine_set_toy_expert_f32(moe_engine* g, int32_t layer, int32_t e
   MOE_REQUIRE(!g->bf16, "set_toy_expert_f32 is for the toy engine");
   const int d = g->d, D = g->dpad;
   float* blk = reinterpret_cast<float*>(
-      g->store.base + (static_cast<long long>(layer) * g->cfg.num_experts + expert) * g->expert_bytes);
+      g->store_block(layer, expert));
   memset(blk, 0, g->expert_bytes);
   float* w1t = blk;
   float* w2t = blk + static_cast<size_t>(D) * D;
@@ -581,12 +583,12 @@ moe_status moe_engine_init_random(moe_engine* g, uint64_t seed, float gate_bias_
   // replica attached to a shared store leaves this to the store's owner)
   uint16_t* scratch = reinterpret_cast<uint16_t*>(g->pool);
   const long long fd = 1ll * f * d;
-  for (int l = 0; l < (init_experts ? L : 0); ++l)
+  for (int l = 0; l < (init_experts ? g->SL : 0); ++l)
     for (int e = 0; e < E; ++e) {
       TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW1), sd, fd, scratch, s));
       TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW3), sd, fd, scratch + fd, s));
       TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW2), sf, fd, scratch + 2 * fd, s));
-      MOE_CUDA(cudaMemcpyAsync(g->store.base + (static_cast<long long>(l) * E + e) * g->expert_bytes,
+      MOE_CUDA(cudaMemcpyAsync(g->store_block(l, e),
                                scratch, g->expert_bytes, cudaMemcpyDeviceToHost, s));
     }
   MOE_CUDA(cudaStreamSynchronize(s));
@@ -598,7 +600,7 @@ moe_status moe_engine_expert_host_ptr(moe_engine* g, int32_t layer, int32_t expe
   MOE_REQUIRE(g && layer >= 0 && layer < g->cfg.num_layers && expert >= 0 &&
                   expert < g->cfg.num_experts,
               "expert (%d, %d) out of range", layer, expert);
-  *ptr = g->store.base + (static_cast<long long>(layer) * g->cfg.num_experts + expert) * g->expert_bytes;
+  *ptr = g->store_block(layer, expert);
   *bytes = g->expert_bytes;
   return MOE_OK;
 }
@@ -663,6 +665,25 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
     cudaFuncSetAttribute(toy_up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(down_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(down_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    // one shared-memory carveout for every kernel of the step: switching the L1/shared split
+    // between consecutive kernels drains the SMs (seen as ~20 us gaps around the FFN launches)
+    if (!getenv("MOE_NO_CARVEOUT")) {
+      const int mx = cudaSharedmemCarveoutMaxShared;
+      cudaFuncSetAttribute(gate_cache_kernel<8>, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(gate_cache_kernel<kMaxE>, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(fetch_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(token_begin_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(token_end_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(set_cursor_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(mix_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(mix_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(swiglu_up_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(toy_up_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(down_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(down_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      set_stream_carveout(mx);
+    }
     attrs = true;
   }
   MOE_REQUIRE(mix_smem <= 200 * 1024 && down_smem <= 200 * 1024, "hidden/ffn dims too large");
@@ -821,7 +842,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       if (g->sm_transfer) {
         // device-driven: the SMs fetch the missed experts, then one FFN pass over all K
         FetchParams fp2{trec + l, g->states + l,
-                        g->store_dev + static_cast<long long>(l) * c.num_experts * g->expert_bytes,
+                        g->store_block_dev(l, 0),
                         g->pool + static_cast<long long>(l) * g->NB * g->expert_bytes, g->expert_bytes,
                         K, g->dstats};
         const long long n16 = g->expert_bytes / 16;

@@ -108,6 +108,7 @@ using namespace moe;
 struct moe_engine {
   moe_engine_config cfg{};
   int d = 0, dpad = 0, f = 0, NB = 0, S = 0;
+  int SL = 0;  // layers held by the host store (layer l uses store layer l % SL)
   bool bf16 = false;
   long long expert_bytes = 0;
   int device = 0;
@@ -177,5 +178,13 @@ struct moe_engine {
 
   // batched prefill (prefill.cu), allocated on first use
   moe::PrefillState* pf = nullptr;
+
+  // host block of expert e of layer l (store layers alias modulo SL)
+  char* store_block(int layer, int expert) const {
+    return store.base + (static_cast<long long>(layer % SL) * cfg.num_experts + expert) * expert_bytes;
+  }
+  const char* store_block_dev(int layer, int expert) const {
+    return store_dev + (static_cast<long long>(layer % SL) * cfg.num_experts + expert) * expert_bytes;
+  }
 };
 

@@ -360,7 +360,7 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
       const int e = m.load_expert[i], dst = m.load_dst[i];
       char* to = dst >= 0 ? g->pool + (static_cast<long long>(l) * g->NB + dst) * g->expert_bytes
                           : pf->scratch + static_cast<long long>(-1 - dst) * g->expert_bytes;
-      const char* from = g->store.base + (static_cast<long long>(l) * E + e) * g->expert_bytes;
+      const char* from = g->store_block(l, e);
       MOE_CUDA(cudaMemcpyAsync(to, from, split, cudaMemcpyHostToDevice, g->copy_stream));
       MOE_CUDA(cudaEventRecord(pf->ev[2 * i], g->copy_stream));
       MOE_CUDA(cudaMemcpyAsync(to + split, from + split, g->expert_bytes - split, cudaMemcpyHostToDevice,

@@ -357,6 +357,20 @@ inline StreamGeom stream_geometry_rpb(int mode, int d, int f, int stage_budget, 
 // the expert count so each active expert gets an equal band of CTAs.
 inline int stream_grid(int experts, int sms = 148) { return sms / experts * experts; }
 
+// Preferred L1/shared carveout of every stream GEMV instantiation (engine.cu keeps all kernels
+// of a decode step on the same split).
+inline void set_stream_carveout(int carveout) {
+  cudaFuncSetAttribute(stream_gemv_kernel<kModeMix, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  cudaFuncSetAttribute(stream_gemv_kernel<kModeMix, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  cudaFuncSetAttribute(stream_gemv_kernel<kModeMix, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  cudaFuncSetAttribute(stream_gemv_kernel<kModeUp, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  cudaFuncSetAttribute(stream_gemv_kernel<kModeUp, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  cudaFuncSetAttribute(stream_gemv_kernel<kModeUp, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  cudaFuncSetAttribute(stream_gemv_kernel<kModeDown, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  cudaFuncSetAttribute(stream_gemv_kernel<kModeDown, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  cudaFuncSetAttribute(stream_gemv_kernel<kModeDown, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+}
+
 // Launch one stream GEMV with the template instantiation matching the geometry.
 template <int MODE>
 inline cudaError_t launch_stream(const StreamGeom& g, int grid, const StreamParams& sp,

@@ -54,6 +54,8 @@ class EngineConfig:
     rms_norm: bool = False               # Mixtral presets: True (RMSNorm before gate/experts)
     rms_eps: float = 1e-5
     transfer: str = "auto"               # "auto" | "copy_engine" | "sm" (see moeb200.h)
+    store_layers: int = 0                # host store depth (0 = num_layers; else layers alias l % S)
+    prefetch_buffers: int = 0            # staging buffers per layer with prefetch (0 = top_k)
 
     @staticmethod
     def mixtral_8x7b(**kw) -> "EngineConfig":
@@ -70,6 +72,10 @@ class EngineConfig:
                     expert_kind="swiglu", mixing_scale=0.1 * math.sqrt(16 / 6144), rms_norm=True)
         base.update(kw)
         return EngineConfig(**base)
+
+    @property
+    def host_store_layers(self) -> int:
+        return min(self.store_layers, self.num_layers) if self.store_layers > 0 else self.num_layers
 
     @property
     def expert_bytes(self) -> int:
@@ -100,7 +106,8 @@ class EngineConfig:
             renormalize=int(self.renormalize), record_speculation=int(self.record_speculation),
             max_tokens=self.max_tokens, chunk_bytes=self.chunk_bytes,
             prefetch_depth=self.prefetch_depth, device=self.device, rms_norm=int(self.rms_norm),
-            rms_eps=self.rms_eps, transfer=transfers[self.transfer])
+            rms_eps=self.rms_eps, transfer=transfers[self.transfer], store_layers=self.store_layers,
+            prefetch_buffers=self.prefetch_buffers)
 
 
 class OffloadEngine:
