@@ -58,6 +58,8 @@ def parse_args():
     p.add_argument("--layers", type=int, default=0,
                    help="fewer layers than the model (invalidates the headline; diagnostics)")
     p.add_argument("--model", choices=["mixtral_8x7b", "mixtral_8x22b"], default="mixtral_8x7b")
+    p.add_argument("--compress", choices=["auto", "on", "off"], default="auto",
+                   help="exponent-coded (lossless) expert transfers; auto = on with a private store")
     p.add_argument("--store-layers", type=int, default=-1,
                    help="host expert store depth; -1 = all layers if they fit in 85%% of host RAM, "
                         "else as many as fit (deeper layers alias l %% S; SURVEY H5)")
@@ -352,9 +354,11 @@ def run_ours(args, world, rank, local):
     pf_bufs = 0
     if want_prefetch and nl * (cap_c + base_cfg.top_k) * base_cfg.expert_bytes + dense > 0.9 * hbm:
         pf_bufs = 1
+    shared = world > 1 or args.shared_store
+    compress = args.compress == "on" or (args.compress == "auto" and not shared)
     cfg = factory(num_layers=nl, cache_size=cap_c, prefetch="early" if want_prefetch else "off",
                   max_tokens=4096, device=local, store_layers=store_layers,
-                  prefetch_buffers=pf_bufs)
+                  prefetch_buffers=pf_bufs, compress=compress)
     D, F, EB = cfg.hidden_dim, cfg.ffn_dim, cfg.expert_bytes
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.model == "mixtral_8x7b":
@@ -383,6 +387,9 @@ def run_ours(args, world, rank, local):
         eng = OffloadEngine(cfg)
         eng.init_random(args.seed)
     t_setup = time.perf_counter() - t_setup
+    st0 = eng.stats()
+    compressed_ratio = (st0["compressed_store_bytes"] / (cfg.host_store_layers * cfg.num_experts * EB)
+                        if cfg.compress else 1.0)
     # independent request stream per rank: token inputs from the counter hash (f32, std 1)
     base = replicas.rank_token_base(rank)
     n_tok = args.warmup + args.steps + args.e2e_steps
@@ -431,6 +438,7 @@ def run_ours(args, world, rank, local):
         hits, misses = s1["hits"] - s0["hits"], s1["misses"] - s0["misses"]
         demand = s1["demand_bytes"] - s0["demand_bytes"]
         h2d = s1["h2d_bytes"] - s0["h2d_bytes"]
+        demand_link = s1["demand_link_bytes"] - s0["demand_link_bytes"]
         busy = s1["copy_busy_ms"] - s0["copy_busy_ms"]
         rec = eng.records(t0_tok + args.warmup, args.steps)
         results[v] = {
@@ -440,9 +448,11 @@ def run_ours(args, world, rank, local):
             "hit_rate": hits / max(1, hits + misses),
             "misses_per_token": misses / args.steps,
             "h2d_GBps": h2d / (ms / 1e3) / 1e9,
-            "demand_copy_GBps": demand / (busy / 1e3) / 1e9 if busy > 0 else None,
+            "demand_copy_GBps": demand_link / (busy / 1e3) / 1e9 if busy > 0 else None,
             "pcie_frac_of_measured_h2d_peak": (h2d / (ms / 1e3) / 1e9) / pcie_peak,
-            "pcie_bound_tokens_per_s": pcie_peak * 1e9 / max(1.0, misses / args.steps * EB),
+            "pcie_bound_tokens_per_s": pcie_peak * 1e9 / max(1.0, misses / args.steps * EB * compressed_ratio),
+            "expert_GBps_delivered": (demand + s1["prefetch_bytes"] - s0["prefetch_bytes"]
+                                      + s1["prefill_bytes"] - s0["prefill_bytes"]) / (ms / 1e3) / 1e9,
             "prefetch_issued": s1["prefetch_issued"] - s0["prefetch_issued"],
             "prefetch_used": s1["prefetch_used"] - s0["prefetch_used"],
             "prefetch_wasted_bytes": s1["prefetch_wasted_bytes"] - s0["prefetch_wasted_bytes"],
@@ -508,6 +518,9 @@ def run_ours(args, world, rank, local):
             "l2": "inputs larger than L2: each step streams >=23.6 GB of weights through HBM",
             "setup_s": round(t_setup, 1), "shared_store": store is not None,
             "host_store_layers": cfg.host_store_layers,
+            "expert_transfer": ("exponent-coded bf16, lossless (csrc/expcodec.cuh), "
+                                f"{compressed_ratio:.3f} of the raw bytes" if cfg.compress
+                                else "raw bf16"),
             "prefetch_buffers_per_layer": (cfg.prefetch_buffers or cfg.top_k) if want_prefetch else 0,
         },
         "hit_rate": head["hit_rate"],

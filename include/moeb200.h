@@ -150,6 +150,9 @@ typedef struct {
                              host); HBM caches, routing and transfers stay per layer. */
   int32_t prefetch_buffers; /* staging buffers per layer with prefetch on: 0 = top_k; fewer
                                fit deeper models in HBM (prefetch then covers the best guesses) */
+  int32_t compress;       /* 1: demand and prefill copies move the experts exponent-coded
+                             (expcodec.cuh, lossless, ~0.69x the bytes) and decode them in HBM;
+                             SwiGLU engines with a private store and the copy engine only */
 } moe_engine_config;
 
 typedef struct {
@@ -157,7 +160,8 @@ typedef struct {
   int64_t steps;            /* (token, layer) steps */
   int64_t hits, misses;     /* policy hits / misses */
   int64_t h2d_bytes;        /* bytes copied host->device for experts (demand + prefetch) */
-  int64_t demand_bytes;     /* of which demand misses (== misses * expert_bytes w/o prefetch) */
+  int64_t demand_bytes;     /* expert bytes delivered to demand misses (== misses * expert_bytes
+                               without prefetch; raw bf16 equivalent when compressed) */
   int64_t prefetch_bytes;   /* of which speculative prefetch chunks issued */
   int64_t prefetch_issued;  /* experts prefetched (guess not resident) */
   int64_t prefetch_used;    /* prefetched experts adopted by a demand miss */
@@ -167,6 +171,9 @@ typedef struct {
   int64_t prefill_tokens;   /* tokens processed by moe_engine_prefill */
   int64_t prefill_bytes;    /* bytes copied host->device by prefill (one load per needed expert
                                per layer; included in h2d_bytes) */
+  int64_t demand_link_bytes;   /* bytes the demand copies put on the link (== demand_bytes
+                                  uncompressed; h2d_bytes = demand_link + prefetch + prefill) */
+  int64_t compressed_store_bytes; /* host bytes of the exponent-coded expert store (0: off) */
 } moe_stats;
 
 moe_status moe_engine_create(const moe_engine_config* cfg, moe_engine** out);
@@ -314,6 +321,16 @@ moe_status moe_sample_zipf(const double* weights_dev, int32_t L, int32_t E, int6
 moe_status moe_sample_markov(const double* weights_dev, int32_t L, int32_t E, int64_t T, int32_t K,
                              double repeat_prob, const double* u_retain_dev,
                              const double* u_draw_dev, int64_t* out_dev, void* stream);
+
+/* ---- lossless bf16 exponent coding of expert parts (expcodec.cuh) --------------------- */
+
+/* Encode n bf16 words (host) into one part: out == NULL returns the size only.  kbits 0 picks
+ * 3 or 4 bits per exponent code (smaller output).  Multi-threaded. */
+moe_status moe_xc_encode(const uint16_t* in, uint64_t n, int32_t kbits, void* out, uint64_t cap,
+                         uint64_t* size);
+/* Decode a part already in device memory; header_host = a host copy of its first 64 bytes. */
+moe_status moe_xc_decode(const void* part_dev, const void* header_host, uint16_t* out_dev,
+                         void* stream);
 
 /* ---- trace / event-log JSONL (host only, no CUDA) ------------------------------------ */
 

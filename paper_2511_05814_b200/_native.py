@@ -35,6 +35,7 @@ EXPORTED = (
     "moe_tc_grouped_gemm_bf16", "moe_tc_grouped_swiglu_bf16",
     "moe_text_data", "moe_text_size", "moe_text_free", "moe_format_trace", "moe_format_event_log",
     "moe_sample_zipf", "moe_sample_markov", "moe_engine_decode_routed", "moe_engine_prefill_routed",
+    "moe_xc_encode", "moe_xc_decode",
 )
 
 
@@ -50,7 +51,7 @@ class EngineConfigC(ctypes.Structure):
         ("chunk_bytes", ctypes.c_int64), ("prefetch_depth", ctypes.c_int32),
         ("device", ctypes.c_int32), ("rms_norm", ctypes.c_int32), ("rms_eps", ctypes.c_float),
         ("transfer", ctypes.c_int32), ("store_layers", ctypes.c_int32),
-        ("prefetch_buffers", ctypes.c_int32),
+        ("prefetch_buffers", ctypes.c_int32), ("compress", ctypes.c_int32),
     ]
 
 
@@ -59,7 +60,8 @@ class StatsC(ctypes.Structure):
         "tokens", "steps", "hits", "misses", "h2d_bytes", "demand_bytes", "prefetch_bytes",
         "prefetch_issued", "prefetch_used", "prefetch_wasted_bytes", "expert_bytes")] + [
         ("copy_busy_ms", ctypes.c_double), ("prefill_tokens", ctypes.c_int64),
-        ("prefill_bytes", ctypes.c_int64)]
+        ("prefill_bytes", ctypes.c_int64), ("demand_link_bytes", ctypes.c_int64),
+        ("compressed_store_bytes", ctypes.c_int64)]
 
 
 class KernelTimesC(ctypes.Structure):
@@ -108,6 +110,8 @@ _SIGNATURES = {
     "moe_hash_weights_bf16": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
     "moe_hash_weights_f32": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
     "moe_tc_grouped_gemm_bf16": ([_P, _P, _P, _I32, _P, _I32, _I32, _I32, _I32, ctypes.POINTER(_F32), _P], _I32),
+    "moe_xc_encode": ([_P, _U64, _I32, _P, _U64, ctypes.POINTER(_U64)], _I32),
+    "moe_xc_decode": ([_P, _P, _P, _P], _I32),
     "moe_sample_zipf": ([_P, _I32, _I32, _I64, _I32, _P, _P, _P], _I32),
     "moe_sample_markov": ([_P, _I32, _I32, _I64, _I32, _F64, _P, _P, _P, _P], _I32),
     "moe_engine_decode_routed": ([_P, _P, _I64, _P, _P, _P], _I32),

@@ -69,6 +69,11 @@ cudaEvent_t take_sync_event(moe_engine* g) {
 struct DemandPlan {
   int n = 0;
   cudaEvent_t ev_a[kMaxK], ev_b[kMaxK];
+  // compressed transfer of miss k: decode the landing slot into the expert's buffer
+  bool comp[kMaxK] = {};
+  int slot[kMaxK] = {};
+  char* dst[kMaxK] = {};
+  const moe_engine::CPart* part[kMaxK][2] = {};
 };
 
 long long part_a_bytes(const moe_engine* g) {
@@ -97,7 +102,7 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
   for (int i = 0; i < m.n_demand; ++i) order[i] = i;
   std::sort(order, order + m.n_demand,
             [&](int x, int y) { return m.demand_expert[x] < m.demand_expert[y]; });
-  long long demand = 0;
+  long long demand = 0, link = 0;
   std::pair<cudaEvent_t, cudaEvent_t> tev{nullptr, nullptr};
   if (m.n_demand > 0) {
     tev = take_timing_events(g);
@@ -118,10 +123,36 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
       std::lock_guard<std::mutex> lk(g->stats_mu);
       g->st.prefetch_used += 1;
     }
+    plan->comp[k] = false;
+    if (g->cstore && from == 0) {
+      // exponent-coded: both parts land in slot k, the compute stream decodes them into the
+      // expert's buffer (the slot's previous decode must have finished first)
+      const int slot = k;
+      const auto& pa = g->ctab[(static_cast<size_t>(m.layer % g->SL) * g->cfg.num_experts + e) * 2];
+      const auto& pb = g->ctab[(static_cast<size_t>(m.layer % g->SL) * g->cfg.num_experts + e) * 2 + 1];
+      char* land = g->cstage + static_cast<long long>(slot) * g->expert_bytes;
+      MOE_CUDA(cudaStreamWaitEvent(g->copy_stream, g->cstage_free[slot], 0));
+      MOE_CUDA(cudaMemcpyAsync(land, g->cstore + pa.off, pa.size, cudaMemcpyHostToDevice, g->copy_stream));
+      plan->ev_a[k] = next_order_event(g);
+      MOE_CUDA(cudaEventRecord(plan->ev_a[k], g->copy_stream));
+      MOE_CUDA(cudaMemcpyAsync(land + pa.size, g->cstore + pb.off, pb.size, cudaMemcpyHostToDevice,
+                               g->copy_stream));
+      plan->ev_b[k] = next_order_event(g);
+      MOE_CUDA(cudaEventRecord(plan->ev_b[k], g->copy_stream));
+      plan->comp[k] = true;
+      plan->slot[k] = slot;
+      plan->dst[k] = g->pool + (static_cast<long long>(m.layer) * g->NB + b) * g->expert_bytes;
+      plan->part[k][0] = &pa;
+      plan->part[k][1] = &pb;
+      demand += g->expert_bytes;
+      link += static_cast<long long>(pa.size + pb.size);
+      continue;
+    }
     // part A: [from, split), then event; part B: [max(from, split), end), then event
     if (from < split) {
       TRY(issue_copy(g, m.layer, b, e, from, split - from));
       demand += split - from;
+      link += split - from;
     }
     plan->ev_a[k] = next_order_event(g);
     MOE_CUDA(cudaEventRecord(plan->ev_a[k], g->copy_stream));
@@ -129,6 +160,7 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
     if (fb < g->expert_bytes) {
       TRY(issue_copy(g, m.layer, b, e, fb, g->expert_bytes - fb));
       demand += g->expert_bytes - fb;
+      link += g->expert_bytes - fb;
     }
     plan->ev_b[k] = next_order_event(g);
     MOE_CUDA(cudaEventRecord(plan->ev_b[k], g->copy_stream));
@@ -139,7 +171,8 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
                                   nchunks, false, false});
   std::lock_guard<std::mutex> lk(g->stats_mu);
   g->st.demand_bytes += demand;
-  g->st.h2d_bytes += demand;
+  g->st.demand_link_bytes += link;
+  g->st.h2d_bytes += link;
   g->st.prefetch_issued += m.n_prefetch;
   if (m.n_demand > 0) g->busy_events.push_back(tev);
   return MOE_OK;
@@ -309,6 +342,51 @@ int round8(int x) { return (x + 7) / 8 * 8; }
 
 }  // namespace
 
+namespace {
+// Exponent-code every expert part of the host store into a second pinned store (once, after
+// the weights are written), and allocate the HBM landing slots.
+moe_status build_compressed_store(moe_engine* g) {
+  MOE_REQUIRE(!g->ext_store, "compressed transfers need a private expert store");
+  const int E = g->cfg.num_experts;
+  const long long na = 2ll * g->f * g->dpad, nb = 1ll * g->f * g->dpad;
+  if (g->cstore) {
+    cudaFreeHost(g->cstore);
+    g->cstore = nullptr;
+  }
+  g->ctab.assign(static_cast<size_t>(g->SL) * E * 2, moe_engine::CPart{});
+  uint64_t total = 0;
+  for (int l = 0; l < g->SL; ++l)
+    for (int e = 0; e < E; ++e)
+      for (int part = 0; part < 2; ++part) {
+        const uint16_t* w = reinterpret_cast<const uint16_t*>(g->store_block(l, e)) + (part ? na : 0);
+        auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * 2 + part];
+        c.off = total;
+        c.size = xc::encoded_size(w, part ? nb : na, 0);
+        total += c.size;
+      }
+  MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->cstore), total, cudaHostAllocPortable));
+  for (int l = 0; l < g->SL; ++l)
+    for (int e = 0; e < E; ++e)
+      for (int part = 0; part < 2; ++part) {
+        const uint16_t* w = reinterpret_cast<const uint16_t*>(g->store_block(l, e)) + (part ? na : 0);
+        auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * 2 + part];
+        xc::encode(w, part ? nb : na, 0, reinterpret_cast<uint8_t*>(g->cstore + c.off));
+        memcpy(&c.hdr, g->cstore + c.off, sizeof(c.hdr));
+      }
+  if (!g->cstage) {
+    const int slots = std::max(g->cfg.top_k, 1);
+    MOE_CUDA(cudaMalloc(reinterpret_cast<void**>(&g->cstage), static_cast<size_t>(slots) * g->expert_bytes));
+    for (int i = 0; i < slots; ++i) {
+      cudaEvent_t ev = nullptr;
+      MOE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      g->cstage_free.push_back(ev);
+    }
+  }
+  g->st.compressed_store_bytes = static_cast<int64_t>(total);
+  return MOE_OK;
+}
+}  // namespace
+
 extern "C" {
 
 moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) {
@@ -348,6 +426,10 @@ moe_status moe_engine_create_ex(const moe_engine_config* cfg_in, void* store, in
   MOE_REQUIRE(!(c.transfer == MOE_TRANSFER_SM && c.prefetch),
               "speculative prefetch runs on the copy engine (transfer=SM has no staging path)");
   MOE_REQUIRE(c.prefetch_buffers >= 0, "prefetch_buffers must be >= 0");
+  MOE_REQUIRE(!c.compress || c.expert_kind == MOE_EXPERT_SWIGLU_BF16,
+              "compressed transfers code bf16 experts (SwiGLU engines)");
+  MOE_REQUIRE(!c.compress || c.transfer != MOE_TRANSFER_SM,
+              "compressed transfers run on the copy engine (transfer=SM reads the raw store)");
   MOE_REQUIRE(c.cache_size + (c.prefetch ? c.top_k : 0) <= kMaxBuf,
               "cache_size + staging buffers must be <= %d", kMaxBuf);
 
@@ -368,7 +450,8 @@ moe_status moe_engine_create_ex(const moe_engine_config* cfg_in, void* store, in
     g->expert_bytes = 2ll * g->dpad * g->dpad * 4;
   }
   g->sm_transfer = c.transfer == MOE_TRANSFER_SM ||
-                   (c.transfer == MOE_TRANSFER_AUTO && !c.prefetch && g->expert_bytes <= (16ll << 20));
+                   (c.transfer == MOE_TRANSFER_AUTO && !c.prefetch && !c.compress &&
+                    g->expert_bytes <= (16ll << 20));
   g->S = c.prefetch ? (c.prefetch_buffers > 0 ? std::min(c.prefetch_buffers, c.top_k) : c.top_k) : 0;
   g->SL = c.store_layers > 0 ? std::min(c.store_layers, c.num_layers) : c.num_layers;
   g->NB = c.cache_size + g->S;
@@ -491,6 +574,9 @@ moe_status moe_engine_destroy(moe_engine* g) {
     for (auto e : a) cudaEventDestroy(e);
   if (g->prof_bytes_dev) cudaFree(g->prof_bytes_dev);
   if (g->pf) prefill_release(g->pf);
+  if (g->cstore) cudaFreeHost(g->cstore);
+  if (g->cstage) cudaFree(g->cstage);
+  for (auto e : g->cstage_free) cudaEventDestroy(e);
   if (g->graph_exec) cudaGraphExecDestroy(g->graph_exec);
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
   for (void* p : {static_cast<void*>(g->cursor), static_cast<void*>(g->cur_rec), static_cast<void*>(g->x_cur),
@@ -592,6 +678,7 @@ moe_status moe_engine_init_random(moe_engine* g, uint64_t seed, float gate_bias_
                                scratch, g->expert_bytes, cudaMemcpyDeviceToHost, s));
     }
   MOE_CUDA(cudaStreamSynchronize(s));
+  if (g->cfg.compress && init_experts) TRY(build_compressed_store(g));
   return MOE_OK;
 }
 
@@ -891,10 +978,21 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       if (g->bf16) {
         for (int i = 0; i < plan.n; ++i) {
           MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_a[i], 0));
+          if (plan.comp[i]) {
+            const char* land = g->cstage + static_cast<long long>(plan.slot[i]) * g->expert_bytes;
+            TRY(xc::decode(land, plan.part[i][0]->hdr, reinterpret_cast<uint16_t*>(plan.dst[i]), s));
+          }
           TRY(prof_begin(fev));
           TRY(launch_ffn(fp, i));
           TRY(prof_end(fev));
           MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_b[i], 0));
+          if (plan.comp[i]) {
+            const char* land = g->cstage + static_cast<long long>(plan.slot[i]) * g->expert_bytes +
+                               plan.part[i][0]->size;
+            TRY(xc::decode(land, plan.part[i][1]->hdr,
+                           reinterpret_cast<uint16_t*>(plan.dst[i] + part_a_bytes(g)), s));
+            MOE_CUDA(cudaEventRecord(g->cstage_free[plan.slot[i]], s));
+          }
           TRY(prof_begin(fev));
           TRY(launch_down(fp, i));
           TRY(prof_end(fev));
@@ -1108,6 +1206,7 @@ moe_status moe_engine_stats(moe_engine* g, moe_stats* out) {
   out->hits = static_cast<int64_t>(ds.hits);
   out->misses = static_cast<int64_t>(ds.misses);
   out->demand_bytes += static_cast<int64_t>(ds.fetched_bytes);
+  out->demand_link_bytes += static_cast<int64_t>(ds.fetched_bytes);
   out->h2d_bytes += static_cast<int64_t>(ds.fetched_bytes);
   out->tokens = g->tokens_done;
   out->steps = g->tokens_done * g->cfg.num_layers;

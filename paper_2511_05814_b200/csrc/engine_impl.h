@@ -1,6 +1,7 @@
 // Host-side state of one offload engine (engine.cu: decode; prefill.cu: batched prefill).
 #pragma once
 #include "engine_kernels.cuh"
+#include "expcodec.cuh"
 
 #include <sys/mman.h>
 #include <unistd.h>
@@ -134,6 +135,15 @@ struct moe_engine {
   HostControl* ctl_d = nullptr;
 
   PinnedStore store;
+  // exponent-coded copy of the store (compress = 1): parts A (w1|w3) and B (w2) per expert
+  struct CPart {
+    uint64_t off, size;
+    moe::xc::PartHeader hdr;
+  };
+  char* cstore = nullptr;                 // pinned host
+  std::vector<CPart> ctab;                // [(SL * E + e) * 2 + part]
+  char* cstage = nullptr;                 // HBM landing slots: [K][expert_bytes]
+  std::vector<cudaEvent_t> cstage_free;   // per slot: decoded (slot may be overwritten)
   const char* store_dev = nullptr;  // device view of the store (SM transfer)
   bool sm_transfer = false;
   // token graph (SM transfer): one token captured once, replayed per token

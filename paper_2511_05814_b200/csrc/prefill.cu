@@ -356,10 +356,27 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
       }
       MOE_CUDA(cudaEventRecord(tev.first, g->copy_stream));
     }
+    std::vector<char*> dest(m.n_loads);
     for (int i = 0; i < m.n_loads; ++i) {
       const int e = m.load_expert[i], dst = m.load_dst[i];
       char* to = dst >= 0 ? g->pool + (static_cast<long long>(l) * g->NB + dst) * g->expert_bytes
                           : pf->scratch + static_cast<long long>(-1 - dst) * g->expert_bytes;
+      dest[i] = to;
+      if (g->cstore) {
+        // exponent-coded: land in slot i % K (after that slot's previous decode), decode later
+        const int slot = i % static_cast<int>(g->cstage_free.size());
+        const auto& pa = g->ctab[(static_cast<size_t>(l % g->SL) * E + e) * 2];
+        const auto& pb = g->ctab[(static_cast<size_t>(l % g->SL) * E + e) * 2 + 1];
+        char* land = g->cstage + static_cast<long long>(slot) * g->expert_bytes;
+        MOE_CUDA(cudaStreamWaitEvent(g->copy_stream, g->cstage_free[slot], 0));
+        MOE_CUDA(cudaMemcpyAsync(land, g->cstore + pa.off, pa.size, cudaMemcpyHostToDevice, g->copy_stream));
+        MOE_CUDA(cudaEventRecord(pf->ev[2 * i], g->copy_stream));
+        MOE_CUDA(cudaMemcpyAsync(land + pa.size, g->cstore + pb.off, pb.size, cudaMemcpyHostToDevice,
+                                 g->copy_stream));
+        MOE_CUDA(cudaEventRecord(pf->ev[2 * i + 1], g->copy_stream));
+        loaded += static_cast<long long>(pa.size + pb.size);
+        continue;
+      }
       const char* from = g->store_block(l, e);
       MOE_CUDA(cudaMemcpyAsync(to, from, split, cudaMemcpyHostToDevice, g->copy_stream));
       MOE_CUDA(cudaEventRecord(pf->ev[2 * i], g->copy_stream));
@@ -411,9 +428,17 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
       TRY(ffn_down(0, m.res_rows, m.n_res_groups));
     }
     for (int i = 0; i < m.n_loads; ++i) {
+      const int slot = g->cstore ? i % static_cast<int>(g->cstage_free.size()) : 0;
+      const char* land = g->cstore ? g->cstage + static_cast<long long>(slot) * g->expert_bytes : nullptr;
+      const auto* pa = g->cstore ? &g->ctab[(static_cast<size_t>(l % g->SL) * E + m.load_expert[i]) * 2] : nullptr;
       MOE_CUDA(cudaStreamWaitEvent(s, pf->ev[2 * i], 0));
+      if (pa) TRY(xc::decode(land, pa->hdr, reinterpret_cast<uint16_t*>(dest[i]), s));
       TRY(ffn(1 + i, m.load_rows[i], 1));
       MOE_CUDA(cudaStreamWaitEvent(s, pf->ev[2 * i + 1], 0));
+      if (pa) {
+        TRY(xc::decode(land + pa->size, pa[1].hdr, reinterpret_cast<uint16_t*>(dest[i] + split), s));
+        MOE_CUDA(cudaEventRecord(g->cstage_free[slot], s));
+      }
       TRY(ffn_down(1 + i, m.load_rows[i], 1));
     }
     // experts that stay cached but were loaded into scratch move into their cache buffer

@@ -56,6 +56,7 @@ class EngineConfig:
     transfer: str = "auto"               # "auto" | "copy_engine" | "sm" (see moeb200.h)
     store_layers: int = 0                # host store depth (0 = num_layers; else layers alias l % S)
     prefetch_buffers: int = 0            # staging buffers per layer with prefetch (0 = top_k)
+    compress: bool = False               # exponent-coded (lossless) demand / prefill transfers
 
     @staticmethod
     def mixtral_8x7b(**kw) -> "EngineConfig":
@@ -107,7 +108,7 @@ class EngineConfig:
             max_tokens=self.max_tokens, chunk_bytes=self.chunk_bytes,
             prefetch_depth=self.prefetch_depth, device=self.device, rms_norm=int(self.rms_norm),
             rms_eps=self.rms_eps, transfer=transfers[self.transfer], store_layers=self.store_layers,
-            prefetch_buffers=self.prefetch_buffers)
+            prefetch_buffers=self.prefetch_buffers, compress=int(self.compress))
 
 
 class OffloadEngine:

@@ -188,3 +188,21 @@ def test_prefill_full_mixtral_8x7b_shape_two_layers():
     assert st["prefill_bytes"] == _needed_loads(rec, 8) * 352321536
     print(f"prefill GEMMs: {kt['gemm_launches']} launches {kt['gemm_ms']:.3f} ms "
           f"{kt['gemm_flops'] / kt['gemm_ms'] / 1e9:.1f} TFLOP/s; prefill {kt['prefill_ms']:.1f} ms")
+
+
+def test_prefill_compressed_loads_bit_exact():
+    cfg0 = small_cfg(cache_size=3, policy=PolicyKind.lru(), transfer="copy_engine")
+    cfg1 = small_cfg(cache_size=3, policy=PolicyKind.lru(), transfer="copy_engine", compress=True)
+    X = oracle.MixtralRef.inputs(31, 128, cfg0.hidden_dim)
+    res = []
+    for cfg in (cfg0, cfg1):
+        with OffloadEngine(cfg) as eng:
+            eng.init_random(31)
+            out = eng.prefill(X[:100])
+            out2 = eng.decode(X[100:])
+            res.append((out, out2, eng.records(0, 128), eng.stats()))
+    (a, a2, ra, sa), (b, b2, rb, sb) = res
+    assert np.array_equal(a, b) and np.array_equal(a2, b2)
+    for k in ("acts", "resident_before", "evicted", "probs"):
+        assert np.array_equal(ra[k], rb[k]), k
+    assert sb["prefill_bytes"] < 0.75 * sa["prefill_bytes"]
