@@ -71,7 +71,8 @@ struct DemandPlan {
   cudaEvent_t ev_a[kMaxK], ev_b[kMaxK];
   // compressed transfer of miss k: decode the landing slot into the expert's buffer
   bool comp[kMaxK] = {};
-  int slot[kMaxK] = {};
+  const char* land[kMaxK] = {};      // where the coded parts landed (A then B)
+  cudaEvent_t free_ev[kMaxK] = {};   // recorded once decoded: the landing area may be reused
   char* dst[kMaxK] = {};
   const moe_engine::CPart* part[kMaxK][2] = {};
 };
@@ -95,7 +96,7 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
       if (!j.cancelled && !j.adopted && j.layer == m.layer && j.buf == m.cancel_buf[i]) {
         j.cancelled = true;
         std::lock_guard<std::mutex> lk(g->stats_mu);
-        g->st.prefetch_wasted_bytes += std::min(j.next_chunk * chunk, g->expert_bytes);
+        g->st.prefetch_wasted_bytes += std::min(j.next_chunk * chunk, j.bytes);
       }
   // demand entries in ascending expert id (the order the phase-1 kernels enumerate misses)
   int order[kMaxK];
@@ -113,17 +114,49 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
     const int i = order[k];
     const int e = m.demand_expert[i], b = m.demand_buf[i];
     long long from = 0;
+    int zone = -1;
     if (m.demand_adopt[i]) {
       for (auto& j : g->jobs)
         if (!j.cancelled && !j.adopted && j.layer == m.layer && j.buf == b && j.expert == e) {
           j.adopted = true;
-          from = std::min(j.next_chunk * chunk, g->expert_bytes);
+          from = std::min(j.next_chunk * chunk, j.bytes);
+          zone = j.zone;
           break;
         }
       std::lock_guard<std::mutex> lk(g->stats_mu);
       g->st.prefetch_used += 1;
     }
     plan->comp[k] = false;
+    if (zone >= 0) {
+      // adopted compressed prefetch: finish the coded bytes in its zone, decode like a demand
+      const auto& pa = g->ctab[(static_cast<size_t>(m.layer % g->SL) * g->cfg.num_experts + e) * 2];
+      const auto& pb = g->ctab[(static_cast<size_t>(m.layer % g->SL) * g->cfg.num_experts + e) * 2 + 1];
+      char* land = g->pzone + static_cast<long long>(zone) * g->pzone_bytes;
+      const long long sa = static_cast<long long>(pa.size), tot = sa + static_cast<long long>(pb.size);
+      if (from < sa) {
+        MOE_CUDA(cudaMemcpyAsync(land + from, g->cstore + pa.off + from, sa - from, cudaMemcpyHostToDevice,
+                                 g->copy_stream));
+        link += sa - from;
+      }
+      plan->ev_a[k] = next_order_event(g);
+      MOE_CUDA(cudaEventRecord(plan->ev_a[k], g->copy_stream));
+      const long long fb = std::max(from, sa);
+      if (fb < tot) {
+        MOE_CUDA(cudaMemcpyAsync(land + fb, g->cstore + pa.off + fb, tot - fb, cudaMemcpyHostToDevice,
+                                 g->copy_stream));
+        link += tot - fb;
+      }
+      plan->ev_b[k] = next_order_event(g);
+      MOE_CUDA(cudaEventRecord(plan->ev_b[k], g->copy_stream));
+      plan->comp[k] = true;
+      plan->land[k] = land;
+      plan->free_ev[k] = g->pzone_free[zone];
+      plan->dst[k] = g->pool + (static_cast<long long>(m.layer) * g->NB + b) * g->expert_bytes;
+      plan->part[k][0] = &pa;
+      plan->part[k][1] = &pb;
+      demand += g->expert_bytes - static_cast<long long>(static_cast<double>(from) / tot * g->expert_bytes);
+      continue;
+    }
     if (g->cstore && from == 0) {
       // exponent-coded: both parts land in slot k, the compute stream decodes them into the
       // expert's buffer (the slot's previous decode must have finished first)
@@ -140,7 +173,8 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
       plan->ev_b[k] = next_order_event(g);
       MOE_CUDA(cudaEventRecord(plan->ev_b[k], g->copy_stream));
       plan->comp[k] = true;
-      plan->slot[k] = slot;
+      plan->land[k] = land;
+      plan->free_ev[k] = g->cstage_free[slot];
       plan->dst[k] = g->pool + (static_cast<long long>(m.layer) * g->NB + b) * g->expert_bytes;
       plan->part[k][0] = &pa;
       plan->part[k][1] = &pb;
@@ -166,9 +200,18 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
     MOE_CUDA(cudaEventRecord(plan->ev_b[k], g->copy_stream));
   }
   if (m.n_demand > 0) MOE_CUDA(cudaEventRecord(tev.second, g->copy_stream));
-  for (int i = 0; i < m.n_prefetch; ++i)
-    g->jobs.push_back(PrefetchJob{m.layer + 1, m.prefetch_buf[i], m.prefetch_expert[i], 0,
-                                  nchunks, false, false});
+  for (int i = 0; i < m.n_prefetch; ++i) {
+    PrefetchJob j{m.layer + 1, m.prefetch_buf[i], m.prefetch_expert[i], 0, nchunks, false, false};
+    j.bytes = g->expert_bytes;
+    if (g->pzone) {
+      const size_t ci = (static_cast<size_t>((m.layer + 1) % g->SL) * g->cfg.num_experts + j.expert) * 2;
+      j.zone = g->pzone_next;
+      g->pzone_next = (g->pzone_next + 1) % static_cast<int>(g->pzone_free.size());
+      j.bytes = static_cast<long long>(g->ctab[ci].size + g->ctab[ci + 1].size);
+      j.n_chunks = (j.bytes + chunk - 1) / chunk;
+    }
+    g->jobs.push_back(j);
+  }
   std::lock_guard<std::mutex> lk(g->stats_mu);
   g->st.demand_bytes += demand;
   g->st.demand_link_bytes += link;
@@ -213,9 +256,17 @@ moe_status pump_prefetch(moe_engine* g, bool* did) {
   if (g->prefetch_inflight.size() >= static_cast<size_t>(g->cfg.prefetch_depth)) return MOE_OK;
   PrefetchJob& j = g->jobs.front();
   const long long chunk = g->cfg.chunk_bytes;
-  const long long off = j.next_chunk * chunk, n = std::min(chunk, g->expert_bytes - off);
-  moe_status s = issue_copy(g, j.layer, j.buf, j.expert, off, n);
-  if (s != MOE_OK) return s;
+  const long long off = j.next_chunk * chunk, n = std::min(chunk, j.bytes - off);
+  if (j.zone >= 0) {
+    // coded bytes into the job's landing zone (after the zone's previous decode)
+    const size_t ci = (static_cast<size_t>(j.layer % g->SL) * g->cfg.num_experts + j.expert) * 2;
+    if (j.next_chunk == 0) MOE_CUDA(cudaStreamWaitEvent(g->copy_stream, g->pzone_free[j.zone], 0));
+    MOE_CUDA(cudaMemcpyAsync(g->pzone + static_cast<long long>(j.zone) * g->pzone_bytes + off,
+                             g->cstore + g->ctab[ci].off + off, n, cudaMemcpyHostToDevice, g->copy_stream));
+  } else {
+    moe_status s = issue_copy(g, j.layer, j.buf, j.expert, off, n);
+    if (s != MOE_OK) return s;
+  }
   j.next_chunk += 1;
   cudaEvent_t ev = take_sync_event(g);
   MOE_CUDA(cudaEventRecord(ev, g->copy_stream));
@@ -380,6 +431,18 @@ moe_status build_compressed_store(moe_engine* g) {
       cudaEvent_t ev = nullptr;
       MOE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
       g->cstage_free.push_back(ev);
+    }
+  }
+  if (g->S > 0 && !g->pzone) {
+    uint64_t mx = 0;
+    for (size_t i = 0; i + 1 < g->ctab.size(); i += 2) mx = std::max<uint64_t>(mx, g->ctab[i].size + g->ctab[i + 1].size);
+    g->pzone_bytes = static_cast<long long>(xc::align16(mx));
+    const int zones = 2 * g->cfg.top_k;
+    MOE_CUDA(cudaMalloc(reinterpret_cast<void**>(&g->pzone), static_cast<size_t>(zones) * g->pzone_bytes));
+    for (int i = 0; i < zones; ++i) {
+      cudaEvent_t ev = nullptr;
+      MOE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      g->pzone_free.push_back(ev);
     }
   }
   g->st.compressed_store_bytes = static_cast<int64_t>(total);
@@ -576,6 +639,8 @@ moe_status moe_engine_destroy(moe_engine* g) {
   if (g->pf) prefill_release(g->pf);
   if (g->cstore) cudaFreeHost(g->cstore);
   if (g->cstage) cudaFree(g->cstage);
+  if (g->pzone) cudaFree(g->pzone);
+  for (auto e : g->pzone_free) cudaEventDestroy(e);
   for (auto e : g->cstage_free) cudaEventDestroy(e);
   if (g->graph_exec) cudaGraphExecDestroy(g->graph_exec);
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
@@ -978,20 +1043,16 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       if (g->bf16) {
         for (int i = 0; i < plan.n; ++i) {
           MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_a[i], 0));
-          if (plan.comp[i]) {
-            const char* land = g->cstage + static_cast<long long>(plan.slot[i]) * g->expert_bytes;
-            TRY(xc::decode(land, plan.part[i][0]->hdr, reinterpret_cast<uint16_t*>(plan.dst[i]), s));
-          }
+          if (plan.comp[i])
+            TRY(xc::decode(plan.land[i], plan.part[i][0]->hdr, reinterpret_cast<uint16_t*>(plan.dst[i]), s));
           TRY(prof_begin(fev));
           TRY(launch_ffn(fp, i));
           TRY(prof_end(fev));
           MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_b[i], 0));
           if (plan.comp[i]) {
-            const char* land = g->cstage + static_cast<long long>(plan.slot[i]) * g->expert_bytes +
-                               plan.part[i][0]->size;
-            TRY(xc::decode(land, plan.part[i][1]->hdr,
+            TRY(xc::decode(plan.land[i] + plan.part[i][0]->size, plan.part[i][1]->hdr,
                            reinterpret_cast<uint16_t*>(plan.dst[i] + part_a_bytes(g)), s));
-            MOE_CUDA(cudaEventRecord(g->cstage_free[plan.slot[i]], s));
+            MOE_CUDA(cudaEventRecord(plan.free_ev[i], s));
           }
           TRY(prof_begin(fev));
           TRY(launch_down(fp, i));

@@ -100,6 +100,9 @@ struct PrefetchJob {
   int layer, buf, expert;
   long long next_chunk, n_chunks;
   bool cancelled, adopted;
+  int zone = -1;        // compressed: landing zone of the exponent-coded expert (-1: raw copy
+                        // straight into the staging buffer)
+  long long bytes = 0;  // bytes this job moves (expert_bytes raw, or the coded size)
 };
 
 }  // namespace moe
@@ -144,6 +147,10 @@ struct moe_engine {
   std::vector<CPart> ctab;                // [(SL * E + e) * 2 + part]
   char* cstage = nullptr;                 // HBM landing slots: [K][expert_bytes]
   std::vector<cudaEvent_t> cstage_free;   // per slot: decoded (slot may be overwritten)
+  char* pzone = nullptr;                  // prefetch landing zones [NZ][pzone_bytes]
+  long long pzone_bytes = 0;
+  std::vector<cudaEvent_t> pzone_free;    // per zone: decoded
+  int pzone_next = 0;
   const char* store_dev = nullptr;  // device view of the store (SM transfer)
   bool sm_transfer = false;
   // token graph (SM transfer): one token captured once, replayed per token
