@@ -355,7 +355,10 @@ def run_ours(args, world, rank, local):
     if want_prefetch and nl * (cap_c + base_cfg.top_k) * base_cfg.expert_bytes + dense > 0.9 * hbm:
         pf_bufs = 1
     shared = world > 1 or args.shared_store
-    compress = args.compress == "on" or (args.compress == "auto" and not shared)
+    raw_store = (min(store_layers, nl) if store_layers > 0 else nl) * base_cfg.num_experts * base_cfg.expert_bytes
+    # the coded store (~0.7x) sits beside the raw one in pinned host memory
+    compress = args.compress == "on" or (args.compress == "auto" and not shared and
+                                         1.75 * raw_store <= 0.85 * host_available_bytes())
     cfg = factory(num_layers=nl, cache_size=cap_c, prefetch="early" if want_prefetch else "off",
                   max_tokens=4096, device=local, store_layers=store_layers,
                   prefetch_buffers=pf_bufs, compress=compress)
