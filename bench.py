@@ -357,7 +357,7 @@ def run_ours(args, world, rank, local):
     shared = world > 1 or args.shared_store
     raw_store = (min(store_layers, nl) if store_layers > 0 else nl) * base_cfg.num_experts * base_cfg.expert_bytes
     # the coded store (~0.7x) sits beside the raw one in pinned host memory
-    compress = args.compress == "on" or (args.compress == "auto" and not shared and
+    compress = args.compress == "on" or (args.compress == "auto" and
                                          1.75 * raw_store <= 0.85 * host_available_bytes())
     cfg = factory(num_layers=nl, cache_size=cap_c, prefetch="early" if want_prefetch else "off",
                   max_tokens=4096, device=local, store_layers=store_layers,
@@ -370,6 +370,7 @@ def run_ours(args, world, rank, local):
 
     t_setup = time.perf_counter()
     store = None
+    coded = None
     local_rank, local_world = replicas.local_world()
     if world > 1 or args.shared_store:
         # one host copy of the experts per node, page-locked by every local replica
@@ -386,6 +387,8 @@ def run_ours(args, world, rank, local):
         if eng is None:
             eng = OffloadEngine(cfg, store=store)
             eng.init_random(args.seed, init_experts=False)
+        if cfg.compress:
+            coded = replicas.open_shared_coded(name + "x", eng, local_rank, lambda: barrier(world))
     else:
         eng = OffloadEngine(cfg)
         eng.init_random(args.seed)
@@ -480,6 +483,9 @@ def run_ours(args, world, rank, local):
     if args.prefill_tokens > 0:
         prefill = run_prefill(args, eng, inputs, base, stream, world, pcie_peak)
     eng.close()
+    if coded is not None:
+        barrier(world)
+        coded.close()
     gemm_iso = isolated_gemm(D, F) if rank == 0 and args.prefill_tokens > 0 else None
     tiny = run_tiny(args) if rank == 0 and world == 1 and args.tiny_tokens > 0 else None
     if store is not None:

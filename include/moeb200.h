@@ -200,6 +200,12 @@ moe_status moe_engine_init_random(moe_engine* eng, uint64_t seed, float gate_bia
 /* Host view of one expert block in the pinned store ([w1 | w3 | w2] bf16 or [W1t | W2t] f32). */
 moe_status moe_engine_expert_host_ptr(moe_engine* eng, int32_t layer, int32_t expert,
                                       void** ptr, int64_t* bytes);
+/* Node-shared coded store (compress = 1 with a caller-owned raw store): the raw experts must be
+ * written first.  coded_size returns the bytes of the coded segment (layout planned from the
+ * raw store); attach_coded with build = 1 encodes into `seg` (the segment's owner), build = 0
+ * reads an already built segment (the other replicas).  The segment is page-locked. */
+moe_status moe_engine_coded_size(moe_engine* eng, int64_t* bytes);
+moe_status moe_engine_attach_coded(moe_engine* eng, void* seg, int64_t seg_bytes, int32_t build);
 /* Copy back the device-layout dense weights (for the oracle): mixing (d,d) in the device
  * dtype's bytes, gate_w (E,d) f32, gate_b (E,) f32; host destinations. */
 moe_status moe_engine_dense_host(moe_engine* eng, int32_t layer, void* mixing, float* gate_w,

@@ -35,7 +35,7 @@ EXPORTED = (
     "moe_tc_grouped_gemm_bf16", "moe_tc_grouped_swiglu_bf16",
     "moe_text_data", "moe_text_size", "moe_text_free", "moe_format_trace", "moe_format_event_log",
     "moe_sample_zipf", "moe_sample_markov", "moe_engine_decode_routed", "moe_engine_prefill_routed",
-    "moe_xc_encode", "moe_xc_decode",
+    "moe_xc_encode", "moe_xc_decode", "moe_engine_coded_size", "moe_engine_attach_coded",
 )
 
 
@@ -110,6 +110,8 @@ _SIGNATURES = {
     "moe_hash_weights_bf16": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
     "moe_hash_weights_f32": ([_U64, _U64, _F32, _I64, _P, _P], _I32),
     "moe_tc_grouped_gemm_bf16": ([_P, _P, _P, _I32, _P, _I32, _I32, _I32, _I32, ctypes.POINTER(_F32), _P], _I32),
+    "moe_engine_coded_size": ([_P, ctypes.POINTER(_I64)], _I32),
+    "moe_engine_attach_coded": ([_P, _P, _I64, _I32], _I32),
     "moe_xc_encode": ([_P, _U64, _I32, _P, _U64, ctypes.POINTER(_U64)], _I32),
     "moe_xc_decode": ([_P, _P, _P, _P], _I32),
     "moe_sample_zipf": ([_P, _I32, _I32, _I64, _I32, _P, _P, _P], _I32),

@@ -394,36 +394,59 @@ int round8(int x) { return (x + 7) / 8 * 8; }
 }  // namespace
 
 namespace {
-// Exponent-code every expert part of the host store into a second pinned store (once, after
-// the weights are written), and allocate the HBM landing slots.
-moe_status build_compressed_store(moe_engine* g) {
-  MOE_REQUIRE(!g->ext_store, "compressed transfers need a private expert store");
+// The exponent-coded store (compress = 1): a table of parts [(SL * E + e) * 2 + part] and the
+// parts themselves, either in a private pinned buffer or in a caller's (node-shared) segment:
+//   CodedSegHeader | CodedEntry[n] | parts (16-byte aligned)
+struct CodedSegHeader {
+  uint64_t magic, n_entries, data_off, total;
+};
+struct CodedEntry {
+  uint64_t off, size;  // relative to the segment base
+  xc::PartHeader hdr;
+};
+constexpr uint64_t kCodedMagic = 0x4d4f45584332ull;  // "MOEXC2"
+
+// Sizes of every part from the raw store (the layout of a coded segment).
+moe_status plan_coded(moe_engine* g) {
   const int E = g->cfg.num_experts;
   const long long na = 2ll * g->f * g->dpad, nb = 1ll * g->f * g->dpad;
-  if (g->cstore) {
-    cudaFreeHost(g->cstore);
-    g->cstore = nullptr;
-  }
-  g->ctab.assign(static_cast<size_t>(g->SL) * E * 2, moe_engine::CPart{});
-  uint64_t total = 0;
+  const size_t n = static_cast<size_t>(g->SL) * E * 2;
+  g->ctab.assign(n, moe_engine::CPart{});
+  uint64_t off = xc::align16(sizeof(CodedSegHeader) + sizeof(CodedEntry) * n);
   for (int l = 0; l < g->SL; ++l)
     for (int e = 0; e < E; ++e)
       for (int part = 0; part < 2; ++part) {
         const uint16_t* w = reinterpret_cast<const uint16_t*>(g->store_block(l, e)) + (part ? na : 0);
         auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * 2 + part];
-        c.off = total;
+        c.off = off;
         c.size = xc::encoded_size(w, part ? nb : na, 0);
-        total += c.size;
+        off += c.size;
       }
-  MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->cstore), total, cudaHostAllocPortable));
+  g->coded_total = off;
+  return MOE_OK;
+}
+
+// Encode the planned parts into `seg` (host) and write its table.
+void encode_coded(moe_engine* g, char* seg) {
+  const int E = g->cfg.num_experts;
+  const long long na = 2ll * g->f * g->dpad, nb = 1ll * g->f * g->dpad;
   for (int l = 0; l < g->SL; ++l)
     for (int e = 0; e < E; ++e)
       for (int part = 0; part < 2; ++part) {
         const uint16_t* w = reinterpret_cast<const uint16_t*>(g->store_block(l, e)) + (part ? na : 0);
         auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * 2 + part];
-        xc::encode(w, part ? nb : na, 0, reinterpret_cast<uint8_t*>(g->cstore + c.off));
-        memcpy(&c.hdr, g->cstore + c.off, sizeof(c.hdr));
+        xc::encode(w, part ? nb : na, 0, reinterpret_cast<uint8_t*>(seg + c.off));
+        memcpy(&c.hdr, seg + c.off, sizeof(c.hdr));
       }
+  CodedSegHeader h{kCodedMagic, g->ctab.size(), 0, g->coded_total};
+  h.data_off = xc::align16(sizeof(CodedSegHeader) + sizeof(CodedEntry) * g->ctab.size());
+  memcpy(seg, &h, sizeof(h));
+  CodedEntry* ent = reinterpret_cast<CodedEntry*>(seg + sizeof(CodedSegHeader));
+  for (size_t i = 0; i < g->ctab.size(); ++i) ent[i] = CodedEntry{g->ctab[i].off, g->ctab[i].size, g->ctab[i].hdr};
+}
+
+// HBM landing slots for demand misses (K) and prefetch zones (2K when prefetch is on).
+moe_status alloc_landing(moe_engine* g) {
   if (!g->cstage) {
     const int slots = std::max(g->cfg.top_k, 1);
     MOE_CUDA(cudaMalloc(reinterpret_cast<void**>(&g->cstage), static_cast<size_t>(slots) * g->expert_bytes));
@@ -445,7 +468,19 @@ moe_status build_compressed_store(moe_engine* g) {
       g->pzone_free.push_back(ev);
     }
   }
-  g->st.compressed_store_bytes = static_cast<int64_t>(total);
+  return MOE_OK;
+}
+
+// Private coded store: plan, pinned allocation, encode, landing buffers.
+moe_status build_compressed_store(moe_engine* g) {
+  if (g->cstore && !g->cstore_external) cudaFreeHost(g->cstore);
+  g->cstore = nullptr;
+  TRY(plan_coded(g));
+  MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->cstore), g->coded_total, cudaHostAllocPortable));
+  g->cstore_external = false;
+  encode_coded(g, g->cstore);
+  TRY(alloc_landing(g));
+  g->st.compressed_store_bytes = static_cast<int64_t>(g->coded_total);
   return MOE_OK;
 }
 }  // namespace
@@ -637,7 +672,8 @@ moe_status moe_engine_destroy(moe_engine* g) {
     for (auto e : a) cudaEventDestroy(e);
   if (g->prof_bytes_dev) cudaFree(g->prof_bytes_dev);
   if (g->pf) prefill_release(g->pf);
-  if (g->cstore) cudaFreeHost(g->cstore);
+  if (g->cstore && !g->cstore_external) cudaFreeHost(g->cstore);
+  if (g->cstore && g->cstore_external && g->cstore_registered) cudaHostUnregister(g->cstore);
   if (g->cstage) cudaFree(g->cstage);
   if (g->pzone) cudaFree(g->pzone);
   for (auto e : g->pzone_free) cudaEventDestroy(e);
@@ -743,7 +779,50 @@ moe_status moe_engine_init_random(moe_engine* g, uint64_t seed, float gate_bias_
                                scratch, g->expert_bytes, cudaMemcpyDeviceToHost, s));
     }
   MOE_CUDA(cudaStreamSynchronize(s));
-  if (g->cfg.compress && init_experts) TRY(build_compressed_store(g));
+  // a private store is coded here; replicas of a node-shared store attach a shared coded
+  // segment instead (moe_engine_coded_size / moe_engine_attach_coded)
+  if (g->cfg.compress && init_experts && !g->ext_store) TRY(build_compressed_store(g));
+  return MOE_OK;
+}
+
+moe_status moe_engine_coded_size(moe_engine* g, int64_t* bytes) {
+  MOE_REQUIRE(g && bytes, "null argument");
+  MOE_REQUIRE(g->cfg.compress, "the engine was created with compress = 0");
+  TRY(plan_coded(g));
+  *bytes = static_cast<int64_t>(g->coded_total);
+  return MOE_OK;
+}
+
+moe_status moe_engine_attach_coded(moe_engine* g, void* seg, int64_t seg_bytes, int32_t build) {
+  MOE_REQUIRE(g && seg, "null argument");
+  MOE_REQUIRE(g->cfg.compress, "the engine was created with compress = 0");
+  MOE_CUDA(cudaSetDevice(g->device));
+  char* base = static_cast<char*>(seg);
+  if (build) {
+    if (g->ctab.empty()) TRY(plan_coded(g));
+    MOE_REQUIRE(static_cast<uint64_t>(seg_bytes) >= g->coded_total, "coded segment holds %lld bytes, needs %llu",
+                (long long)seg_bytes, (unsigned long long)g->coded_total);
+    encode_coded(g, base);
+  } else {
+    CodedSegHeader h;
+    memcpy(&h, base, sizeof(h));
+    MOE_REQUIRE(h.magic == kCodedMagic && h.n_entries == static_cast<uint64_t>(g->SL) * g->cfg.num_experts * 2 &&
+                    h.total <= static_cast<uint64_t>(seg_bytes),
+                "not a coded expert segment of this model");
+    const CodedEntry* ent = reinterpret_cast<const CodedEntry*>(base + sizeof(CodedSegHeader));
+    g->ctab.assign(h.n_entries, moe_engine::CPart{});
+    for (size_t i = 0; i < h.n_entries; ++i) g->ctab[i] = moe_engine::CPart{ent[i].off, ent[i].size, ent[i].hdr};
+    g->coded_total = h.total;
+  }
+  if (g->cstore && !g->cstore_external) cudaFreeHost(g->cstore);
+  const cudaError_t re = cudaHostRegister(base, g->coded_total, cudaHostRegisterPortable);
+  if (re == cudaErrorHostMemoryAlreadyRegistered) cudaGetLastError();  // another engine did
+  else MOE_CUDA(re);
+  g->cstore_registered = re == cudaSuccess;
+  g->cstore = base;
+  g->cstore_external = true;
+  TRY(alloc_landing(g));
+  g->st.compressed_store_bytes = static_cast<int64_t>(g->coded_total);
   return MOE_OK;
 }
 

@@ -40,7 +40,12 @@ struct PinnedStore {
     base = static_cast<char*>(p);
     bytes = n;
     external = true;
-    MOE_CUDA(cudaHostRegister(base, n, cudaHostRegisterPortable | cudaHostRegisterMapped));
+    const cudaError_t e = cudaHostRegister(base, n, cudaHostRegisterPortable | cudaHostRegisterMapped);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {  // another engine of this process did
+      cudaGetLastError();
+      return MOE_OK;
+    }
+    MOE_CUDA(e);
     registered = true;
     return MOE_OK;
   }
@@ -143,7 +148,10 @@ struct moe_engine {
     uint64_t off, size;
     moe::xc::PartHeader hdr;
   };
-  char* cstore = nullptr;                 // pinned host
+  char* cstore = nullptr;                 // pinned host (private) or a registered shared segment
+  bool cstore_external = false;
+  bool cstore_registered = false;
+  uint64_t coded_total = 0;
   std::vector<CPart> ctab;                // [(SL * E + e) * 2 + part]
   char* cstage = nullptr;                 // HBM landing slots: [K][expert_bytes]
   std::vector<cudaEvent_t> cstage_free;   // per slot: decoded (slot may be overwritten)

@@ -160,6 +160,19 @@ class OffloadEngine:
         _native.check(self._lib.moe_engine_init_random(self._h, int(seed), float(gate_bias_std),
                                                        int(init_experts)))
 
+    def coded_size(self) -> int:
+        """Bytes of the exponent-coded store (compress=True; raw experts already written)."""
+        n = ctypes.c_int64()
+        _native.check(self._lib.moe_engine_coded_size(self._h, ctypes.byref(n)))
+        return n.value
+
+    def attach_coded(self, segment, build: bool) -> None:
+        """Use a node-shared coded segment (replicas.SharedExpertStore): build=True encodes
+        into it (the owner), build=False reads one the owner built."""
+        _native.check(self._lib.moe_engine_attach_coded(self._h, segment.address, segment.nbytes,
+                                                        int(build)))
+        self._coded = segment
+
     def load_toy_model(self, model) -> None:
         """Upload a ToyMoeModel's weights (reference layout, rounded to f32)."""
         cfg = self.config

@@ -91,6 +91,20 @@ def open_shared_store(name: str, nbytes: int, local_rank: int,
     return SharedExpertStore.attach(name)
 
 
+def open_shared_coded(name: str, engine, local_rank: int, barrier: Callable[[], None]):
+    """The exponent-coded copy of a node-shared store: local rank 0 sizes, creates and encodes
+    it through its engine; the other ranks attach after the barrier.  Returns the segment."""
+    if local_rank == 0:
+        seg = SharedExpertStore.create(name, engine.coded_size())
+        engine.attach_coded(seg, build=True)
+        barrier()
+        return seg
+    barrier()
+    seg = SharedExpertStore.attach(name)
+    engine.attach_coded(seg, build=False)
+    return seg
+
+
 def local_world() -> tuple:
     """(local_rank, local_world_size) from the torch.distributed.run environment."""
     return int(os.environ.get("LOCAL_RANK", "0")), int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
