@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
   const bool active = first < h.n;
   const int cnt = active ? static_cast<int>(h.n - first < 32 ? h.n - first : 32) : 0;
   uint32_t lo[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  unsigned __int128 bits = 0;
+  // the thread's 32 codes as two 64-bit words: codes 0..15 in c0, 16..31 in c1
+  uint64_t c0 = 0, c1 = 0;
   int esc_mask_n = 0;
   uint32_t escm = 0;
   if (active) {
@@ -145,16 +146,19 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
     lo[4] = l1.x; lo[5] = l1.y; lo[6] = l1.z; lo[7] = l1.w;
     if constexpr (K == 4) {
       const uint4 q = *reinterpret_cast<const uint4*>(part + h.code_off + first / 2);
-      bits = (static_cast<unsigned __int128>((static_cast<uint64_t>(q.w) << 32) | q.z) << 64) |
-             ((static_cast<uint64_t>(q.y) << 32) | q.x);
+      c0 = (static_cast<uint64_t>(q.y) << 32) | q.x;
+      c1 = (static_cast<uint64_t>(q.w) << 32) | q.z;
     } else {
       const uint32_t* q = reinterpret_cast<const uint32_t*>(part + h.code_off + first * 3 / 8);
-      bits = (static_cast<unsigned __int128>(q[2]) << 64) |
-             ((static_cast<uint64_t>(q[1]) << 32) | q[0]);
+      const uint32_t w0 = q[0], w1 = q[1], w2 = q[2];
+      c0 = (static_cast<uint64_t>(w1) << 32) | w0;                    // stream bits 0..63
+      c1 = (static_cast<uint64_t>(w2) << 16) | (w1 >> 16);            // stream bits 48..95
     }
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < cnt && !static_cast<uint32_t>((bits >> (K * j)) & ((1u << K) - 1))) escm |= 1u << j;
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t code = static_cast<uint32_t>((j < 16 ? c0 >> (K * j) : c1 >> (K * (j - 16))) & ((1u << K) - 1));
+      if (j < cnt && !code) escm |= 1u << j;
+    }
     esc_mask_n = __popc(escm);
   }
   // exclusive scan of escape counts across the CTA (element order)
@@ -177,15 +181,13 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     const uint32_t b8 = (lo[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-    const uint32_t code = static_cast<uint32_t>((bits >> (K * j)) & ((1u << K) - 1));
-    uint32_t ex;
-    if (code) {
-      ex = static_cast<uint32_t>(ce.base) + 1u - code;
-    } else {
-      ex = (j < cnt) ? esc[e] : 0u;
-      e += (j < cnt);
+    const uint32_t code = static_cast<uint32_t>((j < 16 ? c0 >> (K * j) : c1 >> (K * (j - 16))) & ((1u << K) - 1));
+    uint32_t ex = (static_cast<uint32_t>(ce.base) + 1u - code) & 0xFFu;
+    if ((escm >> j) & 1u) {  // rare (~1 % of weights at k = 3): exponent from the side list
+      ex = esc[e];
+      ++e;
     }
-    const uint32_t w = ((b8 & 0x80u) << 8) | ((ex & 0xFFu) << 7) | (b8 & 0x7Fu);
+    const uint32_t w = ((b8 & 0x80u) << 8) | (ex << 7) | (b8 & 0x7Fu);
     if (j & 1) o[j >> 1] |= w << 16;
     else o[j >> 1] = w;
   }
@@ -196,7 +198,9 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
     op[2] = make_uint4(o[8], o[9], o[10], o[11]);
     op[3] = make_uint4(o[12], o[13], o[14], o[15]);
   } else {
-    for (int j = 0; j < cnt; ++j) out[first + j] = static_cast<uint16_t>(o[j >> 1] >> (16 * (j & 1)));
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < cnt) out[first + j] = static_cast<uint16_t>(o[j >> 1] >> (16 * (j & 1)));
   }
 }
 
