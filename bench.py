@@ -243,15 +243,17 @@ def committed_ffn_traffic():
 
 # ---- CPU path (oracle port of the reference, test-infrastructure only) -------------------
 
-def cpu_reference_sample(seed: int, tokens: int, layers: int, warmup: int = 1) -> dict:
+def cpu_reference_sample(seed: int, tokens: int, layers: int, warmup: int = 1,
+                         shape=(L, E, K, D, F)) -> dict:
     """Time the oracle port (numpy fp64, reference `h @ W` layout, all host threads) on the
     first `tokens` tokens of the same stream through `layers` layers; return tokens/s scaled
-    to the full L=32 model.  Weights are materialised (untimed) by a first pass."""
+    to the full model depth.  Weights are materialised (untimed) by a first pass."""
     import numpy as np
 
     import oracle
     from oracle.model import replay_layers
 
+    L, E, K, D, F = shape
     alpha = 0.1 * math.sqrt(16 / D)
     ref = oracle.MixtralRef(L, E, K, D, F, alpha, seed=seed, layout="ref",
                             layers=list(range(layers)), rms_norm=True)
@@ -364,8 +366,13 @@ def run_ours(args, world, rank, local):
                   prefetch_buffers=pf_bufs, compress=compress)
     D, F, EB = cfg.hidden_dim, cfg.ffn_dim, cfg.expert_bytes
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.model == "mixtral_8x7b":
-        cpu = cpu_reference_sample(args.seed, args.cpu_sample_tokens, args.cpu_sample_layers)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if args.model == "mixtral_8x7b":
+            cpu = cpu_reference_sample(args.seed, args.cpu_sample_tokens, args.cpu_sample_layers)
+        else:  # configs[4]: a bounded sample (fp64 8x22B experts are 2.4 GB each)
+            cpu = cpu_reference_sample(args.seed, 4, 1, shape=(base_cfg.num_layers, base_cfg.num_experts,
+                                                              base_cfg.top_k, base_cfg.hidden_dim,
+                                                              base_cfg.ffn_dim))
     pcie_peak = h2d_peak_gbs(dev)
 
     t_setup = time.perf_counter()
@@ -727,6 +734,8 @@ def run_prefill(args, eng, inputs, base, stream, world, pcie_peak):
                  "algorithmic_GBps": k["gemm_bytes"] / (k["gemm_ms"] / 1e3) / 1e9 if k["gemm_ms"] else None,
                  "share_of_prefill": k["gemm_ms"] / ms_p},
     }
+    if not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_prefill_sample(args.seed, P, X)
     if args.prefill_decode > 0:
         xs = inputs[: args.prefill_decode]
         h0 = eng.stats()
@@ -741,6 +750,29 @@ def run_prefill(args, eng, inputs, base, stream, world, pcie_peak):
                                        "tokens_per_s": args.prefill_decode / (ms_d / 1e3),
                                        "hit_rate": dh / max(1, dh + dm)}
     return out
+
+
+def cpu_prefill_sample(seed, P, X, layers=1):
+    """configs[3] CPU side: the oracle's batched prefill restatement (numpy fp64, the
+    reference's `h @ W` layout, all host threads) over the same P tokens on `layers` of the 32
+    layers, scaled by 32 / layers; the experts are materialised untimed first."""
+    import oracle
+
+    alpha = 0.1 * math.sqrt(16 / D)
+    ref = oracle.MixtralRef(L, E, K, D, F, alpha, seed=seed, layout="ref",
+                            layers=list(range(layers)), rms_norm=True)
+    t_gen = time.perf_counter()
+    ref.materialize()
+    t_gen = time.perf_counter() - t_gen
+    x = X.cpu().numpy()
+    t0 = time.perf_counter()
+    oracle.mixtral_prefill(ref, x)
+    dt = time.perf_counter() - t0
+    per_batch = dt * (L / layers)
+    return {"value": P / per_batch, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{P} tokens x {layers} of {L} layers (oracle.mixtral_prefill, numpy fp64 "
+                      f"batched GEMMs), scaled by {L}/{layers}; {dt:.1f} s timed, {t_gen:.1f} s "
+                      "untimed weight materialisation"}
 
 
 def isolated_gemm(Dd, Ff):
