@@ -132,6 +132,19 @@ def sum_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def broadcast_ints(values, world):
+    """Rank 0's integers on every rank (identical engine configs across replicas)."""
+    if world == 1:
+        return values
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    t = torch.tensor(values, dtype=torch.int64, device=dev)
+    dist.broadcast(t, src=0)
+    return [int(v) for v in t.tolist()]
+
+
 # ---- clocks ------------------------------------------------------------------------------
 
 class ClockSampler:
@@ -361,6 +374,9 @@ def run_ours(args, world, rank, local):
     # the coded store (~0.7x) sits beside the raw one in pinned host memory
     compress = args.compress == "on" or (args.compress == "auto" and
                                          1.75 * raw_store <= 0.85 * host_available_bytes())
+    # every replica must build the same engine (shared stores): rank 0's host view decides
+    store_layers, pf_bufs, compress = broadcast_ints([store_layers, pf_bufs, int(compress)], world)
+    compress = bool(compress)
     cfg = factory(num_layers=nl, cache_size=cap_c, prefetch="early" if want_prefetch else "off",
                   max_tokens=4096, device=local, store_layers=store_layers,
                   prefetch_buffers=pf_bufs, compress=compress)
