@@ -1068,24 +1068,29 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       if (g->profiling) MOE_CUDA(cudaEventRecord(pe[2], s));
       FfnParams fp{(c.rms_norm && !g->bf16) ? g->h_norm : hm, trec + l, g->states + l,
                    g->pool + static_cast<long long>(l) * g->NB * g->expert_bytes, g->expert_bytes,
-                   D, g->f, K, 0, g->act, g->y};
+                   D, g->f, K, 0, g->act, g->y, nullptr, nullptr};
       std::array<cudaEvent_t, 2> fev{};
       if (g->sm_transfer) {
-        // device-driven: the SMs fetch the missed experts, then one FFN pass over all K
-        FetchParams fp2{trec + l, g->states + l,
-                        g->store_block_dev(l, 0),
-                        g->pool + static_cast<long long>(l) * g->NB * g->expert_bytes, g->expert_bytes,
-                        K, g->dstats};
-        const long long n16 = g->expert_bytes / 16;
-        const int fgrid = static_cast<int>(std::max(1ll, std::min<long long>(296, (K * n16 + 4095) / 4096)));
-        // (a side-stream fork of the fetch beside the hits' FFN was measured: no gain on the
-        // latency-bound small configs -- the critical path keeps one up/down after the fetch)
-        fetch_kernel<<<fgrid, 512, 0, s>>>(fp2);
-        MOE_LAUNCHED();
+        // device-driven: the SMs fetch the missed experts, then one FFN pass over all K.
+        // Toy (f32) experts fuse the fetch into the FFN: a missed expert's rows are read from
+        // the mapped store and written through to its buffer as they are used.
+        if (!g->bf16) {
+          fp.store = g->store_block_dev(l, 0);
+          fp.stats = g->dstats;
+        } else {
+          FetchParams fp2{trec + l, g->states + l, g->store_block_dev(l, 0),
+                          g->pool + static_cast<long long>(l) * g->NB * g->expert_bytes, g->expert_bytes,
+                          K, g->dstats};
+          const long long n16 = g->expert_bytes / 16;
+          const int fgrid = static_cast<int>(std::max(1ll, std::min<long long>(296, (K * n16 + 4095) / 4096)));
+          fetch_kernel<<<fgrid, 512, 0, s>>>(fp2);
+          MOE_LAUNCHED();
+        }
         fp.phase = 2;
         TRY(prof_begin(fev));
         TRY(launch_ffn(fp, -1));
         TRY(prof_end(fev));
+        fp.store = nullptr;  // the up pass already brought both matrices of a missed toy expert
         TRY(prof_begin(fev));
         TRY(launch_down(fp, -1));
         TRY(prof_end(fev));

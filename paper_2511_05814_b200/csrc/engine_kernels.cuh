@@ -610,6 +610,10 @@ struct FfnParams {
   int phase;                 // 0: experts that hit (resident before), 1: misses, 2: all
   float* act;                // [K][f]
   float* y;                  // [K][d]
+  // fused SM fetch (toy experts, SM transfer): a missed expert's rows are read from the mapped
+  // host store and written through to its HBM buffer while they are used
+  const char* store;         // this layer's host experts (device view), or nullptr
+  DeviceStats* stats;
 };
 
 __device__ __forceinline__ bool ffn_phase_match(const FfnParams& p, int j, int* e_out) {
@@ -696,6 +700,31 @@ static __global__ void __launch_bounds__(256) swiglu_up_kernel(FfnParams p) {
 }
 
 // Toy up projection: act[j][r] = tanh(W1t[r] . x)   (toymoe.py:144)
+// Per-lane partial dot of one f32 row read from `src` (e.g. mapped host memory) that also
+// stores the row to `dst` (the expert's HBM buffer): fetch and use in one pass.
+__device__ __forceinline__ float lane_dot_f32_copy(const float* __restrict__ src, float* __restrict__ dst,
+                                                   int n, const float4* pa, const float4* pb) {
+  const int lane = threadIdx.x & 31;
+  const float4* r = reinterpret_cast<const float4*>(src);
+  float4* w = reinterpret_cast<float4*>(dst);
+  float acc = 0.f;
+  for (int i = lane; i < (n >> 3); i += 32) {
+    const float4 w0 = r[2 * i], w1 = r[2 * i + 1];
+    w[2 * i] = w0;
+    w[2 * i + 1] = w1;
+    const float4 a = pa[i], b = pb[i];
+    acc = fmaf(w0.x, a.x, acc);
+    acc = fmaf(w0.y, a.y, acc);
+    acc = fmaf(w0.z, a.z, acc);
+    acc = fmaf(w0.w, a.w, acc);
+    acc = fmaf(w1.x, b.x, acc);
+    acc = fmaf(w1.y, b.y, acc);
+    acc = fmaf(w1.z, b.z, acc);
+    acc = fmaf(w1.w, b.w, acc);
+  }
+  return acc;
+}
+
 static __global__ void __launch_bounds__(256) toy_up_kernel(FfnParams p) {
   const int j = blockIdx.y;
   int e;
@@ -706,12 +735,38 @@ static __global__ void __launch_bounds__(256) toy_up_kernel(FfnParams p) {
   stage_planes(p.h_mid, p.d, pa, pb);
   __syncthreads();
   const int b = p.state->buf_of[e];
-  const float* w1 = reinterpret_cast<const float*>(p.pool + b * p.expert_bytes);
+  float* w1 = reinterpret_cast<float*>(const_cast<char*>(p.pool) + b * p.expert_bytes);
+  const bool fetch = p.store && !((p.rec->rb >> e) & 1u);
+  const float* src = fetch ? reinterpret_cast<const float*>(p.store + e * p.expert_bytes) : w1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  // a missed expert's W2t row r travels with its W1t row r (both reads in flight together),
+  // so the down projection finds the whole expert in HBM
+  const size_t half = static_cast<size_t>(p.d) * p.d;  // floats per matrix
   for (int r = blockIdx.x * nwarps + warp; r < p.d; r += gridDim.x * nwarps) {
-    const float s = warp_sum(lane_dot_f32(w1 + static_cast<size_t>(r) * p.d, p.d, pa, pb));
+    const size_t o = static_cast<size_t>(r) * p.d;
+    float4 c2[4];
+    const int n4 = p.d / 4;
+    if (fetch)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = lane + 32 * u;
+        if (i < n4) c2[u] = reinterpret_cast<const float4*>(src + half + o)[i];
+      }
+    const float s = warp_sum(fetch ? lane_dot_f32_copy(src + o, w1 + o, p.d, pa, pb)
+                                   : lane_dot_f32(src + o, p.d, pa, pb));
+    if (fetch) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = lane + 32 * u;
+        if (i < n4) reinterpret_cast<float4*>(w1 + half + o)[i] = c2[u];
+      }
+      for (int i = lane + 128; i < n4; i += 32)  // rows wider than 512 floats
+        reinterpret_cast<float4*>(w1 + half + o)[i] = reinterpret_cast<const float4*>(src + half + o)[i];
+    }
     if (lane == 0) p.act[j * p.f + r] = tanhf(s);
   }
+  if (fetch && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(&p.stats->fetched_bytes, static_cast<unsigned long long>(p.expert_bytes));
 }
 
 // Down projection: y[j][c] = W[c] . act[j]; W = w2 (SwiGLU, [d][f]) or W2t (toy, [d][d]).
@@ -732,10 +787,23 @@ __global__ void __launch_bounds__(256) down_kernel(FfnParams p) {
   const char* W = kBF16 ? blk + 2 * static_cast<size_t>(p.f) * p.d * esz
                         : blk + static_cast<size_t>(p.d) * p.d * esz;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const bool fetch = !kBF16 && p.store && !((p.rec->rb >> e) & 1u);
+  const char* src = fetch ? p.store + e * p.expert_bytes + static_cast<size_t>(p.d) * p.d * esz : W;
   for (int c = blockIdx.x * nwarps + warp; c < p.d; c += gridDim.x * nwarps) {
-    const float s = warp_sum(lane_dot<kBF16>(W + static_cast<size_t>(c) * p.f * esz, p.f, pa, pb));
+    float part;
+    if constexpr (!kBF16) {
+      const size_t o = static_cast<size_t>(c) * p.f;
+      part = fetch ? lane_dot_f32_copy(reinterpret_cast<const float*>(src) + o,
+                                       reinterpret_cast<float*>(const_cast<char*>(W)) + o, p.f, pa, pb)
+                   : lane_dot_f32(reinterpret_cast<const float*>(W) + o, p.f, pa, pb);
+    } else {
+      part = lane_dot<kBF16>(W + static_cast<size_t>(c) * p.f * esz, p.f, pa, pb);
+    }
+    const float s = warp_sum(part);
     if (lane == 0) p.y[j * p.d + c] = s;
   }
+  if (fetch && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(&p.stats->fetched_bytes, static_cast<unsigned long long>(p.expert_bytes / 2));
 }
 
 // Final layer: h_out = h' + sum_j p_j y_j
