@@ -331,6 +331,16 @@ def run_reference(args, world, rank, local):
 
 # ---- our engine ------------------------------------------------------------------------
 
+def speculation_precision(rec) -> float:
+    """metrics.speculation_metrics precision (metrics.py:217-249) of the engine's
+    reference-definition guesses (gate l on the output of l-1) over the timed tokens."""
+    g, a = rec["guessed"], rec["acts"][:, 1:, :]
+    if g.size == 0:
+        return None
+    tp = sum(len(set(g[t, l]) & set(a[t, l])) for t in range(g.shape[0]) for l in range(g.shape[1]))
+    return tp / g.size
+
+
 def parse_variant(v: str, default_c: int):
     """'lru' | 'lfu' | 'lfu+prefetch' | 'lfu@6' | 'lfu+prefetch@2' -> (policy, C, prefetch)."""
     from paper_2511_05814_b200.policies import PolicyKind
@@ -485,6 +495,7 @@ def run_ours(args, world, rank, local):
             "prefetch_issued": s1["prefetch_issued"] - s0["prefetch_issued"],
             "prefetch_used": s1["prefetch_used"] - s0["prefetch_used"],
             "prefetch_wasted_bytes": s1["prefetch_wasted_bytes"] - s0["prefetch_wasted_bytes"],
+            "speculation_precision": speculation_precision(rec),
             "check_hits_from_records": int(sum(
                 int(rec["resident_before"][t, l, rec["acts"][t, l]].sum())
                 for t in range(args.steps) for l in range(nl))) == hits,
