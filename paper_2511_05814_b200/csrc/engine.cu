@@ -1060,10 +1060,22 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
                     g->ctl_d, g->err, g->dstats, c.rms_norm, c.rms_eps, g->h_norm,
                     g->gate_phase_ns, g->bf16 ? g->gate_part : nullptr, grid_mix, g->norm_scale,
                     routing_dev ? routing_dev + (static_cast<size_t>(t) * L + l) * K : nullptr};
-      if (c.num_experts <= 8)
-        gate_cache_kernel<8><<<1, kGateThreads, 0, s>>>(gp);
-      else
-        gate_cache_kernel<kMaxE><<<1, kGateThreads, 0, s>>>(gp);
+      {
+        // programmatic launch: the gate's launch and state staging overlap the mixing tail
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(1);
+        lc.blockDim = dim3(kGateThreads);
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = g->no_pdl ? 0 : 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        if (c.num_experts <= 8)
+          MOE_CUDA(cudaLaunchKernelEx(&lc, gate_cache_kernel<8>, gp));
+        else
+          MOE_CUDA(cudaLaunchKernelEx(&lc, gate_cache_kernel<kMaxE>, gp));
+      }
       MOE_LAUNCHED();
       if (g->profiling) MOE_CUDA(cudaEventRecord(pe[2], s));
       FfnParams fp{(c.rms_norm && !g->bf16) ? g->h_norm : hm, trec + l, g->states + l,

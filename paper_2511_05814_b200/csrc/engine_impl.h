@@ -163,6 +163,7 @@ struct moe_engine {
   bool sm_transfer = false;
   // token graph (SM transfer): one token captured once, replayed per token
   bool no_graph = getenv("MOE_NO_GRAPH") != nullptr;
+  bool no_pdl = getenv("MOE_NO_PDL") != nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   uint64_t graph_kernels = 0;
   cudaStream_t cap_stream = nullptr;

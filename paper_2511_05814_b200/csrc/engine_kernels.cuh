@@ -198,6 +198,7 @@ struct MixParams {
 
 template <bool kBF16>
 __global__ void __launch_bounds__(256) mix_kernel(MixParams p) {
+  pdl_trigger();  // the gate may launch and stage its cache state meanwhile
   extern __shared__ float4 smem4[];
   float4* pa = smem4;
   float4* pb = smem4 + p.d / 8;
@@ -324,6 +325,8 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
   copy16(&sS, &p.states[p.layer], sizeof(LayerState), threadIdx.x, blockDim.x);
   if (do_prefetch) copy16(&sS1, &p.states[p.layer + 1], sizeof(LayerState), threadIdx.x, blockDim.x);
   if (threadIdx.x == 0) s_consumed = p.mail ? p.ctl->consumed : 0;
+  // launched programmatically after the mixing kernel: its outputs are read from here on
+  pdl_wait();
   // RMSNorm scales of h' (route, early guess, experts) and of h_in (reference guess)
   float inv_mid = 1.f, inv_in = 1.f;
   const int njob = 3 * p.E + 2;

@@ -88,6 +88,7 @@ __device__ __forceinline__ int stream_active(const StreamParams& p, int* slot, c
 // pairs/quads combine through shared memory in a fixed order).
 template <int MODE, int RPB>
 __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamParams p) {
+  if constexpr (MODE == kModeMix) pdl_trigger();  // the gate may launch meanwhile
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NM = MODE == kModeUp ? 2 : 1;  // matrices streamed per row block
   constexpr int WPR = kStreamWarps / RPB;
