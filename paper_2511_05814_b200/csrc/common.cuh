@@ -18,6 +18,19 @@ std::atomic<uint64_t>& launch_counter();
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Kernel attributes (cudaFuncSetAttribute) are per device: run `f` once per device per call
+// site.  Concurrent first calls may both run it, which is harmless.
+template <class F>
+inline void once_per_device(std::atomic<uint64_t>& done, F f) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    f();
+    done.fetch_or(bit, std::memory_order_release);
+  }
+}
+
 #define MOE_CUDA(expr)                                                            \
   do {                                                                            \
     cudaError_t _e = (expr);                                                      \

@@ -888,8 +888,8 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
   const int down_grid = std::max(1, std::min(D / 8, 148));
   const size_t up_smem = static_cast<size_t>(D) * 4;
   const size_t down_smem = static_cast<size_t>(g->f) * 4;
-  static bool attrs = false;
-  if (!attrs) {
+  static std::atomic<uint64_t> attrs{0};
+  once_per_device(attrs, [] {
     cudaFuncSetAttribute(mix_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(mix_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(swiglu_up_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -915,8 +915,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       cudaFuncSetAttribute(down_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
       set_stream_carveout(mx);
     }
-    attrs = true;
-  }
+  });
   MOE_REQUIRE(mix_smem <= 200 * 1024 && down_smem <= 200 * 1024, "hidden/ffn dims too large");
   // bf16 path: bulk-copy streaming GEMVs (stream_gemv.cuh)
   StreamGeom gmix{}, gup{}, gdown{};

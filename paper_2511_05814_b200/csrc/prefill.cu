@@ -202,11 +202,10 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
   MOE_CUDA(cudaSetDevice(g->device));
   MOE_REQUIRE(pf_plan_smem(static_cast<int>(T64), c.top_k) <= 160 * 1024,
               "prefill of %lld tokens exceeds the plan kernel's staging (split the batch)", (long long)T64);
-  static bool plan_attr = false;
-  if (!plan_attr) {
-    MOE_CUDA(cudaFuncSetAttribute(pf_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    plan_attr = true;
-  }
+  static std::atomic<uint64_t> plan_attr{0};
+  once_per_device(plan_attr, [] {
+    cudaFuncSetAttribute(pf_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  });
   const int T = static_cast<int>(T64);
   const int L = c.num_layers, E = c.num_experts, K = c.top_k, d = g->d, f = g->f;
   cudaStream_t s = as_stream(stream);

@@ -376,13 +376,12 @@ inline void set_stream_carveout(int carveout) {
 template <int MODE>
 inline cudaError_t launch_stream(const StreamGeom& g, int grid, const StreamParams& sp,
                                  cudaStream_t s) {
-  static bool attrs = false;
-  if (!attrs) {
+  static std::atomic<uint64_t> attrs{0};
+  once_per_device(attrs, [] {
     cudaFuncSetAttribute(stream_gemv_kernel<MODE, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(stream_gemv_kernel<MODE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(stream_gemv_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attrs = true;
-  }
+  });
   StreamParams p = sp;
   p.cb = g.cb;
   p.ncb = g.ncb;

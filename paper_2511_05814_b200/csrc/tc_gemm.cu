@@ -50,12 +50,10 @@ moe_status make_tmap_bf16(CUtensorMap* map, const void* base, long long rows, lo
 
 moe_status launch_grouped(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
                           const Params& p, int grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    MOE_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  SMEM_BYTES));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [] {
+    cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  });
   grouped_gemm_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(a, b0, b1, p);
   MOE_LAUNCHED();
   return MOE_OK;
