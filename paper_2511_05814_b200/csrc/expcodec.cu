@@ -13,14 +13,19 @@ namespace xc {
 namespace {
 
 inline int expo(uint16_t w) { return (w >> 7) & 0xFF; }
+inline uint32_t pad8(uint32_t x) { return (x + 7) & ~7u; }
+
+struct ChunkStats {
+  uint8_t base;
+  uint32_t e3, e4, l2, l3;  // escapes of mode 3 / 4; mode 23 level-2 codes and byte escapes
+};
 
 struct Plan {
-  int kbits;
+  int mode;
   uint32_t nch;
-  std::vector<uint8_t> base;
-  std::vector<uint32_t> esc_off;
-  std::vector<uint16_t> n_esc;
-  uint64_t low_off, code_off, esc_off_bytes, total, total_esc;
+  std::vector<ChunkStats> st;
+  std::vector<uint32_t> esc_off, l2_off;
+  uint64_t low_off, code_off, l2_off_b, esc_off_b, total;
 };
 
 template <class F>
@@ -35,162 +40,149 @@ void parallel_chunks(uint32_t nch, F f) {
   for (auto& t : th) t.join();
 }
 
-Plan make_plan(const uint16_t* in, uint64_t n, int kbits_req) {
+Plan make_plan(const uint16_t* in, uint64_t n, int mode_req) {
   Plan p{};
   p.nch = static_cast<uint32_t>((n + kChunk - 1) / kChunk);
-  p.base.assign(p.nch, 0);
-  std::vector<uint32_t> esc3(p.nch, 0), esc4(p.nch, 0);
+  p.st.assign(p.nch, ChunkStats{});
   parallel_chunks(p.nch, [&](uint32_t c) {
     const uint64_t a = static_cast<uint64_t>(c) * kChunk, b = std::min<uint64_t>(n, a + kChunk);
     int mx = 0;
     for (uint64_t i = a; i < b; ++i) mx = std::max(mx, expo(in[i]));
-    uint32_t e3 = 0, e4 = 0;
+    ChunkStats s{static_cast<uint8_t>(mx), 0, 0, 0, 0};
     for (uint64_t i = a; i < b; ++i) {
-      const int dlt = mx - expo(in[i]);
-      e3 += dlt >= 7;
-      e4 += dlt >= 15;
+      const int dl = mx - expo(in[i]);
+      s.e3 += dl >= 7;
+      s.e4 += dl >= 15;
+      s.l2 += dl >= 3;
+      s.l3 += dl >= 10;
     }
-    p.base[c] = static_cast<uint8_t>(mx);
-    esc3[c] = e3;
-    esc4[c] = e4;
+    p.st[c] = s;
   });
-  auto size_for = [&](int k, const std::vector<uint32_t>& esc, uint64_t* tot_esc) {
-    uint64_t t = 0;
-    for (auto e : esc) t += e;
-    *tot_esc = t;
-    return align16(sizeof(PartHeader)) + align16(sizeof(ChunkEntry) * p.nch) + align16(n) +
-           align16((n * k + 7) / 8) + align16(t);
-  };
-  uint64_t t3 = 0, t4 = 0;
-  const uint64_t s3 = size_for(3, esc3, &t3), s4 = size_for(4, esc4, &t4);
-  p.kbits = kbits_req == 3 || kbits_req == 4 ? kbits_req : (s3 <= s4 ? 3 : 4);
-  const std::vector<uint32_t>& esc = p.kbits == 3 ? esc3 : esc4;
-  p.total_esc = p.kbits == 3 ? t3 : t4;
+  uint64_t t3 = 0, t4 = 0, tl2 = 0, tl3 = 0;
+  for (const auto& s : p.st) {
+    t3 += s.e3;
+    t4 += s.e4;
+    tl2 += pad8(s.l2);
+    tl3 += s.l3;
+  }
+  const uint64_t head = align16(sizeof(PartHeader)) + align16(sizeof(ChunkEntry) * p.nch) + align16(n);
+  const uint64_t s3 = head + align16((n * 3 + 7) / 8) + align16(t3);
+  const uint64_t s4 = head + align16((n * 4 + 7) / 8) + align16(t4);
+  const uint64_t s23 = head + align16((n * 2 + 7) / 8) + align16(tl2 * 3 / 8 + 16) + align16(tl3);
+  if (mode_req == 3 || mode_req == 4 || mode_req == kMode23) {
+    p.mode = mode_req;
+  } else {
+    p.mode = s23 <= s3 && s23 <= s4 ? kMode23 : (s3 <= s4 ? 3 : 4);
+  }
   p.esc_off.assign(p.nch, 0);
-  p.n_esc.assign(p.nch, 0);
-  uint32_t run = 0;
+  p.l2_off.assign(p.nch, 0);
+  uint32_t run = 0, run2 = 0;
   for (uint32_t c = 0; c < p.nch; ++c) {
+    const auto& s = p.st[c];
     p.esc_off[c] = run;
-    p.n_esc[c] = static_cast<uint16_t>(esc[c]);
-    run += esc[c];
+    p.l2_off[c] = run2;
+    run += p.mode == 3 ? s.e3 : p.mode == 4 ? s.e4 : s.l3;
+    run2 += p.mode == kMode23 ? pad8(s.l2) : 0;
   }
   p.low_off = align16(sizeof(PartHeader)) + align16(sizeof(ChunkEntry) * p.nch);
   p.code_off = p.low_off + align16(n);
-  p.esc_off_bytes = p.code_off + align16((n * p.kbits + 7) / 8);
-  p.total = p.esc_off_bytes + align16(p.total_esc);
+  const int k1 = p.mode == kMode23 ? 2 : p.mode;
+  p.l2_off_b = p.code_off + align16((n * k1 + 7) / 8);
+  p.esc_off_b = p.l2_off_b + (p.mode == kMode23 ? align16(static_cast<uint64_t>(run2) * 3 / 8 + 16) : 0);
+  p.total = p.esc_off_b + align16(run);
   return p;
+}
+
+// bit-stream writer: `k`-bit value at bit position `bit` (little-endian within bytes)
+inline void put_bits(uint8_t* plane, uint64_t bit, uint32_t v, int k) {
+  uint8_t* q = plane + (bit >> 3);
+  const uint32_t sh = bit & 7;
+  const uint32_t x = v << sh;
+  q[0] |= static_cast<uint8_t>(x);
+  if (sh + k > 8) q[1] |= static_cast<uint8_t>(x >> 8);
 }
 
 }  // namespace
 
-uint64_t encoded_size(const uint16_t* in, uint64_t n, int kbits) { return make_plan(in, n, kbits).total; }
+uint64_t encoded_size(const uint16_t* in, uint64_t n, int mode) { return make_plan(in, n, mode).total; }
 
-uint64_t encode(const uint16_t* in, uint64_t n, int kbits_req, uint8_t* out) {
-  const Plan p = make_plan(in, n, kbits_req);
+uint64_t encode(const uint16_t* in, uint64_t n, int mode_req, uint8_t* out) {
+  const Plan p = make_plan(in, n, mode_req);
   memset(out, 0, p.total);
   PartHeader h{};
   h.magic = kMagic;
-  h.kbits = static_cast<uint32_t>(p.kbits);
+  h.kbits = static_cast<uint32_t>(p.mode);
   h.n = n;
   h.nch = p.nch;
   h.low_off = p.low_off;
   h.code_off = p.code_off;
-  h.esc_off = p.esc_off_bytes;
+  h.l2_off = p.l2_off_b;
+  h.esc_off = p.esc_off_b;
   h.total = p.total;
   memcpy(out, &h, sizeof(h));
   ChunkEntry* ce = reinterpret_cast<ChunkEntry*>(out + align16(sizeof(PartHeader)));
   uint8_t* low = out + p.low_off;
   uint8_t* codes = out + p.code_off;
-  uint8_t* escb = out + p.esc_off_bytes;
-  const int k = p.kbits, lim = (1 << k) - 1;
+  uint8_t* l2 = out + p.l2_off_b;
+  uint8_t* escb = out + p.esc_off_b;
   parallel_chunks(p.nch, [&](uint32_t c) {
-    ce[c] = ChunkEntry{p.esc_off[c], p.base[c], 0, p.n_esc[c]};
+    ChunkEntry e{};
+    e.esc_off = p.esc_off[c];
+    e.l2_off = p.l2_off[c];
+    e.base = p.st[c].base;
+    ce[c] = e;
     const uint64_t a = static_cast<uint64_t>(c) * kChunk, b = std::min<uint64_t>(n, a + kChunk);
-    uint32_t e = p.esc_off[c];
-    // chunks start on whole bytes of the code plane (kChunk * k is a multiple of 8)
+    uint32_t ei = p.esc_off[c];
+    uint64_t l2i = p.l2_off[c];
+    const int base = p.st[c].base;
+    // chunks start on whole bytes of every plane (kChunk * k bits, 24-bit level-2 runs)
     for (uint64_t i = a; i < b; ++i) {
       const uint16_t w = in[i];
       low[i] = static_cast<uint8_t>(((w >> 8) & 0x80) | (w & 0x7F));
-      const int dlt = p.base[c] - expo(w);
-      const uint32_t code = dlt < lim ? static_cast<uint32_t>(dlt + 1) : 0u;
-      if (!code) escb[e++] = static_cast<uint8_t>(expo(w));
-      const uint64_t bit = i * k;
-      uint32_t v = code << (bit & 7);
-      uint8_t* q = codes + (bit >> 3);
-      q[0] |= static_cast<uint8_t>(v);
-      if ((bit & 7) + k > 8) q[1] |= static_cast<uint8_t>(v >> 8);
+      const int dl = base - expo(w);
+      if (p.mode == kMode23) {
+        const uint32_t c1 = dl < 3 ? static_cast<uint32_t>(dl + 1) : 0u;
+        put_bits(codes, i * 2, c1, 2);
+        if (!c1) {
+          const uint32_t c2 = dl < 10 ? static_cast<uint32_t>(dl - 2) : 0u;
+          put_bits(l2, l2i * 3, c2, 3);
+          ++l2i;
+          if (!c2) escb[ei++] = static_cast<uint8_t>(expo(w));
+        }
+      } else {
+        const int lim = (1 << p.mode) - 1;
+        const uint32_t code = dl < lim ? static_cast<uint32_t>(dl + 1) : 0u;
+        put_bits(codes, i * p.mode, code, p.mode);
+        if (!code) escb[ei++] = static_cast<uint8_t>(expo(w));
+      }
     }
   });
   return p.total;
 }
 
-// One CTA per chunk, 32 consecutive weights per thread; escapes ranked by a block scan.
-template <int K>
-__global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restrict__ part,
-                                                          uint16_t* __restrict__ out) {
-  const PartHeader& h = *reinterpret_cast<const PartHeader*>(part);
-  const uint32_t c = blockIdx.x;
-  const ChunkEntry ce = reinterpret_cast<const ChunkEntry*>(part + align16(sizeof(PartHeader)))[c];
-  const uint64_t first = static_cast<uint64_t>(c) * kChunk + threadIdx.x * 32ull;
-  const bool active = first < h.n;
-  const int cnt = active ? static_cast<int>(h.n - first < 32 ? h.n - first : 32) : 0;
-  uint32_t lo[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  // the thread's 32 codes as two 64-bit words: codes 0..15 in c0, 16..31 in c1
-  uint64_t c0 = 0, c1 = 0;
-  int esc_mask_n = 0;
-  uint32_t escm = 0;
-  if (active) {
-    const uint4* lp = reinterpret_cast<const uint4*>(part + h.low_off + first);
-    const uint4 l0 = lp[0], l1 = lp[1];
-    lo[0] = l0.x; lo[1] = l0.y; lo[2] = l0.z; lo[3] = l0.w;
-    lo[4] = l1.x; lo[5] = l1.y; lo[6] = l1.z; lo[7] = l1.w;
-    if constexpr (K == 4) {
-      const uint4 q = *reinterpret_cast<const uint4*>(part + h.code_off + first / 2);
-      c0 = (static_cast<uint64_t>(q.y) << 32) | q.x;
-      c1 = (static_cast<uint64_t>(q.w) << 32) | q.z;
-    } else {
-      const uint32_t* q = reinterpret_cast<const uint32_t*>(part + h.code_off + first * 3 / 8);
-      const uint32_t w0 = q[0], w1 = q[1], w2 = q[2];
-      c0 = (static_cast<uint64_t>(w1) << 32) | w0;                    // stream bits 0..63
-      c1 = (static_cast<uint64_t>(w2) << 16) | (w1 >> 16);            // stream bits 48..95
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const uint32_t code = static_cast<uint32_t>((j < 16 ? c0 >> (K * j) : c1 >> (K * (j - 16))) & ((1u << K) - 1));
-      if (j < cnt && !code) escm |= 1u << j;
-    }
-    esc_mask_n = __popc(escm);
-  }
-  // exclusive scan of escape counts across the CTA (element order)
-  __shared__ int warp_tot[kThreads / 32];
+// CTA-wide exclusive scan of one int per thread (element order = thread order).
+__device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = esc_mask_n;
+  int incl = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
+    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
   }
   if (lane == 31) warp_tot[warp] = incl;
   __syncthreads();
-  int before = incl - esc_mask_n;
+  int before = incl - v;
   for (int w = 0; w < warp; ++w) before += warp_tot[w];
-  if (!active) return;
-  const uint8_t* esc = part + h.esc_off + ce.esc_off + before;
-  uint32_t o[16];
-  int e = 0;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const uint32_t b8 = (lo[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-    const uint32_t code = static_cast<uint32_t>((j < 16 ? c0 >> (K * j) : c1 >> (K * (j - 16))) & ((1u << K) - 1));
-    uint32_t ex = (static_cast<uint32_t>(ce.base) + 1u - code) & 0xFFu;
-    if ((escm >> j) & 1u) {  // rare (~1 % of weights at k = 3): exponent from the side list
-      ex = esc[e];
-      ++e;
-    }
-    const uint32_t w = ((b8 & 0x80u) << 8) | (ex << 7) | (b8 & 0x7Fu);
-    if (j & 1) o[j >> 1] |= w << 16;
-    else o[j >> 1] = w;
-  }
+  __syncthreads();  // warp_tot may be reused by a second scan
+  return before;
+}
+
+__device__ __forceinline__ uint32_t get3(uint64_t lo, uint64_t hi, int p) {
+  const uint64_t v = p >= 64 ? hi >> (p - 64) : (p == 0 ? lo : (lo >> p) | (hi << (64 - p)));
+  return static_cast<uint32_t>(v & 7u);
+}
+
+__device__ __forceinline__ void store_out(uint16_t* out, uint64_t first, int cnt, const uint32_t (&o)[16]) {
   if (cnt == 32) {
     uint4* op = reinterpret_cast<uint4*>(out + first);
     op[0] = make_uint4(o[0], o[1], o[2], o[3]);
@@ -204,13 +196,123 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
   }
 }
 
+__device__ __forceinline__ uint32_t bf16_word(uint32_t b8, uint32_t ex) {
+  return ((b8 & 0x80u) << 8) | ((ex & 0xFFu) << 7) | (b8 & 0x7Fu);
+}
+
+// One CTA per chunk, 32 consecutive weights per thread; escapes ranked by block scans.
+template <int K>
+__global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restrict__ part,
+                                                          uint16_t* __restrict__ out) {
+  __shared__ int warp_tot[kThreads / 32];
+  const PartHeader& h = *reinterpret_cast<const PartHeader*>(part);
+  const uint32_t c = blockIdx.x;
+  const ChunkEntry ce = reinterpret_cast<const ChunkEntry*>(part + align16(sizeof(PartHeader)))[c];
+  const uint64_t first = static_cast<uint64_t>(c) * kChunk + threadIdx.x * 32ull;
+  const bool active = first < h.n;
+  const int cnt = active ? static_cast<int>(h.n - first < 32 ? h.n - first : 32) : 0;
+  uint32_t lo[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint64_t c0 = 0, c1 = 0;  // K-bit codes 0..15 / 16..31 (mode 23: all 32 2-bit codes in c0)
+  uint32_t escm = 0;
+  if (active) {
+    const uint4* lp = reinterpret_cast<const uint4*>(part + h.low_off + first);
+    const uint4 l0 = lp[0], l1 = lp[1];
+    lo[0] = l0.x; lo[1] = l0.y; lo[2] = l0.z; lo[3] = l0.w;
+    lo[4] = l1.x; lo[5] = l1.y; lo[6] = l1.z; lo[7] = l1.w;
+    if constexpr (K == kMode23) {
+      const uint2 q = *reinterpret_cast<const uint2*>(part + h.code_off + first / 4);
+      c0 = (static_cast<uint64_t>(q.y) << 32) | q.x;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < cnt && !((c0 >> (2 * j)) & 3u)) escm |= 1u << j;
+    } else if constexpr (K == 4) {
+      const uint4 q = *reinterpret_cast<const uint4*>(part + h.code_off + first / 2);
+      c0 = (static_cast<uint64_t>(q.y) << 32) | q.x;
+      c1 = (static_cast<uint64_t>(q.w) << 32) | q.z;
+    } else {
+      const uint32_t* q = reinterpret_cast<const uint32_t*>(part + h.code_off + first * 3 / 8);
+      const uint32_t w0 = q[0], w1 = q[1], w2 = q[2];
+      c0 = (static_cast<uint64_t>(w1) << 32) | w0;                    // stream bits 0..63
+      c1 = (static_cast<uint64_t>(w2) << 16) | (w1 >> 16);            // stream bits 48..95
+    }
+    if constexpr (K != kMode23) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t code = static_cast<uint32_t>((j < 16 ? c0 >> (K * j) : c1 >> (K * (j - 16))) & ((1u << K) - 1));
+        if (j < cnt && !code) escm |= 1u << j;
+      }
+    }
+  }
+  const int n1 = __popc(escm);
+  const int before1 = block_exclusive_scan(n1, warp_tot);
+  uint32_t o[16];
+  if constexpr (K == kMode23) {
+    // level-2 codes of this thread: n1 consecutive 3-bit codes from index l2_off + before1
+    const uint64_t bit = (static_cast<uint64_t>(ce.l2_off) + before1) * 3;
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(part + h.l2_off) + (bit >> 5);
+    uint64_t wlo = 0, whi = 0;
+    const int sh = static_cast<int>(bit & 31);
+    if (n1) {
+      wlo = (static_cast<uint64_t>(wp[1]) << 32) | wp[0];
+      whi = (static_cast<uint64_t>(wp[3]) << 32) | wp[2];
+    }
+    int n2 = 0;
+    for (int k = 0; k < n1; ++k) n2 += get3(wlo, whi, sh + 3 * k) == 0u;
+    const int before2 = block_exclusive_scan(n2, warp_tot);
+    if (!active) return;
+    const uint8_t* esc = part + h.esc_off + ce.esc_off + before2;
+    int k = 0, e = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t b8 = (lo[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+      const uint32_t cc = static_cast<uint32_t>((c0 >> (2 * j)) & 3u);
+      uint32_t ex = static_cast<uint32_t>(ce.base) + 1u - cc;
+      if ((escm >> j) & 1u) {
+        const uint32_t c2 = get3(wlo, whi, sh + 3 * k);
+        ++k;
+        if (c2) {
+          ex = static_cast<uint32_t>(ce.base) - 2u - c2;
+        } else {
+          ex = esc[e];
+          ++e;
+        }
+      }
+      const uint32_t w = bf16_word(b8, ex);
+      if (j & 1) o[j >> 1] |= w << 16;
+      else o[j >> 1] = w;
+    }
+  } else {
+    if (!active) return;
+    const uint8_t* esc = part + h.esc_off + ce.esc_off + before1;
+    int e = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t b8 = (lo[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+      const uint32_t code = static_cast<uint32_t>((j < 16 ? c0 >> (K * j) : c1 >> (K * (j - 16))) & ((1u << K) - 1));
+      uint32_t ex = static_cast<uint32_t>(ce.base) + 1u - code;
+      if ((escm >> j) & 1u) {  // rare: exponent from the side list
+        ex = esc[e];
+        ++e;
+      }
+      const uint32_t w = bf16_word(b8, ex);
+      if (j & 1) o[j >> 1] |= w << 16;
+      else o[j >> 1] = w;
+    }
+  }
+  store_out(out, first, cnt, o);
+}
+
 moe_status decode(const void* part_dev, const PartHeader& h, uint16_t* out_dev, cudaStream_t s) {
-  MOE_REQUIRE(h.magic == kMagic && (h.kbits == 3 || h.kbits == 4), "not an exponent-coded part");
+  MOE_REQUIRE(h.magic == kMagic && (h.kbits == 3 || h.kbits == 4 || h.kbits == kMode23),
+              "not an exponent-coded part");
   if (h.n == 0) return MOE_OK;
+  const uint8_t* p = static_cast<const uint8_t*>(part_dev);
   if (h.kbits == 3)
-    decode_kernel<3><<<h.nch, kThreads, 0, s>>>(static_cast<const uint8_t*>(part_dev), out_dev);
+    decode_kernel<3><<<h.nch, kThreads, 0, s>>>(p, out_dev);
+  else if (h.kbits == 4)
+    decode_kernel<4><<<h.nch, kThreads, 0, s>>>(p, out_dev);
   else
-    decode_kernel<4><<<h.nch, kThreads, 0, s>>>(static_cast<const uint8_t*>(part_dev), out_dev);
+    decode_kernel<kMode23><<<h.nch, kThreads, 0, s>>>(p, out_dev);
   MOE_LAUNCHED();
   return MOE_OK;
 }
@@ -225,7 +327,8 @@ extern "C" {
 moe_status moe_xc_encode(const uint16_t* in, uint64_t n, int32_t kbits, void* out, uint64_t cap,
                          uint64_t* size) {
   MOE_REQUIRE(size && (in || n == 0), "null argument");
-  MOE_REQUIRE(kbits == 0 || kbits == 3 || kbits == 4, "kbits must be 0 (auto), 3 or 4");
+  MOE_REQUIRE(kbits == 0 || kbits == 3 || kbits == 4 || kbits == xc::kMode23,
+              "mode must be 0 (auto), 3, 4 or 23");
   if (!out) {
     *size = xc::encoded_size(in, n, kbits);
     return MOE_OK;

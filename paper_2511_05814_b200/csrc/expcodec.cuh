@@ -1,16 +1,18 @@
 // Lossless bf16 expert compression for the PCIe path ("exponent coding", in the spirit of
 // ZipNN / DFloat11): a bf16 word is sign(1) | exponent(8) | mantissa(7).  Weights concentrate
 // their exponents in a few values just below each block's maximum (entropy ~2.1 bits on the
-// synthetic Mixtral weights), so a part is stored as
-//   low plane   1 byte / weight   sign << 7 | mantissa
-//   code plane  k bits / weight   c = base - exponent + 1 in [1, 2^k - 1], 0 = escape
-//   escapes     1 byte / escape   the exponent, in element order within the chunk
-// with base = the chunk's largest exponent, per 4096-weight chunk.  k = 3 or 4, chosen per part
-// (smaller output wins).  1.38 bytes / weight at k = 3 on the synthetic weights (-31 % PCIe
-// bytes); decoding is exact, so everything downstream is bit-identical.
+// synthetic Mixtral weights), so a part is stored as a sign+mantissa byte per weight plus an
+// exponent code relative to the largest exponent of its 4096-weight chunk (dl = base - exp):
+//   mode 3 / 4   k-bit code c = dl + 1 in [1, 2^k - 1]; c = 0 escapes to an exponent byte
+//   mode 23      2-bit code c1 = dl + 1 for dl < 3; c1 = 0 escapes to a 3-bit second-level
+//                code c2 = dl - 2 for dl < 10, whose 0 escapes to an exponent byte
+// The encoder picks the smallest mode per part: 1.305 bytes / weight with mode 23 on the
+// synthetic weights (1.384 with mode 3, 1.5 with 4; raw 2).  Decoding is exact, so everything
+// downstream is bit-identical.
 //
 // Part layout (every section 16-byte aligned):
-//   PartHeader | ChunkEntry[nch] | low[n] | codes[n * k / 8] | escapes[total]
+//   PartHeader | ChunkEntry[nch] | low[n] | codes (k * n bits, or 2 * n bits in mode 23)
+//   | level-2 codes (mode 23: 3 bits each, each chunk's run padded to 8 codes) | escape bytes
 #pragma once
 #include <cstdint>
 
@@ -21,28 +23,30 @@ namespace xc {
 
 constexpr int kChunk = 4096;        // weights per chunk
 constexpr int kThreads = 128;       // decoder CTA: 32 weights per thread
-constexpr uint32_t kMagic = 0x58503331u;  // "XP31"
+constexpr uint32_t kMagic = 0x58503332u;  // "XP32"
+constexpr int kMode23 = 23;
 
 struct __align__(16) PartHeader {
-  uint32_t magic, kbits;
-  uint64_t n;           // weights
-  uint32_t nch;         // chunks
+  uint32_t magic, kbits;  // kbits: 3, 4 or kMode23
+  uint64_t n;             // weights
+  uint32_t nch;           // chunks
   uint32_t pad;
-  uint64_t low_off, code_off, esc_off, total;  // byte offsets from the header; total size
+  uint64_t low_off, code_off, l2_off, esc_off, total;  // byte offsets from the header; size
 };
 
 struct ChunkEntry {
   uint32_t esc_off;     // index of the chunk's first escape byte
+  uint32_t l2_off;      // mode 23: index of the chunk's first level-2 code (multiple of 8)
   uint8_t base;         // largest exponent in the chunk
-  uint8_t pad;
-  uint16_t n_esc;
+  uint8_t pad[7];
 };
 
 inline __host__ __device__ uint64_t align16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
 
-// host: size of / encode n bf16 words into one part (kbits 0 = pick 3 or 4); multi-threaded
-uint64_t encoded_size(const uint16_t* in, uint64_t n, int kbits);
-uint64_t encode(const uint16_t* in, uint64_t n, int kbits, uint8_t* out);
+// host: size of / encode n bf16 words into one part (mode 0 = smallest of 3, 4, 23);
+// multi-threaded over chunks
+uint64_t encoded_size(const uint16_t* in, uint64_t n, int mode);
+uint64_t encode(const uint16_t* in, uint64_t n, int mode, uint8_t* out);
 // device: decode a part (already in HBM) into n bf16 words, on stream s
 moe_status decode(const void* part_dev, const PartHeader& h, uint16_t* out_dev, cudaStream_t s);
 
