@@ -207,4 +207,61 @@ __device__ __forceinline__ bool scalar_policy_step(ScalarCacheState<EM>& st, int
   return ok;
 }
 
+// The same step with the top-k a compile-time constant and the activation ids in registers
+// (the prefill replay software-pipelines the next step's ids behind the current step).
+template <int EM, int KK>
+__device__ __forceinline__ bool scalar_policy_step_k(ScalarCacheState<EM>& st, int E, int C,
+                                                     int policy, double decay_factor,
+                                                     long long decay_period, long long t,
+                                                     const uint32_t (&act)[KK], uint32_t& rb,
+                                                     uint32_t& ev) {
+  if (policy == MOE_P_LFU_AGED && t > 0 && (t % decay_period) == 0) {
+#pragma unroll
+    for (int e = 0; e < EM; ++e) st.freq[e] *= decay_factor;
+  }
+  uint32_t in_act = 0;
+  int n_miss = 0;
+#pragma unroll
+  for (int j = 0; j < KK; ++j) {
+    in_act |= 1u << act[j];
+    n_miss += !((st.resident >> act[j]) & 1u);
+  }
+  rb = st.resident;
+  ev = 0;
+  const int need = __popc(st.resident) + n_miss - C;
+  bool ok = true;
+  for (int r = 0; r < need; ++r) {
+    const uint32_t cand = st.resident & ~in_act;
+    if (!cand) {
+      ok = false;
+      break;
+    }
+    int best = -1;
+    uint64_t bf = ~0ull, bl = ~0ull;
+#pragma unroll
+    for (int e = 0; e < EM; ++e) {
+      if (e >= E || !((cand >> e) & 1u)) continue;
+      const uint64_t lk = static_cast<uint64_t>(st.last_touch[e] + kTouchBias);
+      const uint64_t fk = (policy == MOE_P_LFU || policy == MOE_P_LFU_AGED)
+                              ? static_cast<uint64_t>(__double_as_longlong(st.freq[e]))
+                              : 0ull;
+      if (fk < bf || (fk == bf && lk < bl)) {
+        bf = fk;
+        bl = lk;
+        best = e;
+      }
+    }
+    st.resident &= ~(1u << best);
+    ev |= 1u << best;
+  }
+#pragma unroll
+  for (int e = 0; e < EM; ++e)
+    if ((in_act >> e) & 1u) {
+      st.freq[e] += 1.0;
+      st.last_touch[e] = t;
+    }
+  st.resident |= in_act;
+  return ok;
+}
+
 }  // namespace moe

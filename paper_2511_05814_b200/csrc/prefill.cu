@@ -356,24 +356,31 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
       MOE_CUDA(cudaEventRecord(tev.first, g->copy_stream));
     }
     std::vector<char*> dest(m.n_loads);
+    const int nslots = g->cstore ? static_cast<int>(g->cstage_free.size()) : 0;
+    // exponent-coded load i lands in slot i % nslots once that slot's previous part is decoded:
+    // issued here for the first nslots loads, later right after the decode that frees the slot
+    // (a stream wait captures the event's latest record at the time of the call)
+    auto issue_coded = [&](int i) -> moe_status {
+      const int e = m.load_expert[i], slot = i % nslots;
+      const auto& pa = g->ctab[(static_cast<size_t>(l % g->SL) * E + e) * 2];
+      const auto& pb = g->ctab[(static_cast<size_t>(l % g->SL) * E + e) * 2 + 1];
+      char* land = g->cstage + static_cast<long long>(slot) * g->expert_bytes;
+      MOE_CUDA(cudaStreamWaitEvent(g->copy_stream, g->cstage_free[slot], 0));
+      MOE_CUDA(cudaMemcpyAsync(land, g->cstore + pa.off, pa.size, cudaMemcpyHostToDevice, g->copy_stream));
+      MOE_CUDA(cudaEventRecord(pf->ev[2 * i], g->copy_stream));
+      MOE_CUDA(cudaMemcpyAsync(land + pa.size, g->cstore + pb.off, pb.size, cudaMemcpyHostToDevice,
+                               g->copy_stream));
+      MOE_CUDA(cudaEventRecord(pf->ev[2 * i + 1], g->copy_stream));
+      loaded += static_cast<long long>(pa.size + pb.size);
+      return MOE_OK;
+    };
     for (int i = 0; i < m.n_loads; ++i) {
       const int e = m.load_expert[i], dst = m.load_dst[i];
       char* to = dst >= 0 ? g->pool + (static_cast<long long>(l) * g->NB + dst) * g->expert_bytes
                           : pf->scratch + static_cast<long long>(-1 - dst) * g->expert_bytes;
       dest[i] = to;
       if (g->cstore) {
-        // exponent-coded: land in slot i % K (after that slot's previous decode), decode later
-        const int slot = i % static_cast<int>(g->cstage_free.size());
-        const auto& pa = g->ctab[(static_cast<size_t>(l % g->SL) * E + e) * 2];
-        const auto& pb = g->ctab[(static_cast<size_t>(l % g->SL) * E + e) * 2 + 1];
-        char* land = g->cstage + static_cast<long long>(slot) * g->expert_bytes;
-        MOE_CUDA(cudaStreamWaitEvent(g->copy_stream, g->cstage_free[slot], 0));
-        MOE_CUDA(cudaMemcpyAsync(land, g->cstore + pa.off, pa.size, cudaMemcpyHostToDevice, g->copy_stream));
-        MOE_CUDA(cudaEventRecord(pf->ev[2 * i], g->copy_stream));
-        MOE_CUDA(cudaMemcpyAsync(land + pa.size, g->cstore + pb.off, pb.size, cudaMemcpyHostToDevice,
-                                 g->copy_stream));
-        MOE_CUDA(cudaEventRecord(pf->ev[2 * i + 1], g->copy_stream));
-        loaded += static_cast<long long>(pa.size + pb.size);
+        if (i < nslots) TRY(issue_coded(i));
         continue;
       }
       const char* from = g->store_block(l, e);
@@ -383,11 +390,6 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
                                g->copy_stream));
       MOE_CUDA(cudaEventRecord(pf->ev[2 * i + 1], g->copy_stream));
       loaded += g->expert_bytes;
-    }
-    if (m.n_loads > 0) {
-      MOE_CUDA(cudaEventRecord(tev.second, g->copy_stream));
-      std::lock_guard<std::mutex> lk(g->stats_mu);
-      g->busy_events.push_back(tev);
     }
     g->ctl_h->consumed = seq + 1;
     // ---- expert FFN: resident experts now, each loaded expert after its copies ----
@@ -437,8 +439,14 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
       if (pa) {
         TRY(xc::decode(land + pa->size, pa[1].hdr, reinterpret_cast<uint16_t*>(dest[i] + split), s));
         MOE_CUDA(cudaEventRecord(g->cstage_free[slot], s));
+        if (i + nslots < m.n_loads) TRY(issue_coded(i + nslots));
       }
       TRY(ffn_down(1 + i, m.load_rows[i], 1));
+    }
+    if (m.n_loads > 0) {
+      MOE_CUDA(cudaEventRecord(tev.second, g->copy_stream));
+      std::lock_guard<std::mutex> lk(g->stats_mu);
+      g->busy_events.push_back(tev);
     }
     // experts that stay cached but were loaded into scratch move into their cache buffer
     for (int i = 0; i < m.n_moves; ++i) {

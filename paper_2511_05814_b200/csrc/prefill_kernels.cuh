@@ -279,7 +279,6 @@ __device__ __noinline__ void pf_replay(const PfPlanParams& p, LayerState& S, uin
         ++done;
         for (int j = 0; j < K; ++j) hits += (rb >> acts[j]) & 1u;
         needed |= amask;
-        for (int j = 0; j < K; ++j) cnt[acts[j]] += 1;
       }
       RT = st.resident & emask;
 #pragma unroll
@@ -292,6 +291,72 @@ __device__ __noinline__ void pf_replay(const PfPlanParams& p, LayerState& S, uin
       atomicAdd(&p.stats->hits, hits);
       atomicAdd(&p.stats->misses, done * K - hits);
     }
+}
+
+// pf_replay for a compile-time top-k: the next step's ids and flag are loaded while the current
+// step is decided (a single thread's replay is a dependency chain; shared-memory loads off it).
+template <int EM, int KK>
+__device__ __noinline__ void pf_replay_k(const PfPlanParams& p, LayerState& S, uint32_t R0,
+                                         uint32_t emask, uint8_t* s_flags, const uint8_t* s_acts,
+                                         uint32_t* s_rb, uint32_t* s_ev, uint32_t& RT,
+                                         uint32_t& needed) {
+  const int T = p.T;
+  ScalarCacheState<EM> st;
+  st.resident = R0;
+#pragma unroll
+  for (int e = 0; e < EM; ++e) {
+    st.freq[e] = e < p.E ? S.freq[e] : 0.0;
+    st.last_touch[e] = e < p.E ? S.last_touch[e] : -1;
+  }
+  long long step = S.step;
+  unsigned long long hits = 0, done = 0;
+  uint32_t cur[KK], nxt[KK];
+  uint32_t fcur = T > 0 ? s_flags[0] : 0, fnxt = 0;
+#pragma unroll
+  for (int j = 0; j < KK; ++j) cur[j] = T > 0 ? s_acts[j] : 0;
+  for (int t = 0; t < T; ++t) {
+    if (t + 1 < T) {
+      fnxt = s_flags[t + 1];
+#pragma unroll
+      for (int j = 0; j < KK; ++j) nxt[j] = s_acts[(t + 1) * KK + j];
+    }
+    if (fcur) {
+      s_rb[t] = s_ev[t] = 0;
+    } else {
+      const uint32_t res_save = st.resident;
+      uint32_t rb = 0, ev = 0;
+      const bool ok = scalar_policy_step_k<EM, KK>(st, p.E, p.C, p.policy, p.decay_factor,
+                                                   p.decay_period, step, cur, rb, ev);
+      s_rb[t] = rb & emask;
+      s_ev[t] = ev & emask;
+      if (!ok) {
+        s_flags[t] |= 2u;
+        atomicOr(p.err, 2);
+        st.resident = res_save;
+      } else {
+        ++step;
+        ++done;
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+          hits += (rb >> cur[j]) & 1u;
+          needed |= 1u << cur[j];
+        }
+      }
+    }
+    fcur = fnxt;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) cur[j] = nxt[j];
+  }
+  RT = st.resident & emask;
+#pragma unroll
+  for (int e = 0; e < EM; ++e)
+    if (e < p.E) {
+      S.freq[e] = st.freq[e];
+      S.last_touch[e] = st.last_touch[e];
+    }
+  S.step = step;
+  atomicAdd(&p.stats->hits, hits);
+  atomicAdd(&p.stats->misses, done * KK - hits);
 }
 
 __global__ void __launch_bounds__(256) pf_plan_kernel(PfPlanParams p) {
@@ -321,24 +386,41 @@ __global__ void __launch_bounds__(256) pf_plan_kernel(PfPlanParams p) {
   __syncthreads();
   const uint32_t emask = p.E >= 32 ? 0xffffffffu : ((1u << p.E) - 1u);
   const uint32_t R0 = S.resident & emask;
+  __shared__ uint32_t s_RT;
+  // sequential replay by one thread, experts in registers (scalar_policy_step == the warp
+  // step decode uses, without its shuffle latency)
+  if (tid == 0) {
+    uint32_t RT = 0, needed = 0;
+    if (p.E <= 8 && K == 2)
+      pf_replay_k<8, 2>(p, S, R0, emask, s_flags, s_acts, s_rb, s_ev, RT, needed);
+    else if (p.E <= 8)
+      pf_replay<8>(p, S, R0, emask, s_flags, s_acts, s_rb, s_ev, cnt, RT, needed);
+    else
+      pf_replay<kMaxE>(p, S, R0, emask, s_flags, s_acts, s_rb, s_ev, cnt, RT, needed);
+    s_RT = RT;
+    s_needed = needed;
+  }
+  __syncthreads();
+  // token rows per expert (tokens whose gate and policy step succeeded), one warp per expert
+  for (int e = warp; e < p.E; e += nwarps) {
+    int n = 0;
+    for (int t0 = 0; t0 < T; t0 += 32) {
+      const int t = t0 + lane;
+      bool hit = false;
+      if (t < T && !s_flags[t])
+        for (int j = 0; j < K; ++j) hit |= s_acts[t * K + j] == e;
+      n += __popc(__ballot_sync(FULL, hit));
+    }
+    if (lane == 0) cnt[e] = n;
+  }
+  __syncthreads();
   if (warp == 0) {
     const bool valid = lane < p.E;
-    // sequential replay by one thread, experts in registers (scalar_policy_step == the warp
-    // step decode uses, without its shuffle latency)
-    uint32_t RT = 0, needed = 0;
-    if (lane == 0) {
-      if (p.E <= 8)
-        pf_replay<8>(p, S, R0, emask, s_flags, s_acts, s_rb, s_ev, cnt, RT, needed);
-      else
-        pf_replay<kMaxE>(p, S, R0, emask, s_flags, s_acts, s_rb, s_ev, cnt, RT, needed);
-    }
-    RT = __shfl_sync(FULL, RT, 0);
-    needed = __shfl_sync(FULL, needed, 0);
+    const uint32_t RT = s_RT, needed = s_needed;
     if (valid) buf_before[lane] = S.buf_of[lane];
     __syncwarp();
     if (lane == 0) {
       S.resident = RT;
-      s_needed = needed;
       // group (list) order: experts already resident first, then the loads in ascending id
       int ng = 0, rows = 0;
       for (int e = 0; e < p.E; ++e)
