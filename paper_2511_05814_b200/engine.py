@@ -280,16 +280,35 @@ class OffloadEngine:
         self.tokens_done += T
         return h_out
 
-    def prefill(self, h_in, routing=None) -> np.ndarray:
-        """Public prefill: host (T, d) array in, host (T, d) float32 out (copies included)."""
+    def _host_io(self, h_in):
+        """Stage a host (T, d) array in reusable pinned buffers: returns (device input, pinned
+        output view).  Pinned once and grown on demand, so a call's copies are plain DMA."""
         import torch
 
-        x = torch.as_tensor(np.ascontiguousarray(h_in, dtype=np.float32))
-        x = x.pin_memory().to(self._dev, non_blocking=True)
-        y = self.prefill_device(x, routing=routing)
-        out = y.cpu().numpy()
-        self.sync()
-        return out
+        a = np.ascontiguousarray(h_in, dtype=np.float32)
+        T, d = a.shape
+        if getattr(self, "_pin_rows", 0) < T:
+            rows = max(T, 16)
+            self._pin_in = torch.empty((rows, d), dtype=torch.float32, pin_memory=True)
+            self._pin_out = torch.empty((rows, d), dtype=torch.float32, pin_memory=True)
+            self._dev_in = torch.empty((rows, d), dtype=torch.float32, device=self._dev)
+            self._dev_out = torch.empty((rows, d), dtype=torch.float32, device=self._dev)
+            self._pin_rows = rows
+        self._pin_in[:T].numpy()[:] = a
+        x = self._dev_in[:T]
+        x.copy_(self._pin_in[:T], non_blocking=True)
+        return x, self._dev_out[:T], self._pin_out[:T]
+
+    def _run_host(self, fn, h_in, routing) -> np.ndarray:
+        x, y, out = self._host_io(h_in)
+        fn(x, h_out=y, routing=routing)
+        out.copy_(y, non_blocking=True)
+        self.sync()  # synchronises the device (and reports non-finite gates)
+        return out.numpy().copy()
+
+    def prefill(self, h_in, routing=None) -> np.ndarray:
+        """Public prefill: host (T, d) array in, host (T, d) float32 out (copies included)."""
+        return self._run_host(self.prefill_device, h_in, routing)
 
     def set_mode(self, policy: Optional[PolicyKind] = None, cache_size: Optional[int] = None,
                  prefetch: Optional[str] = None) -> None:
@@ -322,12 +341,7 @@ class OffloadEngine:
         routing: optional (T, L, K) activation trace (trace-driven mode)."""
         import torch
 
-        x = torch.as_tensor(np.ascontiguousarray(h_in, dtype=np.float32))
-        x = x.pin_memory().to(self._dev, non_blocking=True)
-        y = self.decode_device(x, routing=routing)
-        out = y.cpu().numpy()
-        self.sync()
-        return out
+        return self._run_host(self.decode_device, h_in, routing)
 
     # -- records / stats --
     def records(self, t0: int, T: int) -> dict:
