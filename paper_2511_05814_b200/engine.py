@@ -300,6 +300,11 @@ class OffloadEngine:
         return x, self._dev_out[:T], self._pin_out[:T]
 
     def _run_host(self, fn, h_in, routing) -> np.ndarray:
+        a = np.asarray(h_in)
+        if a.ndim == 2 and a.shape[0] == 0:
+            if a.shape[1] != self.config.hidden_dim:
+                raise ConfigError(f"h_in must be (T, {self.config.hidden_dim})")
+            return np.zeros((0, self.config.hidden_dim), np.float32)
         x, y, out = self._host_io(h_in)
         fn(x, h_out=y, routing=routing)
         out.copy_(y, non_blocking=True)

@@ -206,3 +206,19 @@ def test_prefill_compressed_loads_bit_exact():
     for k in ("acts", "resident_before", "evicted", "probs"):
         assert np.array_equal(ra[k], rb[k]), k
     assert sb["prefill_bytes"] < 0.75 * sa["prefill_bytes"]
+
+
+def test_prefill_single_token_and_nonfinite():
+    cfg = small_cfg(cache_size=2)
+    X = oracle.MixtralRef.inputs(9, 4, cfg.hidden_dim)
+    with OffloadEngine(cfg) as eng:
+        eng.init_random(9)
+        out1 = eng.prefill(X[:1])
+        rec = eng.records(0, 1)
+        bad = X[1:].copy()
+        bad[1, 0] = np.nan
+        with pytest.raises(FloatingPointError):
+            eng.prefill(bad)
+    ref_out, ref_acts = ref_for(cfg, 9).decode(X[:1])
+    assert np.array_equal(rec["acts"], ref_acts)
+    assert np.abs(out1 - ref_out).max() / np.abs(ref_out).max() < 1e-2
