@@ -582,9 +582,12 @@ def run_ours(args, world, rank, local):
             "achieved_incl_empty_phase_launches": ffn_all_gbs,
             "achieved_in_kernel": (ktimes["ffn_active_bytes"] / (ktimes["ffn_kernel_ms"] / 1e3) / 1e9
                                    if ktimes.get("ffn_kernel_ms") else None),
-            "in_kernel_note": "globaltimer span first CTA start -> last CTA end per launch; the "
-                              "CUDA-event span adds launch / front-end latency (~20 us per launch "
-                              "live, with the copy engine busy)",
+            "in_kernel_note": "globaltimer span first CTA start -> last CTA end per launch. The "
+                              "CUDA-event span of a single launch is inflated while the copy "
+                              "engine runs: tools/dma_event_probe.py times a 235 MB D2D copy "
+                              "kernel at 80 us with or without H2D traffic under one event pair "
+                              "over 20 launches, but at 105 us with an event pair per launch "
+                              "under H2D traffic (80 us without)",
             "traffic": traffic.get("dram_bytes_per_expert") if traffic else None,
             "traffic_unit": "DRAM bytes per expert (ncu, profiles/ncu_ffn_traffic.json)",
             "algorithmic_bytes_per_expert": EB,
