@@ -612,6 +612,9 @@ def run_ours(args, world, rank, local):
             rec["tensor_frac"] = rec["tflops"] / tf_peak
             rec["hbm_frac"] = rec["algorithmic_GBps"] / hbm_peak
             rec["bound"] = "tensor" if rec["tensor_frac"] >= rec["hbm_frac"] else "hbm"
+            if rec.get("in_kernel_GBps"):
+                rec["in_kernel_hbm_frac"] = rec["in_kernel_GBps"] / hbm_peak
+                rec["in_kernel_tensor_frac"] = rec["in_kernel_tflops"] / tf_peak
             rec["peaks"] = {"bf16_tflops": tf_peak, "hbm_gbs": hbm_peak,
                             "source": peaks.get("source", "MEASURED_PEAKS.json")}
         prefill["gemm_isolated"] = gemm_iso
@@ -762,6 +765,11 @@ def run_prefill(args, eng, inputs, base, stream, world, pcie_peak):
                  "launches": k["gemm_launches"], "ms": k["gemm_ms"],
                  "tflops": k["gemm_flops"] / (k["gemm_ms"] / 1e3) / 1e12 if k["gemm_ms"] else None,
                  "algorithmic_GBps": k["gemm_bytes"] / (k["gemm_ms"] / 1e3) / 1e9 if k["gemm_ms"] else None,
+                 "in_kernel_ms": k["gemm_kernel_ms"],
+                 "in_kernel_GBps": (k["gemm_bytes"] / (k["gemm_kernel_ms"] / 1e3) / 1e9
+                                    if k["gemm_kernel_ms"] else None),
+                 "in_kernel_tflops": (k["gemm_flops"] / (k["gemm_kernel_ms"] / 1e3) / 1e12
+                                      if k["gemm_kernel_ms"] else None),
                  "share_of_prefill": k["gemm_ms"] / ms_p},
     }
     if not args.no_cpu_baseline and world == 1:

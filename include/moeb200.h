@@ -237,6 +237,7 @@ typedef struct {
   double ffn_kernel_ms;     /* in-kernel span (globaltimer, first CTA start -> last CTA end) of
                                the FFN launches that processed >= 1 expert: excludes launch
                                latency and the host-side gaps the events see */
+  double gemm_kernel_ms;    /* the same in-kernel span summed over the prefill GEMM launches */
 } moe_kernel_times;
 moe_status moe_engine_profile(moe_engine* eng, int32_t enable);
 /* Resolves outstanding events (synchronises) and returns the running totals. */

@@ -243,18 +243,30 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
     cudaEvent_t a, b;
     double flops;
     long long bytes;
+    int slot;  // in-kernel span slot (prof buffer), -1 none
   };
+  long long* gprof = nullptr;  // [launches][2] in-kernel spans (profiling only)
+  constexpr int kMaxGemmProf = 4096;
+  if (g->profiling) {
+    MOE_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gprof), sizeof(long long) * 2 * kMaxGemmProf, s));
+    MOE_CUDA(cudaMemsetAsync(gprof, 0, sizeof(long long) * 2 * kMaxGemmProf, s));
+  }
   std::vector<GemmEv> gev;
   cudaEvent_t pf_begin = nullptr, pf_end = nullptr;
   auto gemm = [&](const CUtensorMap& ma, const CUtensorMap& mb0, const CUtensorMap& mb1,
                   const tc::Params& p, double flops, long long bytes) -> moe_status {
-    GemmEv e{nullptr, nullptr, flops, bytes};
+    GemmEv e{nullptr, nullptr, flops, bytes, -1};
+    tc::Params pp = p;
+    if (g->profiling && gev.size() < static_cast<size_t>(kMaxGemmProf)) {
+      e.slot = static_cast<int>(gev.size());
+      pp.prof = gprof + 2 * e.slot;
+    }
     if (g->profiling) {
       MOE_CUDA(cudaEventCreate(&e.a));
       MOE_CUDA(cudaEventCreate(&e.b));
       MOE_CUDA(cudaEventRecord(e.a, s));
     }
-    TRY(tc::launch_grouped(ma, mb0, mb1, p, grid, s));
+    TRY(tc::launch_grouped(ma, mb0, mb1, pp, grid, s));
     if (g->profiling) {
       MOE_CUDA(cudaEventRecord(e.b, s));
       gev.push_back(e);
@@ -467,7 +479,14 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
     MOE_CUDA(cudaEventRecord(pf_end, s));
     MOE_CUDA(cudaEventSynchronize(pf_end));
     moe_kernel_times& k = g->ktimes;
+    std::vector<long long> spans(2 * kMaxGemmProf, 0);
+    MOE_CUDA(cudaMemcpy(spans.data(), gprof, sizeof(long long) * spans.size(), cudaMemcpyDeviceToHost));
+    cudaFree(gprof);
     for (auto& e : gev) {
+      if (e.slot >= 0) {
+        const long long t0 = 0x7fffffffffffffffll - spans[2 * e.slot], t1 = spans[2 * e.slot + 1];
+        if (spans[2 * e.slot] > 0 && t1 > t0) k.gemm_kernel_ms += (t1 - t0) / 1e6;
+      }
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e.a, e.b);
       k.gemm_ms += ms;

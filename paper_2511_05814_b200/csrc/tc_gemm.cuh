@@ -70,6 +70,8 @@ struct Params {
   // the consumer sums the planes in split order (deterministic, no atomics)
   int splits;
   long long split_stride;
+  // optional profiling slot [2]: max(LLONG_MAX - CTA start ns), max(CTA end ns) (globaltimer)
+  long long* prof;
 };
 
 __device__ __forceinline__ float silu_mul(float a1, float a3) {
@@ -94,6 +96,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ uint32_t tmem_base_s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.prof && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&p.prof[0], 0x7fffffffffffffffll - static_cast<long long>(t));
+  }
   const int nbase = *p.n_tiles;
   const int splits = p.splits > 1 ? p.splits : 1;
   const int ntiles = nbase * splits;
@@ -267,6 +274,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem_base);
+  if (p.prof && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&p.prof[1], static_cast<long long>(t));
+  }
 }
 #endif  // MOE_TC_GEMM_KERNEL
 
