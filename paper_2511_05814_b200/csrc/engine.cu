@@ -71,11 +71,42 @@ struct DemandPlan {
   cudaEvent_t ev_a[kMaxK], ev_b[kMaxK];
   // compressed transfer of miss k: decode the landing slot into the expert's buffer
   bool comp[kMaxK] = {};
-  const char* land[kMaxK] = {};      // where the coded parts landed (A then B)
+  cudaEvent_t ev_part[kMaxK][moe_engine::kCodedParts] = {};  // coded: after part p landed
+  const char* land[kMaxK] = {};      // where the coded parts landed (contiguous, in order)
   cudaEvent_t free_ev[kMaxK] = {};   // recorded once decoded: the landing area may be reused
   char* dst[kMaxK] = {};
-  const moe_engine::CPart* part[kMaxK][2] = {};
+  const moe_engine::CPart* part[kMaxK] = {};  // the expert's first coded part
 };
+
+cudaEvent_t next_order_event(moe_engine* g);
+
+// Copy the coded bytes [from, total) of (layer, expert) to `land` on the copy stream with an
+// event after each part boundary (ev[p] fires once part p has fully landed).
+moe_status copy_coded(moe_engine* g, int layer, int expert, char* land, long long from,
+                      cudaEvent_t* ev, long long* link) {
+  const moe_engine::CPart* cp = g->coded_parts(layer, expert);
+  long long end = 0;
+  for (int p = 0; p < moe_engine::kCodedParts; ++p) {
+    const long long a = end;
+    end += static_cast<long long>(cp[p].size);
+    const long long lo = std::max(from, a);
+    if (lo < end) {
+      MOE_CUDA(cudaMemcpyAsync(land + lo, g->cstore + cp[0].off + lo, end - lo, cudaMemcpyHostToDevice,
+                               g->copy_stream));
+      *link += end - lo;
+    }
+    ev[p] = next_order_event(g);
+    MOE_CUDA(cudaEventRecord(ev[p], g->copy_stream));
+  }
+  return MOE_OK;
+}
+
+long long coded_total(const moe_engine* g, int layer, int expert) {
+  const moe_engine::CPart* cp = g->coded_parts(layer, expert);
+  long long t = 0;
+  for (int p = 0; p < moe_engine::kCodedParts; ++p) t += static_cast<long long>(cp[p].size);
+  return t;
+}
 
 long long part_a_bytes(const moe_engine* g) {
   return g->bf16 ? 2ll * g->f * g->dpad * 2 : static_cast<long long>(g->dpad) * g->dpad * 4;
@@ -127,59 +158,28 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
       g->st.prefetch_used += 1;
     }
     plan->comp[k] = false;
-    if (zone >= 0) {
-      // adopted compressed prefetch: finish the coded bytes in its zone, decode like a demand
-      const auto& pa = g->ctab[(static_cast<size_t>(m.layer % g->SL) * g->cfg.num_experts + e) * 2];
-      const auto& pb = g->ctab[(static_cast<size_t>(m.layer % g->SL) * g->cfg.num_experts + e) * 2 + 1];
-      char* land = g->pzone + static_cast<long long>(zone) * g->pzone_bytes;
-      const long long sa = static_cast<long long>(pa.size), tot = sa + static_cast<long long>(pb.size);
-      if (from < sa) {
-        MOE_CUDA(cudaMemcpyAsync(land + from, g->cstore + pa.off + from, sa - from, cudaMemcpyHostToDevice,
-                                 g->copy_stream));
-        link += sa - from;
+    if (zone >= 0 || (g->cstore && from == 0)) {
+      // exponent-coded: an adopted prefetch finishes the coded bytes in its zone, a fresh miss
+      // lands in slot k (after that slot's previous decode); the compute stream decodes each
+      // part into the expert's buffer as it lands
+      char* land;
+      if (zone >= 0) {
+        land = g->pzone + static_cast<long long>(zone) * g->pzone_bytes;
+        plan->free_ev[k] = g->pzone_free[zone];
+      } else {
+        land = g->cstage + static_cast<long long>(k) * g->expert_bytes;
+        plan->free_ev[k] = g->cstage_free[k];
+        MOE_CUDA(cudaStreamWaitEvent(g->copy_stream, g->cstage_free[k], 0));
       }
-      plan->ev_a[k] = next_order_event(g);
-      MOE_CUDA(cudaEventRecord(plan->ev_a[k], g->copy_stream));
-      const long long fb = std::max(from, sa);
-      if (fb < tot) {
-        MOE_CUDA(cudaMemcpyAsync(land + fb, g->cstore + pa.off + fb, tot - fb, cudaMemcpyHostToDevice,
-                                 g->copy_stream));
-        link += tot - fb;
-      }
-      plan->ev_b[k] = next_order_event(g);
-      MOE_CUDA(cudaEventRecord(plan->ev_b[k], g->copy_stream));
+      const long long tot = coded_total(g, m.layer, e);
+      TRY(copy_coded(g, m.layer, e, land, from, plan->ev_part[k], &link));
+      plan->ev_a[k] = plan->ev_part[k][0];
+      plan->ev_b[k] = plan->ev_part[k][moe_engine::kCodedParts - 1];
       plan->comp[k] = true;
       plan->land[k] = land;
-      plan->free_ev[k] = g->pzone_free[zone];
       plan->dst[k] = g->pool + (static_cast<long long>(m.layer) * g->NB + b) * g->expert_bytes;
-      plan->part[k][0] = &pa;
-      plan->part[k][1] = &pb;
+      plan->part[k] = g->coded_parts(m.layer, e);
       demand += g->expert_bytes - static_cast<long long>(static_cast<double>(from) / tot * g->expert_bytes);
-      continue;
-    }
-    if (g->cstore && from == 0) {
-      // exponent-coded: both parts land in slot k, the compute stream decodes them into the
-      // expert's buffer (the slot's previous decode must have finished first)
-      const int slot = k;
-      const auto& pa = g->ctab[(static_cast<size_t>(m.layer % g->SL) * g->cfg.num_experts + e) * 2];
-      const auto& pb = g->ctab[(static_cast<size_t>(m.layer % g->SL) * g->cfg.num_experts + e) * 2 + 1];
-      char* land = g->cstage + static_cast<long long>(slot) * g->expert_bytes;
-      MOE_CUDA(cudaStreamWaitEvent(g->copy_stream, g->cstage_free[slot], 0));
-      MOE_CUDA(cudaMemcpyAsync(land, g->cstore + pa.off, pa.size, cudaMemcpyHostToDevice, g->copy_stream));
-      plan->ev_a[k] = next_order_event(g);
-      MOE_CUDA(cudaEventRecord(plan->ev_a[k], g->copy_stream));
-      MOE_CUDA(cudaMemcpyAsync(land + pa.size, g->cstore + pb.off, pb.size, cudaMemcpyHostToDevice,
-                               g->copy_stream));
-      plan->ev_b[k] = next_order_event(g);
-      MOE_CUDA(cudaEventRecord(plan->ev_b[k], g->copy_stream));
-      plan->comp[k] = true;
-      plan->land[k] = land;
-      plan->free_ev[k] = g->cstage_free[slot];
-      plan->dst[k] = g->pool + (static_cast<long long>(m.layer) * g->NB + b) * g->expert_bytes;
-      plan->part[k][0] = &pa;
-      plan->part[k][1] = &pb;
-      demand += g->expert_bytes;
-      link += static_cast<long long>(pa.size + pb.size);
       continue;
     }
     // part A: [from, split), then event; part B: [max(from, split), end), then event
@@ -204,10 +204,9 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
     PrefetchJob j{m.layer + 1, m.prefetch_buf[i], m.prefetch_expert[i], 0, nchunks, false, false};
     j.bytes = g->expert_bytes;
     if (g->pzone) {
-      const size_t ci = (static_cast<size_t>((m.layer + 1) % g->SL) * g->cfg.num_experts + j.expert) * 2;
       j.zone = g->pzone_next;
       g->pzone_next = (g->pzone_next + 1) % static_cast<int>(g->pzone_free.size());
-      j.bytes = static_cast<long long>(g->ctab[ci].size + g->ctab[ci + 1].size);
+      j.bytes = coded_total(g, m.layer + 1, j.expert);
       j.n_chunks = (j.bytes + chunk - 1) / chunk;
     }
     g->jobs.push_back(j);
@@ -259,10 +258,10 @@ moe_status pump_prefetch(moe_engine* g, bool* did) {
   const long long off = j.next_chunk * chunk, n = std::min(chunk, j.bytes - off);
   if (j.zone >= 0) {
     // coded bytes into the job's landing zone (after the zone's previous decode)
-    const size_t ci = (static_cast<size_t>(j.layer % g->SL) * g->cfg.num_experts + j.expert) * 2;
     if (j.next_chunk == 0) MOE_CUDA(cudaStreamWaitEvent(g->copy_stream, g->pzone_free[j.zone], 0));
     MOE_CUDA(cudaMemcpyAsync(g->pzone + static_cast<long long>(j.zone) * g->pzone_bytes + off,
-                             g->cstore + g->ctab[ci].off + off, n, cudaMemcpyHostToDevice, g->copy_stream));
+                             g->cstore + g->coded_parts(j.layer, j.expert)[0].off + off, n,
+                             cudaMemcpyHostToDevice, g->copy_stream));
   } else {
     moe_status s = issue_copy(g, j.layer, j.buf, j.expert, off, n);
     if (s != MOE_OK) return s;
@@ -406,20 +405,30 @@ struct CodedEntry {
 };
 constexpr uint64_t kCodedMagic = 0x4d4f45584332ull;  // "MOEXC2"
 
-// Sizes of every part from the raw store (the layout of a coded segment).
+// Sizes of every part from the raw store (the layout of a coded segment).  Parts of an expert:
+// w1|w3, then kCodedBParts row pieces of w2, contiguous.
+void part_span(const moe_engine* g, int part, long long* first, long long* n) {
+  const long long na = 2ll * g->f * g->dpad, pb = 1ll * (g->dpad / moe_engine::kCodedBParts) * g->f;
+  *first = part == 0 ? 0 : na + (part - 1) * pb;
+  *n = part == 0 ? na : pb;
+}
+
 moe_status plan_coded(moe_engine* g) {
-  const int E = g->cfg.num_experts;
-  const long long na = 2ll * g->f * g->dpad, nb = 1ll * g->f * g->dpad;
-  const size_t n = static_cast<size_t>(g->SL) * E * 2;
+  MOE_REQUIRE(g->dpad % moe_engine::kCodedBParts == 0, "compressed transfers need hidden_dim %% %d == 0",
+              moe_engine::kCodedBParts);
+  const int E = g->cfg.num_experts, NP = moe_engine::kCodedParts;
+  const size_t n = static_cast<size_t>(g->SL) * E * NP;
   g->ctab.assign(n, moe_engine::CPart{});
   uint64_t off = xc::align16(sizeof(CodedSegHeader) + sizeof(CodedEntry) * n);
   for (int l = 0; l < g->SL; ++l)
     for (int e = 0; e < E; ++e)
-      for (int part = 0; part < 2; ++part) {
-        const uint16_t* w = reinterpret_cast<const uint16_t*>(g->store_block(l, e)) + (part ? na : 0);
-        auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * 2 + part];
+      for (int part = 0; part < NP; ++part) {
+        long long first, cnt;
+        part_span(g, part, &first, &cnt);
+        const uint16_t* w = reinterpret_cast<const uint16_t*>(g->store_block(l, e)) + first;
+        auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * NP + part];
         c.off = off;
-        c.size = xc::encoded_size(w, part ? nb : na, 0);
+        c.size = xc::encoded_size(w, cnt, 0);
         off += c.size;
       }
   g->coded_total = off;
@@ -428,14 +437,15 @@ moe_status plan_coded(moe_engine* g) {
 
 // Encode the planned parts into `seg` (host) and write its table.
 void encode_coded(moe_engine* g, char* seg) {
-  const int E = g->cfg.num_experts;
-  const long long na = 2ll * g->f * g->dpad, nb = 1ll * g->f * g->dpad;
+  const int E = g->cfg.num_experts, NP = moe_engine::kCodedParts;
   for (int l = 0; l < g->SL; ++l)
     for (int e = 0; e < E; ++e)
-      for (int part = 0; part < 2; ++part) {
-        const uint16_t* w = reinterpret_cast<const uint16_t*>(g->store_block(l, e)) + (part ? na : 0);
-        auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * 2 + part];
-        xc::encode(w, part ? nb : na, 0, reinterpret_cast<uint8_t*>(seg + c.off));
+      for (int part = 0; part < NP; ++part) {
+        long long first, cnt;
+        part_span(g, part, &first, &cnt);
+        const uint16_t* w = reinterpret_cast<const uint16_t*>(g->store_block(l, e)) + first;
+        auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * NP + part];
+        xc::encode(w, cnt, 0, reinterpret_cast<uint8_t*>(seg + c.off));
         memcpy(&c.hdr, seg + c.off, sizeof(c.hdr));
       }
   CodedSegHeader h{kCodedMagic, g->ctab.size(), 0, g->coded_total};
@@ -458,7 +468,11 @@ moe_status alloc_landing(moe_engine* g) {
   }
   if (g->S > 0 && !g->pzone) {
     uint64_t mx = 0;
-    for (size_t i = 0; i + 1 < g->ctab.size(); i += 2) mx = std::max<uint64_t>(mx, g->ctab[i].size + g->ctab[i + 1].size);
+    for (size_t i = 0; i < g->ctab.size(); i += moe_engine::kCodedParts) {
+      uint64_t t = 0;
+      for (int q = 0; q < moe_engine::kCodedParts; ++q) t += g->ctab[i + q].size;
+      mx = std::max<uint64_t>(mx, t);
+    }
     g->pzone_bytes = static_cast<long long>(xc::align16(mx));
     const int zones = 2 * g->cfg.top_k;
     MOE_CUDA(cudaMalloc(reinterpret_cast<void**>(&g->pzone), static_cast<size_t>(zones) * g->pzone_bytes));
@@ -806,7 +820,8 @@ moe_status moe_engine_attach_coded(moe_engine* g, void* seg, int64_t seg_bytes, 
   } else {
     CodedSegHeader h;
     memcpy(&h, base, sizeof(h));
-    MOE_REQUIRE(h.magic == kCodedMagic && h.n_entries == static_cast<uint64_t>(g->SL) * g->cfg.num_experts * 2 &&
+    MOE_REQUIRE(h.magic == kCodedMagic &&
+                    h.n_entries == static_cast<uint64_t>(g->SL) * g->cfg.num_experts * moe_engine::kCodedParts &&
                     h.total <= static_cast<uint64_t>(seg_bytes),
                 "not a coded expert segment of this model");
     const CodedEntry* ent = reinterpret_cast<const CodedEntry*>(base + sizeof(CodedSegHeader));
@@ -1138,16 +1153,24 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       if (g->bf16) {
         for (int i = 0; i < plan.n; ++i) {
           MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_a[i], 0));
-          if (plan.comp[i])
-            TRY(xc::decode(plan.land[i], plan.part[i][0]->hdr, reinterpret_cast<uint16_t*>(plan.dst[i]), s));
+          long long coff = 0;
+          if (plan.comp[i]) {
+            TRY(xc::decode(plan.land[i], plan.part[i][0].hdr, reinterpret_cast<uint16_t*>(plan.dst[i]), s));
+            coff = static_cast<long long>(plan.part[i][0].size);
+          }
           TRY(prof_begin(fev));
           TRY(launch_ffn(fp, i));
           TRY(prof_end(fev));
-          MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_b[i], 0));
           if (plan.comp[i]) {
-            TRY(xc::decode(plan.land[i] + plan.part[i][0]->size, plan.part[i][1]->hdr,
-                           reinterpret_cast<uint16_t*>(plan.dst[i] + part_a_bytes(g)), s));
+            for (int q = 1; q < moe_engine::kCodedParts; ++q) {
+              MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_part[i][q], 0));
+              TRY(xc::decode(plan.land[i] + coff, plan.part[i][q].hdr,
+                             reinterpret_cast<uint16_t*>(plan.dst[i] + g->coded_part_out_off(q)), s));
+              coff += static_cast<long long>(plan.part[i][q].size);
+            }
             MOE_CUDA(cudaEventRecord(plan.free_ev[i], s));
+          } else {
+            MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_b[i], 0));
           }
           TRY(prof_begin(fev));
           TRY(launch_down(fp, i));

@@ -148,6 +148,18 @@ struct moe_engine {
     uint64_t off, size;
     moe::xc::PartHeader hdr;
   };
+  // coded expert = part 0 (w1|w3) + kCodedBParts row pieces of w2, contiguous in the store, so
+  // the last piece of a transfer is small and its decode (the step's tail) short
+  static constexpr int kCodedBParts = 4;
+  static constexpr int kCodedParts = 1 + kCodedBParts;
+  const CPart* coded_parts(int layer, int expert) const {
+    return &ctab[(static_cast<size_t>(layer % SL) * cfg.num_experts + expert) * kCodedParts];
+  }
+  // decoded bytes of part p and its offset in the expert block
+  long long coded_part_out_off(int p) const {
+    const long long a = 2ll * f * dpad * 2, pb = 1ll * (dpad / kCodedBParts) * f * 2;
+    return p == 0 ? 0 : a + (p - 1) * pb;
+  }
   char* cstore = nullptr;                 // pinned host (private) or a registered shared segment
   bool cstore_external = false;
   bool cstore_registered = false;

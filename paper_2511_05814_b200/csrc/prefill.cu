@@ -79,7 +79,7 @@ moe_status ensure_state(moe_engine* g, int T) {
                            cudaHostAllocMapped | cudaHostAllocPortable));
     memset(pf->mail_h, 0, sizeof(PrefillMail));
     MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&pf->mail_d), pf->mail_h, 0));
-    for (int i = 0; i < 2 * kMaxE; ++i) {
+    for (int i = 0; i < moe_engine::kCodedParts * kMaxE; ++i) {
       cudaEvent_t e = nullptr;
       MOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       pf->ev.push_back(e);
@@ -374,16 +374,18 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
     // (a stream wait captures the event's latest record at the time of the call)
     auto issue_coded = [&](int i) -> moe_status {
       const int e = m.load_expert[i], slot = i % nslots;
-      const auto& pa = g->ctab[(static_cast<size_t>(l % g->SL) * E + e) * 2];
-      const auto& pb = g->ctab[(static_cast<size_t>(l % g->SL) * E + e) * 2 + 1];
+      const moe_engine::CPart* cp = g->coded_parts(l, e);
       char* land = g->cstage + static_cast<long long>(slot) * g->expert_bytes;
       MOE_CUDA(cudaStreamWaitEvent(g->copy_stream, g->cstage_free[slot], 0));
-      MOE_CUDA(cudaMemcpyAsync(land, g->cstore + pa.off, pa.size, cudaMemcpyHostToDevice, g->copy_stream));
-      MOE_CUDA(cudaEventRecord(pf->ev[2 * i], g->copy_stream));
-      MOE_CUDA(cudaMemcpyAsync(land + pa.size, g->cstore + pb.off, pb.size, cudaMemcpyHostToDevice,
-                               g->copy_stream));
-      MOE_CUDA(cudaEventRecord(pf->ev[2 * i + 1], g->copy_stream));
-      loaded += static_cast<long long>(pa.size + pb.size);
+      long long off = 0;
+      for (int q = 0; q < moe_engine::kCodedParts; ++q) {
+        MOE_CUDA(cudaMemcpyAsync(land + off, g->cstore + cp[q].off, cp[q].size, cudaMemcpyHostToDevice,
+                                 g->copy_stream));
+        off += static_cast<long long>(cp[q].size);
+        // events: part 0 (w1|w3) lets the up GEMM go; the w2 pieces are decoded as they land
+        MOE_CUDA(cudaEventRecord(pf->ev[i * moe_engine::kCodedParts + q], g->copy_stream));
+      }
+      loaded += off;
       return MOE_OK;
     };
     for (int i = 0; i < m.n_loads; ++i) {
@@ -441,17 +443,26 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
       TRY(ffn_down(0, m.res_rows, m.n_res_groups));
     }
     for (int i = 0; i < m.n_loads; ++i) {
-      const int slot = g->cstore ? i % static_cast<int>(g->cstage_free.size()) : 0;
-      const char* land = g->cstore ? g->cstage + static_cast<long long>(slot) * g->expert_bytes : nullptr;
-      const auto* pa = g->cstore ? &g->ctab[(static_cast<size_t>(l % g->SL) * E + m.load_expert[i]) * 2] : nullptr;
-      MOE_CUDA(cudaStreamWaitEvent(s, pf->ev[2 * i], 0));
-      if (pa) TRY(xc::decode(land, pa->hdr, reinterpret_cast<uint16_t*>(dest[i]), s));
-      TRY(ffn(1 + i, m.load_rows[i], 1));
-      MOE_CUDA(cudaStreamWaitEvent(s, pf->ev[2 * i + 1], 0));
-      if (pa) {
-        TRY(xc::decode(land + pa->size, pa[1].hdr, reinterpret_cast<uint16_t*>(dest[i] + split), s));
+      if (g->cstore) {
+        const int slot = i % nslots, NP = moe_engine::kCodedParts;
+        const char* land = g->cstage + static_cast<long long>(slot) * g->expert_bytes;
+        const moe_engine::CPart* cp = g->coded_parts(l, m.load_expert[i]);
+        MOE_CUDA(cudaStreamWaitEvent(s, pf->ev[i * NP], 0));
+        TRY(xc::decode(land, cp[0].hdr, reinterpret_cast<uint16_t*>(dest[i]), s));
+        TRY(ffn(1 + i, m.load_rows[i], 1));
+        long long coff = static_cast<long long>(cp[0].size);
+        for (int q = 1; q < NP; ++q) {
+          MOE_CUDA(cudaStreamWaitEvent(s, pf->ev[i * NP + q], 0));
+          TRY(xc::decode(land + coff, cp[q].hdr,
+                         reinterpret_cast<uint16_t*>(dest[i] + g->coded_part_out_off(q)), s));
+          coff += static_cast<long long>(cp[q].size);
+        }
         MOE_CUDA(cudaEventRecord(g->cstage_free[slot], s));
         if (i + nslots < m.n_loads) TRY(issue_coded(i + nslots));
+      } else {
+        MOE_CUDA(cudaStreamWaitEvent(s, pf->ev[2 * i], 0));
+        TRY(ffn(1 + i, m.load_rows[i], 1));
+        MOE_CUDA(cudaStreamWaitEvent(s, pf->ev[2 * i + 1], 0));
       }
       TRY(ffn_down(1 + i, m.load_rows[i], 1));
     }
