@@ -367,11 +367,24 @@ def run_ours(args, world, rank, local):
     want_prefetch = any(pf for _, _, pf in parsed)
     base_cfg = factory()
     nl = args.layers or base_cfg.num_layers
-    store_layers = args.store_layers
+    # host memory: raw store + coded store when both fit; else the coded store alone
+    # (compress = 2, private stores); else raw with layer aliasing
+    shared = world > 1 or args.shared_store
+    per_layer = base_cfg.num_experts * base_cfg.expert_bytes
+    budget = 0.85 * host_available_bytes()
+    store_layers, compress = args.store_layers, 0
+    want_comp = args.compress != "off"
+    if want_comp and nl * per_layer * 1.75 <= budget:
+        compress = 1
+    elif want_comp and not shared:
+        compress = 2
+        if store_layers < 0 and nl * per_layer * 0.67 > budget:
+            store_layers = max(1, int(budget // (0.67 * per_layer)))
+    elif want_comp and args.compress == "on":
+        compress = 1
     if store_layers < 0:
-        per_layer = base_cfg.num_experts * base_cfg.expert_bytes
-        avail = host_available_bytes()
-        store_layers = 0 if nl * per_layer <= 0.85 * avail else max(1, int(0.85 * avail // per_layer))
+        store_layers = 0 if (compress == 2 or nl * per_layer * (1.75 if compress else 1.0) <= budget) \
+            else max(1, int(budget // (per_layer * (1.75 if compress else 1.0))))
     # HBM: per-layer pool of C policy + S staging buffers; deeper models stage 1 guess per layer
     import torch as _t
     hbm = _t.cuda.get_device_properties(local).total_memory
@@ -379,14 +392,8 @@ def run_ours(args, world, rank, local):
     pf_bufs = 0
     if want_prefetch and nl * (cap_c + base_cfg.top_k) * base_cfg.expert_bytes + dense > 0.9 * hbm:
         pf_bufs = 1
-    shared = world > 1 or args.shared_store
-    raw_store = (min(store_layers, nl) if store_layers > 0 else nl) * base_cfg.num_experts * base_cfg.expert_bytes
-    # the coded store (~0.7x) sits beside the raw one in pinned host memory
-    compress = args.compress == "on" or (args.compress == "auto" and
-                                         1.75 * raw_store <= 0.85 * host_available_bytes())
     # every replica must build the same engine (shared stores): rank 0's host view decides
     store_layers, pf_bufs, compress = broadcast_ints([store_layers, pf_bufs, int(compress)], world)
-    compress = bool(compress)
     cfg = factory(num_layers=nl, cache_size=cap_c, prefetch="early" if want_prefetch else "off",
                   max_tokens=4096, device=local, store_layers=store_layers,
                   prefetch_buffers=pf_bufs, compress=compress)
@@ -420,7 +427,7 @@ def run_ours(args, world, rank, local):
         if eng is None:
             eng = OffloadEngine(cfg, store=store)
             eng.init_random(args.seed, init_experts=False)
-        if cfg.compress:
+        if cfg.compress == 1:
             coded = replicas.open_shared_coded(name + "x", eng, local_rank, lambda: barrier(world))
     else:
         eng = OffloadEngine(cfg)
@@ -562,8 +569,9 @@ def run_ours(args, world, rank, local):
             "setup_s": round(t_setup, 1), "shared_store": store is not None,
             "host_store_layers": cfg.host_store_layers,
             "expert_transfer": ("exponent-coded bf16, lossless (csrc/expcodec.cuh), "
-                                f"{compressed_ratio:.3f} of the raw bytes" if cfg.compress
-                                else "raw bf16"),
+                                f"{compressed_ratio:.3f} of the raw bytes"
+                                + (", coded store only" if cfg.compress == 2 else "")
+                                if cfg.compress else "raw bf16"),
             "prefetch_buffers_per_layer": (cfg.prefetch_buffers or cfg.top_k) if want_prefetch else 0,
         },
         "hit_rate": head["hit_rate"],

@@ -151,8 +151,9 @@ typedef struct {
   int32_t prefetch_buffers; /* staging buffers per layer with prefetch on: 0 = top_k; fewer
                                fit deeper models in HBM (prefetch then covers the best guesses) */
   int32_t compress;       /* 1: demand and prefill copies move the experts exponent-coded
-                             (expcodec.cuh, lossless, ~0.69x the bytes) and decode them in HBM;
-                             SwiGLU engines with a private store and the copy engine only */
+                             (expcodec.cuh, lossless, ~0.65x the bytes) and decode them in HBM;
+                             SwiGLU engines, copy engine.  2: the same with no raw store kept
+                             (coded store only: deeper models fit the host; private stores) */
 } moe_engine_config;
 
 typedef struct {

@@ -413,46 +413,62 @@ void part_span(const moe_engine* g, int part, long long* first, long long* n) {
   *n = part == 0 ? na : pb;
 }
 
+// Raw bf16 words of expert e of a layer whose blocks start at `raw_layer` ([E][expert]).
+inline const uint16_t* raw_words(const moe_engine* g, const char* raw_layer, int e) {
+  return reinterpret_cast<const uint16_t*>(raw_layer + static_cast<long long>(e) * g->expert_bytes);
+}
+
+// Sizes of one layer's parts (offsets assigned in order from *off).
+void plan_layer(moe_engine* g, int l, const char* raw_layer, uint64_t* off) {
+  const int E = g->cfg.num_experts, NP = moe_engine::kCodedParts;
+  for (int e = 0; e < E; ++e)
+    for (int part = 0; part < NP; ++part) {
+      long long first, cnt;
+      part_span(g, part, &first, &cnt);
+      auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * NP + part];
+      c.off = *off;
+      c.size = xc::encoded_size(raw_words(g, raw_layer, e) + first, cnt, 0);
+      *off += c.size;
+    }
+}
+
+void encode_layer(moe_engine* g, int l, const char* raw_layer, char* seg) {
+  const int E = g->cfg.num_experts, NP = moe_engine::kCodedParts;
+  for (int e = 0; e < E; ++e)
+    for (int part = 0; part < NP; ++part) {
+      long long first, cnt;
+      part_span(g, part, &first, &cnt);
+      auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * NP + part];
+      xc::encode(raw_words(g, raw_layer, e) + first, cnt, 0, reinterpret_cast<uint8_t*>(seg + c.off));
+      memcpy(&c.hdr, seg + c.off, sizeof(c.hdr));
+    }
+}
+
+void write_seg_table(moe_engine* g, char* seg) {
+  CodedSegHeader h{kCodedMagic, g->ctab.size(), 0, g->coded_total};
+  h.data_off = xc::align16(sizeof(CodedSegHeader) + sizeof(CodedEntry) * g->ctab.size());
+  memcpy(seg, &h, sizeof(h));
+  CodedEntry* ent = reinterpret_cast<CodedEntry*>(seg + sizeof(CodedSegHeader));
+  for (size_t i = 0; i < g->ctab.size(); ++i) ent[i] = CodedEntry{g->ctab[i].off, g->ctab[i].size, g->ctab[i].hdr};
+}
+
 moe_status plan_coded(moe_engine* g) {
   MOE_REQUIRE(g->dpad % moe_engine::kCodedBParts == 0, "compressed transfers need hidden_dim %% %d == 0",
               moe_engine::kCodedBParts);
+  MOE_REQUIRE(!g->coded_only, "a coded-only engine has no raw store to plan from");
   const int E = g->cfg.num_experts, NP = moe_engine::kCodedParts;
   const size_t n = static_cast<size_t>(g->SL) * E * NP;
   g->ctab.assign(n, moe_engine::CPart{});
   uint64_t off = xc::align16(sizeof(CodedSegHeader) + sizeof(CodedEntry) * n);
-  for (int l = 0; l < g->SL; ++l)
-    for (int e = 0; e < E; ++e)
-      for (int part = 0; part < NP; ++part) {
-        long long first, cnt;
-        part_span(g, part, &first, &cnt);
-        const uint16_t* w = reinterpret_cast<const uint16_t*>(g->store_block(l, e)) + first;
-        auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * NP + part];
-        c.off = off;
-        c.size = xc::encoded_size(w, cnt, 0);
-        off += c.size;
-      }
+  for (int l = 0; l < g->SL; ++l) plan_layer(g, l, g->store_block(l, 0), &off);
   g->coded_total = off;
   return MOE_OK;
 }
 
 // Encode the planned parts into `seg` (host) and write its table.
 void encode_coded(moe_engine* g, char* seg) {
-  const int E = g->cfg.num_experts, NP = moe_engine::kCodedParts;
-  for (int l = 0; l < g->SL; ++l)
-    for (int e = 0; e < E; ++e)
-      for (int part = 0; part < NP; ++part) {
-        long long first, cnt;
-        part_span(g, part, &first, &cnt);
-        const uint16_t* w = reinterpret_cast<const uint16_t*>(g->store_block(l, e)) + first;
-        auto& c = g->ctab[(static_cast<size_t>(l) * E + e) * NP + part];
-        xc::encode(w, cnt, 0, reinterpret_cast<uint8_t*>(seg + c.off));
-        memcpy(&c.hdr, seg + c.off, sizeof(c.hdr));
-      }
-  CodedSegHeader h{kCodedMagic, g->ctab.size(), 0, g->coded_total};
-  h.data_off = xc::align16(sizeof(CodedSegHeader) + sizeof(CodedEntry) * g->ctab.size());
-  memcpy(seg, &h, sizeof(h));
-  CodedEntry* ent = reinterpret_cast<CodedEntry*>(seg + sizeof(CodedSegHeader));
-  for (size_t i = 0; i < g->ctab.size(); ++i) ent[i] = CodedEntry{g->ctab[i].off, g->ctab[i].size, g->ctab[i].hdr};
+  for (int l = 0; l < g->SL; ++l) encode_layer(g, l, g->store_block(l, 0), seg);
+  write_seg_table(g, seg);
 }
 
 // HBM landing slots for demand misses (K) and prefetch zones (2K when prefetch is on).
@@ -538,6 +554,8 @@ moe_status moe_engine_create_ex(const moe_engine_config* cfg_in, void* store, in
   MOE_REQUIRE(!(c.transfer == MOE_TRANSFER_SM && c.prefetch),
               "speculative prefetch runs on the copy engine (transfer=SM has no staging path)");
   MOE_REQUIRE(c.prefetch_buffers >= 0, "prefetch_buffers must be >= 0");
+  MOE_REQUIRE(c.compress >= 0 && c.compress <= 2, "compress must be 0, 1 or 2");
+  MOE_REQUIRE(c.compress != 2 || !store, "a coded-only engine owns its store (no shared raw store)");
   MOE_REQUIRE(!c.compress || c.expert_kind == MOE_EXPERT_SWIGLU_BF16,
               "compressed transfers code bf16 experts (SwiGLU engines)");
   MOE_REQUIRE(!c.compress || c.transfer != MOE_TRANSFER_SM,
@@ -561,6 +579,7 @@ moe_status moe_engine_create_ex(const moe_engine_config* cfg_in, void* store, in
     g->f = g->dpad;
     g->expert_bytes = 2ll * g->dpad * g->dpad * 4;
   }
+  g->coded_only = c.compress == 2;
   g->sm_transfer = c.transfer == MOE_TRANSFER_SM ||
                    (c.transfer == MOE_TRANSFER_AUTO && !c.prefetch && !c.compress &&
                     g->expert_bytes <= (16ll << 20));
@@ -637,7 +656,8 @@ moe_status create_resources(moe_engine* g) {
   }
   if (getenv("MOE_GATE_TIMING"))
     TRY(alloc_device(reinterpret_cast<void**>(&g->gate_phase_ns), 8 * sizeof(unsigned long long)));
-  const size_t store_bytes = static_cast<size_t>(g->SL) * E * g->expert_bytes;
+  // coded-only engines keep one raw layer as the encoder's staging buffer
+  const size_t store_bytes = static_cast<size_t>(g->coded_only ? 1 : g->SL) * E * g->expert_bytes;
   if (g->ext_store) {
     MOE_REQUIRE(static_cast<size_t>(g->ext_store_bytes) >= store_bytes,
                 "external expert store holds %lld bytes, the model needs %zu",
@@ -784,6 +804,41 @@ moe_status moe_engine_init_random(moe_engine* g, uint64_t seed, float gate_bias_
   // replica attached to a shared store leaves this to the store's owner)
   uint16_t* scratch = reinterpret_cast<uint16_t*>(g->pool);
   const long long fd = 1ll * f * d;
+  if (g->coded_only && init_experts) {
+    // no raw store: each layer is generated into a one-layer host staging buffer and coded;
+    // two passes (sizes, then bytes) so the coded store is one exact pinned allocation
+    auto gen_layer = [&](int l) -> moe_status {
+      for (int e = 0; e < E; ++e) {
+        TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW1), sd, fd, scratch, s));
+        TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW3), sd, fd, scratch + fd, s));
+        TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW2), sf, fd, scratch + 2 * fd, s));
+        MOE_CUDA(cudaMemcpyAsync(g->store.base + static_cast<long long>(e) * g->expert_bytes, scratch,
+                                 g->expert_bytes, cudaMemcpyDeviceToHost, s));
+      }
+      MOE_CUDA(cudaStreamSynchronize(s));
+      return MOE_OK;
+    };
+    const int NP = moe_engine::kCodedParts;
+    g->ctab.assign(static_cast<size_t>(g->SL) * E * NP, moe_engine::CPart{});
+    uint64_t off = xc::align16(sizeof(CodedSegHeader) + sizeof(CodedEntry) * g->ctab.size());
+    for (int l = 0; l < g->SL; ++l) {
+      TRY(gen_layer(l));
+      plan_layer(g, l, g->store.base, &off);
+    }
+    g->coded_total = off;
+    if (g->cstore) cudaFreeHost(g->cstore);
+    g->cstore = nullptr;
+    MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g->cstore), g->coded_total, cudaHostAllocPortable));
+    g->cstore_external = false;
+    for (int l = 0; l < g->SL; ++l) {
+      TRY(gen_layer(l));
+      encode_layer(g, l, g->store.base, g->cstore);
+    }
+    write_seg_table(g, g->cstore);
+    TRY(alloc_landing(g));
+    g->st.compressed_store_bytes = static_cast<int64_t>(g->coded_total);
+    return MOE_OK;
+  }
   for (int l = 0; l < (init_experts ? g->SL : 0); ++l)
     for (int e = 0; e < E; ++e) {
       TRY(launch_hash_bf16(seed, tensor_id(kTExpert, l, e, kMatW1), sd, fd, scratch, s));
@@ -846,6 +901,7 @@ moe_status moe_engine_expert_host_ptr(moe_engine* g, int32_t layer, int32_t expe
   MOE_REQUIRE(g && layer >= 0 && layer < g->cfg.num_layers && expert >= 0 &&
                   expert < g->cfg.num_experts,
               "expert (%d, %d) out of range", layer, expert);
+  MOE_REQUIRE(!g->coded_only, "a coded-only engine keeps no raw expert blocks");
   *ptr = g->store_block(layer, expert);
   *bytes = g->expert_bytes;
   return MOE_OK;

@@ -162,6 +162,7 @@ struct moe_engine {
   }
   char* cstore = nullptr;                 // pinned host (private) or a registered shared segment
   bool cstore_external = false;
+  bool coded_only = false;                // compress = 2: no raw store after encoding
   bool cstore_registered = false;
   uint64_t coded_total = 0;
   std::vector<CPart> ctab;                // [(SL * E + e) * 2 + part]
