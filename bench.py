@@ -403,7 +403,7 @@ def run_ours(args, world, rank, local):
         if args.model == "mixtral_8x7b":
             cpu = cpu_reference_sample(args.seed, args.cpu_sample_tokens, args.cpu_sample_layers)
         else:  # configs[4]: a bounded sample (fp64 8x22B experts are 2.4 GB each)
-            cpu = cpu_reference_sample(args.seed, 4, 1, shape=(base_cfg.num_layers, base_cfg.num_experts,
+            cpu = cpu_reference_sample(args.seed, 16, 1, shape=(base_cfg.num_layers, base_cfg.num_experts,
                                                               base_cfg.top_k, base_cfg.hidden_dim,
                                                               base_cfg.ffn_dim))
     pcie_peak = h2d_peak_gbs(dev)
