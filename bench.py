@@ -51,7 +51,7 @@ def parse_args():
     p.add_argument("--cache-size", type=int, default=4)
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--variants", default="lru,lfu,lfu+prefetch")
-    p.add_argument("--e2e-steps", type=int, default=4)
+    p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--cpu-sample-tokens", type=int, default=16)
     p.add_argument("--cpu-sample-layers", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
