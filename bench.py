@@ -528,6 +528,7 @@ def run_ours(args, world, rank, local):
         barrier(world)
         coded.close()
     gemm_iso = isolated_gemm(D, F) if rank == 0 and args.prefill_tokens > 0 else None
+    gemm_iso_t = isolated_gemm(D, F, 1024) if rank == 0 and args.prefill_tokens > 0 else None
     tiny = run_tiny(args) if rank == 0 and world == 1 and args.tiny_tokens > 0 else None
     if store is not None:
         barrier(world)
@@ -616,7 +617,7 @@ def run_ours(args, world, rank, local):
         line["tiny"] = tiny
     if prefill:
         tf_peak = float(peaks.get("bf16_tflops", 1590.0))
-        for rec in [prefill["gemm"]] + ([gemm_iso] if gemm_iso else []):
+        for rec in [prefill["gemm"]] + [r for r in (gemm_iso, gemm_iso_t) if r]:
             rec["tensor_frac"] = rec["tflops"] / tf_peak
             rec["hbm_frac"] = rec["algorithmic_GBps"] / hbm_peak
             rec["bound"] = "tensor" if rec["tensor_frac"] >= rec["hbm_frac"] else "hbm"
@@ -626,6 +627,7 @@ def run_ours(args, world, rank, local):
             rec["peaks"] = {"bf16_tflops": tf_peak, "hbm_gbs": hbm_peak,
                             "source": peaks.get("source", "MEASURED_PEAKS.json")}
         prefill["gemm_isolated"] = gemm_iso
+        prefill["gemm_isolated_tensor_bound"] = gemm_iso_t
         line["prefill"] = prefill
     print(json.dumps(line), flush=True)
 
@@ -821,9 +823,10 @@ def cpu_prefill_sample(seed, P, X, layers=1):
                       "untimed weight materialisation"}
 
 
-def isolated_gemm(Dd, Ff):
-    """K4 alone: the 8 experts of one layer resident in HBM, 128 token rows each (512 tokens x
-    top-2): grouped SwiGLU up (w1|w3) then grouped down, CUDA events per launch."""
+def isolated_gemm(Dd, Ff, m=128):
+    """K4 alone: the 8 experts of one layer resident in HBM, m token rows each (m = 128: 512
+    tokens x top-2, HBM-bound; m = 1024: 4096 tokens, tensor-bound): grouped SwiGLU up (w1|w3)
+    then grouped down, CUDA events per launch."""
     import ctypes
 
     import torch
@@ -831,7 +834,7 @@ def isolated_gemm(Dd, Ff):
     from paper_2511_05814_b200 import _native
 
     lib = _native.lib()
-    G, m = 8, 128
+    G = 8
     gm = (ctypes.c_int32 * G)(*([m] * G))
     X = torch.randn(G * m, Dd, device="cuda").bfloat16()
     W13 = (torch.randn(G, 2 * Ff, Dd, device="cuda") / Dd ** 0.5).bfloat16()
@@ -850,8 +853,8 @@ def isolated_gemm(Dd, Ff):
     ms = ms_u.value + ms_d.value
     del X, W13, act, W2, out
     torch.cuda.empty_cache()
-    return {"kernel": "tc::grouped_gemm_kernel isolated: 8 resident experts x 128 rows, SwiGLU up + "
-                      "down (2 launches, weights 2.82 GB > L2)",
+    return {"kernel": f"tc::grouped_gemm_kernel isolated: 8 resident experts x {m} rows, SwiGLU up + "
+                      "down (2 launches, weights 2.82 GB > L2)", "rows_per_expert": m,
             "up_ms": ms_u.value, "down_ms": ms_d.value, "ms": ms,
             "tflops": flops / (ms / 1e3) / 1e12, "algorithmic_GBps": nbytes / (ms / 1e3) / 1e9}
 
