@@ -51,7 +51,7 @@ def parse_args():
     p.add_argument("--cache-size", type=int, default=4)
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--variants", default="lru,lfu,lfu+prefetch")
-    p.add_argument("--e2e-steps", type=int, default=8)
+    p.add_argument("--e2e-steps", type=int, default=16)
     p.add_argument("--cpu-sample-tokens", type=int, default=16)
     p.add_argument("--cpu-sample-layers", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -88,17 +88,35 @@ def dist_env():
     return world, rank, local
 
 
+def gpu_of(local):
+    """The rank's GPU: its local rank, or MOEB200_REPLICA_DEVICE for every rank (several
+    replicas sharing one GPU -- a one-GPU check of the replica path; the ranks then talk gloo)."""
+    dev = os.environ.get("MOEB200_REPLICA_DEVICE")
+    return int(dev) if dev is not None else local
+
+
 def dist_init(world, local):
     import torch
     import torch.distributed as dist
 
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        if torch.cuda.is_available():
+        if torch.cuda.is_available() and "MOEB200_REPLICA_DEVICE" not in os.environ:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
+
+
+def replicas_per_gpu(world):
+    return int(os.environ.get("LOCAL_WORLD_SIZE", "1")) if "MOEB200_REPLICA_DEVICE" in os.environ else 1
+
+
+def _coll_device():
+    import torch
+    import torch.distributed as dist
+
+    return "cuda" if (torch.cuda.is_available() and dist.get_backend() == "nccl") else "cpu"
 
 
 def barrier(world):
@@ -114,8 +132,7 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -126,8 +143,7 @@ def sum_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -139,8 +155,7 @@ def broadcast_ints(values, world):
     import torch
     import torch.distributed as dist
 
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    t = torch.tensor(values, dtype=torch.int64, device=dev)
+    t = torch.tensor(values, dtype=torch.int64, device=_coll_device())
     dist.broadcast(t, src=0)
     return [int(v) for v in t.tolist()]
 
@@ -351,12 +366,13 @@ def parse_variant(v: str, default_c: int):
 
 
 def run_ours(args, world, rank, local):
+    gpu = gpu_of(local)
     import torch
 
     from paper_2511_05814_b200 import _native, replicas
     from paper_2511_05814_b200.engine import EngineConfig, OffloadEngine, hash_weights, tensor_id
 
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", gpu)
     torch.cuda.set_device(dev)
     factory = EngineConfig.mixtral_8x22b if args.model == "mixtral_8x22b" else EngineConfig.mixtral_8x7b
     variants = [v for v in args.variants.split(",") if v]
@@ -387,7 +403,7 @@ def run_ours(args, world, rank, local):
             else max(1, int(budget // (per_layer * (1.75 if compress else 1.0))))
     # HBM: per-layer pool of C policy + S staging buffers; deeper models stage 1 guess per layer
     import torch as _t
-    hbm = _t.cuda.get_device_properties(local).total_memory
+    hbm = _t.cuda.get_device_properties(gpu).total_memory // max(1, replicas_per_gpu(world))
     dense = nl * (2 * base_cfg.hidden_dim ** 2 + 4 * base_cfg.num_experts * base_cfg.hidden_dim)
     pf_bufs = 0
     if want_prefetch and nl * (cap_c + base_cfg.top_k) * base_cfg.expert_bytes + dense > 0.9 * hbm:
@@ -395,7 +411,7 @@ def run_ours(args, world, rank, local):
     # every replica must build the same engine (shared stores): rank 0's host view decides
     store_layers, pf_bufs, compress = broadcast_ints([store_layers, pf_bufs, int(compress)], world)
     cfg = factory(num_layers=nl, cache_size=cap_c, prefetch="early" if want_prefetch else "off",
-                  max_tokens=4096, device=local, store_layers=store_layers,
+                  max_tokens=4096, device=gpu, store_layers=store_layers,
                   prefetch_buffers=pf_bufs, compress=compress)
     D, F, EB = cfg.hidden_dim, cfg.ffn_dim, cfg.expert_bytes
     cpu = None
@@ -460,7 +476,7 @@ def run_ours(args, world, rank, local):
         n0 = _native.kernel_launches()
         barrier(world)
         torch.cuda.synchronize()
-        sampler = ClockSampler(local) if headline else None
+        sampler = ClockSampler(gpu) if headline else None
         if sampler:
             sampler.__enter__()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -50,7 +50,16 @@ class SharedExpertStore:
 
     @classmethod
     def attach(cls, name: str) -> "SharedExpertStore":
-        return cls(shared_memory.SharedMemory(name=name), False)
+        shm = shared_memory.SharedMemory(name=name)
+        # Python < 3.13 registers attached segments with this process's resource tracker,
+        # which would unlink the owner's segment when an attaching replica exits first
+        from multiprocessing import resource_tracker
+
+        try:
+            resource_tracker.unregister(shm._name, "shared_memory")
+        except Exception:
+            pass
+        return cls(shm, False)
 
     @property
     def nbytes(self) -> int:
