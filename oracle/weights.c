@@ -3,8 +3,10 @@
  *
  * C restatement of the engine's synthetic-weight definition (DESIGN.md "Synthetic
  * weights"), written from the spec, not shared with paper_2511_05814_b200/csrc:
- *   key = sm(seed ^ sm(tensor_id)),  h = sm(key + i)   (sm = splitmix64 finaliser)
- *   s   = (int)(h >> 40) - 2^23,  v = (float)s * (float)(sqrt(3) * std / 2^23)
+ *   key = sm(seed ^ sm(tensor_id))   (sm = splitmix64 finaliser)
+ *   a = sm(key + 2i), b = sm(key + 2i + 1)
+ *   s = t(a >> 40) + t(a >> 16) + t(b >> 40) + t(b >> 16),  t(x) = (x mod 2^24) - 2^23
+ *   v = (float)s * (float)(sqrt(3) * std / 2^24)   (int -> float and the multiply round RNE)
  *   bf16 = round-to-nearest-even(v)
  * Compile with -ffp-contract=off (a single multiply, but keep the rule explicit).
  * Multi-threaded fills let the CPU baseline materialise Mixtral-sized experts quickly.
@@ -20,10 +22,13 @@ static uint64_t sm(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-static float scale_of(float std) { return (float)(1.7320508075688772 * (double)std / 8388608.0); }
+static float scale_of(float std) { return (float)(1.7320508075688772 * (double)std / 16777216.0); }
+
+static inline int32_t t24(uint64_t x) { return (int32_t)(x & 0xFFFFFFu) - (1 << 23); }
 
 static inline float value_at(uint64_t key, uint64_t i, float c) {
-  int32_t s = (int32_t)(sm(key + i) >> 40) - (1 << 23);
+  const uint64_t a = sm(key + 2 * i), b = sm(key + 2 * i + 1);
+  const int32_t s = t24(a >> 40) + t24(a >> 16) + t24(b >> 40) + t24(b >> 16);
   return (float)s * c;
 }
 

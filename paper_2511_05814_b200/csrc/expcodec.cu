@@ -16,7 +16,7 @@ inline int expo(uint16_t w) { return (w >> 7) & 0xFF; }
 inline uint32_t pad8(uint32_t x) { return (x + 7) & ~7u; }
 
 struct ChunkStats {
-  uint8_t base;
+  uint8_t base, win;
   uint32_t e3, e4, l2, l3;  // escapes of mode 3 / 4; mode 23 level-2 codes and byte escapes
 };
 
@@ -48,13 +48,28 @@ Plan make_plan(const uint16_t* in, uint64_t n, int mode_req) {
     const uint64_t a = static_cast<uint64_t>(c) * kChunk, b = std::min<uint64_t>(n, a + kChunk);
     int mx = 0;
     for (uint64_t i = a; i < b; ++i) mx = std::max(mx, expo(in[i]));
-    ChunkStats s{static_cast<uint8_t>(mx), 0, 0, 0, 0};
-    for (uint64_t i = a; i < b; ++i) {
-      const int dl = mx - expo(in[i]);
-      s.e3 += dl >= 7;
-      s.e4 += dl >= 15;
-      s.l2 += dl >= 3;
-      s.l3 += dl >= 10;
+    uint32_t hist[256] = {};
+    for (uint64_t i = a; i < b; ++i) ++hist[mx - expo(in[i])];
+    ChunkStats s{static_cast<uint8_t>(mx), 0, 0, 0, 0, 0};
+    for (int dl = 0; dl < 256; ++dl) {
+      s.e3 += dl >= 7 ? hist[dl] : 0;
+      s.e4 += dl >= 15 ? hist[dl] : 0;
+    }
+    // mode 23 window: level 1 covers dl in [w, w + 3), level 2 the 7 ranks r from w2 =
+    // max(0, w - 2) (r = dl below the window, dl - 3 above it); the rest are escape bytes
+    uint64_t best = ~0ull;
+    const uint32_t cnt = static_cast<uint32_t>(b - a);
+    for (int w = 0; w <= mx; ++w) {
+      const int w2 = w > 2 ? w - 2 : 0;
+      uint32_t in1 = 0, in2 = 0;
+      for (int dl = w; dl < w + 3 && dl < 256; ++dl) in1 += hist[dl];
+      for (int r = w2; r < w2 + 7; ++r) {
+        const int dl = r < w ? r : r + 3;
+        if (dl < 256) in2 += hist[dl];
+      }
+      const uint32_t l2 = cnt - in1, l3 = l2 - in2;
+      const uint64_t cost = 3ull * pad8(l2) + 8ull * l3;
+      if (cost < best) best = cost, s.win = static_cast<uint8_t>(w), s.l2 = l2, s.l3 = l3;
     }
     p.st[c] = s;
   });
@@ -130,21 +145,23 @@ uint64_t encode(const uint16_t* in, uint64_t n, int mode_req, uint8_t* out) {
     e.esc_off = p.esc_off[c];
     e.l2_off = p.l2_off[c];
     e.base = p.st[c].base;
+    e.win = p.mode == kMode23 ? p.st[c].win : 0;
     ce[c] = e;
     const uint64_t a = static_cast<uint64_t>(c) * kChunk, b = std::min<uint64_t>(n, a + kChunk);
     uint32_t ei = p.esc_off[c];
     uint64_t l2i = p.l2_off[c];
-    const int base = p.st[c].base;
+    const int base = p.st[c].base, win = e.win;
     // chunks start on whole bytes of every plane (kChunk * k bits, 24-bit level-2 runs)
     for (uint64_t i = a; i < b; ++i) {
       const uint16_t w = in[i];
       low[i] = static_cast<uint8_t>(((w >> 8) & 0x80) | (w & 0x7F));
       const int dl = base - expo(w);
       if (p.mode == kMode23) {
-        const uint32_t c1 = dl < 3 ? static_cast<uint32_t>(dl + 1) : 0u;
+        const uint32_t c1 = dl >= win && dl < win + 3 ? static_cast<uint32_t>(dl - win + 1) : 0u;
         put_bits(codes, i * 2, c1, 2);
         if (!c1) {
-          const uint32_t c2 = dl < 10 ? static_cast<uint32_t>(dl - 2) : 0u;
+          const int r = dl < win ? dl : dl - 3, w2 = win > 2 ? win - 2 : 0;
+          const uint32_t c2 = r >= w2 && r < w2 + 7 ? static_cast<uint32_t>(r - w2 + 1) : 0u;
           put_bits(l2, l2i * 3, c2, 3);
           ++l2i;
           if (!c2) escb[ei++] = static_cast<uint8_t>(expo(w));
@@ -261,17 +278,19 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
     const int before2 = block_exclusive_scan(n2, warp_tot);
     if (!active) return;
     const uint8_t* esc = part + h.esc_off + ce.esc_off + before2;
+    const uint32_t win = ce.win;
     int k = 0, e = 0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const uint32_t b8 = (lo[j >> 2] >> (8 * (j & 3))) & 0xFFu;
       const uint32_t cc = static_cast<uint32_t>((c0 >> (2 * j)) & 3u);
-      uint32_t ex = static_cast<uint32_t>(ce.base) + 1u - cc;
+      uint32_t ex = static_cast<uint32_t>(ce.base) + 1u - cc - win;
       if ((escm >> j) & 1u) {
         const uint32_t c2 = get3(wlo, whi, sh + 3 * k);
         ++k;
         if (c2) {
-          ex = static_cast<uint32_t>(ce.base) - 2u - c2;
+          const uint32_t r = c2 - 1u + (win > 2u ? win - 2u : 0u);
+          ex = static_cast<uint32_t>(ce.base) - (r < win ? r : r + 3u);
         } else {
           ex = esc[e];
           ++e;

@@ -4,11 +4,14 @@
 // synthetic Mixtral weights), so a part is stored as a sign+mantissa byte per weight plus an
 // exponent code relative to the largest exponent of its 4096-weight chunk (dl = base - exp):
 //   mode 3 / 4   k-bit code c = dl + 1 in [1, 2^k - 1]; c = 0 escapes to an exponent byte
-//   mode 23      2-bit code c1 = dl + 1 for dl < 3; c1 = 0 escapes to a 3-bit second-level
-//                code c2 = dl - 2 for dl < 10, whose 0 escapes to an exponent byte
-// The encoder picks the smallest mode per part: 1.305 bytes / weight with mode 23 on the
-// synthetic weights (1.384 with mode 3, 1.5 with 4; raw 2).  Decoding is exact, so everything
-// downstream is bit-identical.
+//   mode 23      2-bit code c1 = dl - w + 1 for dl in the chunk's window [w, w + 3); c1 = 0
+//                escapes to a 3-bit second-level code over the next 7 values, c2 = r - w2 + 1
+//                for r = (dl < w ? dl : dl - 3) in [w2, w2 + 7), w2 = max(0, w - 2), whose 0
+//                escapes to an exponent byte.  The encoder picks the cheapest w per chunk
+//                (0 for a uniform draw, 1 for a bell-shaped one, deeper under an outlier)
+// The encoder picks the smallest mode per part: on the synthetic (bell-shaped) weights 1.35
+// bytes / weight with mode 23 (1.41 with mode 3, 1.50 with 4; raw 2; the exponent entropy
+// bounds it at 1.32).  Decoding is exact, so everything downstream is bit-identical.
 //
 // Part layout (every section 16-byte aligned):
 //   PartHeader | ChunkEntry[nch] | low[n] | codes (k * n bits, or 2 * n bits in mode 23)
@@ -38,7 +41,8 @@ struct ChunkEntry {
   uint32_t esc_off;     // index of the chunk's first escape byte
   uint32_t l2_off;      // mode 23: index of the chunk's first level-2 code (multiple of 8)
   uint8_t base;         // largest exponent in the chunk
-  uint8_t pad[7];
+  uint8_t win;          // mode 23: first dl of the level-1 window (w)
+  uint8_t pad[6];
 };
 
 inline __host__ __device__ uint64_t align16(uint64_t x) { return (x + 15) & ~uint64_t(15); }

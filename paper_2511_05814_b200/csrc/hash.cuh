@@ -1,10 +1,13 @@
-// Counter-based synthetic weights.
-//   h   = mix64(mix64(seed ^ mix64(tensor_id)) + index)          (splitmix64 finaliser)
-//   s24 = (int32)(h >> 40) - 2^23                                 in [-2^23, 2^23)
-//   v   = (float)s24 * c,  c = (float)(sqrt(3) * std / 2^23)     one fp32 rounding
+// Counter-based synthetic weights, approximately N(0, std^2):
+//   key = mix64(seed ^ mix64(tensor_id))                          (splitmix64 finaliser)
+//   a   = mix64(key + 2 i),  b = mix64(key + 2 i + 1)
+//   s   = u(a >> 40) + u(a >> 16) + u(b >> 40) + u(b >> 16),  u(x) = (x & 0xFFFFFF) - 2^23
+//         (an Irwin-Hall sum of four uniform 24-bit integers: variance 2^48 / 3)
+//   v   = (float)s * c,  c = (float)(sqrt(3) * std / 2^24)       two RNE roundings
 //   w   = bf16_rne(v)  (or v itself for f32 tensors)
-// Uniform with variance std^2; integer-only up to one multiply, so the CUDA kernel, the
-// oracle's C restatement (oracle/weights.c) and numpy produce identical bits.
+// Integer-only up to one conversion and one multiply, so the CUDA kernel, the oracle's C
+// restatement (oracle/weights.c) and numpy produce identical bits.  The bell shape matters for
+// the exponent statistics that expert compression sees (a uniform draw would flatter it).
 #pragma once
 #include <cstdint>
 
@@ -21,12 +24,25 @@ __host__ __device__ __forceinline__ uint64_t tensor_key(uint64_t seed, uint64_t 
   return mix64(seed ^ mix64(tensor_id));
 }
 
-__host__ __device__ __forceinline__ int32_t hash_s24(uint64_t key, uint64_t index) {
-  return static_cast<int32_t>(mix64(key + index) >> 40) - (1 << 23);
+__host__ __device__ __forceinline__ int32_t hash_u24(uint64_t x) {
+  return static_cast<int32_t>(x & 0xFFFFFFull) - (1 << 23);
+}
+
+__host__ __device__ __forceinline__ int32_t hash_sum4(uint64_t key, uint64_t index) {
+  const uint64_t a = mix64(key + 2 * index), b = mix64(key + 2 * index + 1);
+  return hash_u24(a >> 40) + hash_u24(a >> 16) + hash_u24(b >> 40) + hash_u24(b >> 16);
+}
+
+__host__ __device__ __forceinline__ float hash_value(uint64_t key, uint64_t index, float c) {
+#ifdef __CUDA_ARCH__
+  return __fmul_rn(__int2float_rn(hash_sum4(key, index)), c);
+#else
+  return static_cast<float>(hash_sum4(key, index)) * c;
+#endif
 }
 
 inline float hash_scale(float std) {
-  return static_cast<float>(1.7320508075688772 * static_cast<double>(std) / 8388608.0);
+  return static_cast<float>(1.7320508075688772 * static_cast<double>(std) / 16777216.0);
 }
 
 __host__ __device__ __forceinline__ uint16_t f32_to_bf16_rne(float v) {

@@ -12,15 +12,15 @@ __global__ void hash_bf16_kernel(uint64_t key, float c, long long n, uint16_t* _
       uint32_t w[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const float a = static_cast<float>(hash_s24(key, base + 2 * q)) * c;
-        const float b = static_cast<float>(hash_s24(key, base + 2 * q + 1)) * c;
+        const float a = hash_value(key, base + 2 * q, c);
+        const float b = hash_value(key, base + 2 * q + 1, c);
         w[q] = static_cast<uint32_t>(f32_to_bf16_rne(a)) |
                (static_cast<uint32_t>(f32_to_bf16_rne(b)) << 16);
       }
       *reinterpret_cast<uint4*>(out + base) = make_uint4(w[0], w[1], w[2], w[3]);
     } else {
       for (long long i = base; i < n; ++i)
-        out[i] = f32_to_bf16_rne(static_cast<float>(hash_s24(key, i)) * c);
+        out[i] = f32_to_bf16_rne(hash_value(key, i, c));
     }
   }
 }
@@ -29,7 +29,7 @@ __global__ void hash_f32_kernel(uint64_t key, float c, long long n, float* __res
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += stride)
-    out[i] = static_cast<float>(hash_s24(key, i)) * c;
+    out[i] = hash_value(key, i, c);
 }
 
 moe_status launch_hash_bf16(uint64_t seed, uint64_t tid, float std, long long n, uint16_t* out,
