@@ -50,7 +50,10 @@ def parse_args():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--cache-size", type=int, default=4)
     p.add_argument("--seed", type=int, default=42)
-    p.add_argument("--variants", default="lru,lfu,lfu+prefetch")
+    p.add_argument("--variants", default=None,
+                   help="headline = the first; policy[+prefetch][@cache_size]. Default: configs[1] "
+                        "and [2] (LRU, LFU, LFU+prefetch at C=4; LFU, LFU+prefetch at C=2 and 6) "
+                        "for 8x7B, configs[4] (LFU+prefetch at C=4) for 8x22B")
     p.add_argument("--e2e-steps", type=int, default=16)
     p.add_argument("--cpu-sample-tokens", type=int, default=16)
     p.add_argument("--cpu-sample-layers", type=int, default=1)
@@ -67,8 +70,8 @@ def parse_args():
                    help="e.g. 2,4,6: LFU and LFU+prefetch at each cache size (configs[2])")
     p.add_argument("--prefill-tokens", type=int, default=512,
                    help="configs[3]: prefill this many tokens (tcgen05 GEMM path), 0 = skip")
-    p.add_argument("--prefill-decode", type=int, default=8,
-                   help="decode tokens timed after the prefill (configs[3] says 256; bounded here)")
+    p.add_argument("--prefill-decode", type=int, default=256,
+                   help="decode tokens timed after the prefill (configs[3]: 256)")
     p.add_argument("--trace-variants", default="zipf:1.0",
                    help="trace-driven decode (SURVEY 8f.3): comma list of zipf:<skew> / "
                         "markov:<repeat_prob>; LRU and LFU on each; '' = skip")
@@ -375,6 +378,9 @@ def run_ours(args, world, rank, local):
     dev = torch.device("cuda", gpu)
     torch.cuda.set_device(dev)
     factory = EngineConfig.mixtral_8x22b if args.model == "mixtral_8x22b" else EngineConfig.mixtral_8x7b
+    if args.variants is None:
+        args.variants = ("lfu+prefetch" if args.model == "mixtral_8x22b" else
+                         "lru,lfu,lfu+prefetch,lfu@2,lfu+prefetch@2,lfu@6,lfu+prefetch@6")
     variants = [v for v in args.variants.split(",") if v]
     if args.sweep_cache:
         variants = [f"{p}@{c}" for c in args.sweep_cache.split(",") for p in ("lfu", "lfu+prefetch")]
@@ -801,7 +807,8 @@ def run_prefill(args, eng, inputs, base, stream, world, pcie_peak):
     if not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_prefill_sample(args.seed, P, X)
     if args.prefill_decode > 0:
-        xs = inputs[: args.prefill_decode]
+        xs = torch.stack([hash_weights(args.seed, tensor_id(5, base + 200000 + t), 1.0, Dd, "f32")
+                          for t in range(args.prefill_decode)])
         h0 = eng.stats()
         a.record(stream)
         eng.decode_device(xs)
@@ -813,6 +820,7 @@ def run_prefill(args, eng, inputs, base, stream, world, pcie_peak):
         out["decode_after_prefill"] = {"tokens": args.prefill_decode,
                                        "tokens_per_s": args.prefill_decode / (ms_d / 1e3),
                                        "hit_rate": dh / max(1, dh + dm)}
+        out["request_ms"] = ms_p + ms_d  # the whole configs[3] request: prefill + decode
     return out
 
 
