@@ -11,7 +11,8 @@ timing   W untimed warm-up tokens, then K tokens bracketed by barrier + synchron
          events on the compute stream, max over ranks.  Every step streams >= 23.6 GB of
          weights (mixing + 2 experts x 32 layers) through HBM, far above the 126 MB L2.
 e2e      the same decode through the public API (OffloadEngine.decode on a host array):
-         H2D of the token's input and D2H of its output inside the timed region.
+         H2D of the token's input and D2H of its output inside the timed region; the timed
+         tokens replayed from the same cold + warm-up cache state (identical misses).
 reference arm (--impl reference): the oracle port of the reference path (numpy fp64 in the
          reference's `h @ W` layout, all host threads) on the same config, per-token time
          sampled on a bounded subset of layers and scaled by L / L_sample.
@@ -54,7 +55,9 @@ def parse_args():
                    help="headline = the first; policy[+prefetch][@cache_size]. Default: configs[1] "
                         "and [2] (LRU, LFU, LFU+prefetch at C=4; LFU, LFU+prefetch at C=2 and 6) "
                         "for 8x7B, configs[4] (LFU+prefetch at C=4) for 8x22B")
-    p.add_argument("--e2e-steps", type=int, default=16)
+    p.add_argument("--e2e-steps", type=int, default=16,
+                   help="tokens replayed through the public API (<= --steps; same stream and "
+                        "starting cache state as the timed region)")
     p.add_argument("--cpu-sample-tokens", type=int, default=16)
     p.add_argument("--cpu-sample-layers", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -460,7 +463,7 @@ def run_ours(args, world, rank, local):
                         if cfg.compress else 1.0)
     # independent request stream per rank: token inputs from the counter hash (f32, std 1)
     base = replicas.rank_token_base(rank)
-    n_tok = args.warmup + args.steps + args.e2e_steps
+    n_tok = args.warmup + args.steps
     inputs = torch.stack([hash_weights(args.seed, tensor_id(5, base + t), 1.0, D, "f32")
                           for t in range(n_tok)])
     stream = torch.cuda.current_stream()
@@ -530,15 +533,19 @@ def run_ours(args, world, rank, local):
                 for t in range(args.steps) for l in range(nl))) == hits,
         }
         if headline and args.e2e_steps > 0:
-            # public API, host buffers: H2D of the input and D2H of the output every step
-            xs = inputs[args.warmup + args.steps:].cpu().numpy()
+            # public API, host buffers: H2D of the input and D2H of the output every step, on the
+            # same token stream from the same (cold + warm-up) cache state as the timed region
+            ne = min(args.e2e_steps, args.steps)
+            xs = inputs[args.warmup: args.warmup + ne].cpu().numpy()
+            eng.reset()
+            eng.decode_device(inputs[: args.warmup])
+            eng.sync()
             torch.cuda.synchronize()
             barrier(world)
             t0 = time.perf_counter()
-            for i in range(args.e2e_steps):
+            for i in range(ne):
                 eng.decode(xs[i: i + 1])
-            e_tps, _, _ = replicas.reduce_timing((time.perf_counter() - t0) * 1e3,
-                                                 args.e2e_steps, world)
+            e_tps, _, _ = replicas.reduce_timing((time.perf_counter() - t0) * 1e3, ne, world)
             e2e = {"value": e_tps, "unit": "tokens/s",
                    "h2d_bytes_per_step": D * 4, "d2h_bytes_per_step": D * 4}
     trace_driven = run_trace_driven(args, eng, inputs, stream, world) if args.trace_variants else None
@@ -613,12 +620,15 @@ def run_ours(args, world, rank, local):
             "achieved_incl_empty_phase_launches": ffn_all_gbs,
             "achieved_in_kernel": (ktimes["ffn_active_bytes"] / (ktimes["ffn_kernel_ms"] / 1e3) / 1e9
                                    if ktimes.get("ffn_kernel_ms") else None),
+            "frac_in_kernel": (ktimes["ffn_active_bytes"] / (ktimes["ffn_kernel_ms"] / 1e3) / 1e9 / hbm_peak
+                               if ktimes.get("ffn_kernel_ms") else None),
             "in_kernel_note": "globaltimer span first CTA start -> last CTA end per launch. The "
                               "CUDA-event span of a single launch is inflated while the copy "
                               "engine runs: tools/dma_event_probe.py times a 235 MB D2D copy "
                               "kernel at 80 us with or without H2D traffic under one event pair "
                               "over 20 launches, but at 105 us with an event pair per launch "
-                              "under H2D traffic (80 us without)",
+                              "under H2D traffic (80 us without). The per-launch events cost "
+                              "the timed decode ~0.8 % (tools/profile_overhead_probe.py)",
             "traffic": traffic.get("dram_bytes_per_expert") if traffic else None,
             "traffic_unit": "DRAM bytes per expert (ncu, profiles/ncu_ffn_traffic.json)",
             "algorithmic_bytes_per_expert": EB,
