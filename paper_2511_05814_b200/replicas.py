@@ -83,6 +83,53 @@ class SharedExpertStore:
                 pass
 
 
+def parse_node_list(text: str) -> list:
+    """'0-1,3' -> [0, 1, 3] (the sysfs node-list format)."""
+    out = []
+    for part in text.strip().split(","):
+        if not part:
+            continue
+        lo, _, hi = part.partition("-")
+        out.extend(range(int(lo), int(hi or lo) + 1))
+    return out
+
+
+def memory_nodes() -> list:
+    try:
+        with open("/sys/devices/system/node/has_memory") as f:
+            return parse_node_list(f.read())
+    except OSError:
+        return []
+
+
+MPOL_INTERLEAVE = 3
+_SYS_MBIND = {"x86_64": 237, "aarch64": 235}
+
+
+def interleave_pages(address: int, nbytes: int, nodes: Optional[list] = None) -> bool:
+    """Spread the (not yet touched) pages of a shared segment round-robin over the host's
+    memory nodes (mbind MPOL_INTERLEAVE): every GPU of the node streams experts from it, so no
+    single socket's DRAM serves all of them.  No-op (False) on a one-node host."""
+    import ctypes
+    import platform
+
+    nodes = memory_nodes() if nodes is None else nodes
+    nr = _SYS_MBIND.get(platform.machine())
+    if len(nodes) < 2 or nr is None or nbytes <= 0:
+        return False
+    maxnode = max(nodes) + 1
+    words = (maxnode + 63) // 64
+    mask = (ctypes.c_ulong * words)()
+    for n in nodes:
+        mask[n // 64] |= 1 << (n % 64)
+    libc = ctypes.CDLL(None, use_errno=True)
+    libc.syscall.restype = ctypes.c_long
+    rc = libc.syscall(ctypes.c_long(nr), ctypes.c_void_p(address), ctypes.c_ulong(nbytes),
+                      ctypes.c_int(MPOL_INTERLEAVE), mask, ctypes.c_ulong(maxnode + 1),
+                      ctypes.c_uint(0))
+    return rc == 0
+
+
 def open_shared_store(name: str, nbytes: int, local_rank: int,
                       barrier: Callable[[], None],
                       fill: Optional[Callable[[SharedExpertStore], None]] = None):
@@ -92,6 +139,7 @@ def open_shared_store(name: str, nbytes: int, local_rank: int,
     """
     if local_rank == 0:
         store = SharedExpertStore.create(name, nbytes)
+        interleave_pages(store.address, store.nbytes)
         if fill is not None:
             fill(store)
         barrier()
@@ -105,6 +153,7 @@ def open_shared_coded(name: str, engine, local_rank: int, barrier: Callable[[], 
     it through its engine; the other ranks attach after the barrier.  Returns the segment."""
     if local_rank == 0:
         seg = SharedExpertStore.create(name, engine.coded_size())
+        interleave_pages(seg.address, seg.nbytes)
         engine.attach_coded(seg, build=True)
         barrier()
         return seg

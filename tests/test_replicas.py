@@ -2,6 +2,7 @@
 N GPUs: disjoint request streams, the max-over-ranks / sum-of-tokens reduction, and the
 node-shared expert store (local rank 0 creates and fills, the other ranks attach)."""
 import os
+import platform
 import socket
 
 import numpy as np
@@ -74,3 +75,21 @@ def test_store_create_replaces_stale_segment():
     s2 = replicas.SharedExpertStore.create(name, 8192)
     assert s2.nbytes >= 8192 and s2.shm.buf[0] == 0
     s2.close()
+
+
+def test_node_list_parsing():
+    assert replicas.parse_node_list("0") == [0]
+    assert replicas.parse_node_list("0-1,3\n") == [0, 1, 3]
+    assert replicas.parse_node_list("") == []
+
+
+def test_interleave_pages_mbind():
+    import mmap
+    import ctypes
+
+    m = mmap.mmap(-1, 1 << 21)
+    addr = ctypes.addressof(ctypes.c_char.from_buffer(m))
+    assert replicas.interleave_pages(addr, 1 << 21, nodes=[0]) is False   # one node: no-op
+    if platform.machine() in ("x86_64", "aarch64"):
+        # the syscall path itself (interleave over node 0 twice is valid on any host)
+        assert replicas.interleave_pages(addr, 1 << 21, nodes=[0, 0]) is True
