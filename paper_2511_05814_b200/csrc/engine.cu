@@ -515,6 +515,26 @@ moe_status build_compressed_store(moe_engine* g) {
 }
 }  // namespace
 
+namespace {
+// <<<grid, block, smem, s>>> with programmatic stream serialization when `pdl` (the kernel may
+// launch while its predecessor runs; every kernel of such a chain pdl_wait()s first)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...);
+}
+}  // namespace
+
 extern "C" {
 
 moe_status moe_engine_create(const moe_engine_config* cfg_in, moe_engine** out) {
@@ -998,6 +1018,8 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
                 "bf16 engine needs hidden_dim and ffn_dim multiples of 256");
   }
   const int grid_mix = stream_grid(1), grid_ffn = stream_grid(K);
+  // SM transfer runs a token as one kernel chain (no copy-event waits): launch it programmatically
+  const bool pdl = g->sm_transfer && !g->no_pdl;
   // one expert-FFN launch group: phase 0 = hits, 1 = misses; only = -1 all, i = i-th miss
   if (g->profiling && !g->prof_bytes_dev)
     MOE_CUDA(cudaMalloc(&g->prof_bytes_dev, 4 * sizeof(long long) * moe_engine::kProfSlots));
@@ -1047,7 +1069,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       MOE_LAUNCHED();
       return MOE_OK;
     }
-    toy_up_kernel<<<dim3(up_grid, K), 256, up_smem, s>>>(fp);
+    MOE_CUDA(launch_k(pdl, toy_up_kernel, dim3(up_grid, K), dim3(256), up_smem, s, fp));
     MOE_LAUNCHED();
     return MOE_OK;
   };
@@ -1071,7 +1093,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       MOE_LAUNCHED();
       return MOE_OK;
     }
-    down_kernel<false><<<dim3(down_grid, K), 256, down_smem, s>>>(fp);
+    MOE_CUDA(launch_k(pdl, down_kernel<false>, dim3(down_grid, K), dim3(256), down_smem, s, fp));
     MOE_LAUNCHED();
     return MOE_OK;
   };
@@ -1119,7 +1141,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
         sp.part = g->gate_part;
         MOE_CUDA(launch_stream<kModeMix>(gmix, grid_mix, sp, s));
       } else {
-        mix_kernel<false><<<mix_grid, 256, mix_smem, s>>>(mp);
+        MOE_CUDA(launch_k(pdl, mix_kernel<false>, dim3(mix_grid), dim3(256), mix_smem, s, mp));
       }
       MOE_LAUNCHED();
       if (g->profiling) MOE_CUDA(cudaEventRecord(pe[1], s));
@@ -1165,7 +1187,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
                           K, g->dstats};
           const long long n16 = g->expert_bytes / 16;
           const int fgrid = static_cast<int>(std::max(1ll, std::min<long long>(296, (K * n16 + 4095) / 4096)));
-          fetch_kernel<<<fgrid, 512, 0, s>>>(fp2);
+          MOE_CUDA(launch_k(pdl, fetch_kernel, dim3(fgrid), dim3(512), 0, s, fp2));
           MOE_LAUNCHED();
         }
         fp.phase = 2;
@@ -1253,8 +1275,10 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       fe = {take_prof_event(g), take_prof_event(g)};
       MOE_CUDA(cudaEventRecord(fe[0], s));
     }
-    finalize_kernel<<<(D + 255) / 256, 256, 0, s>>>(g->h_mid + ((L - 1) & 1) * D, g->y,
-                                                   trec + (L - 1), K, D, dst);
+    MOE_CUDA(launch_k(pdl, finalize_kernel, dim3((D + 255) / 256), dim3(256), 0, s,
+                      static_cast<const float*>(g->h_mid + ((L - 1) & 1) * D),
+                      static_cast<const float*>(g->y), static_cast<const StepRecord*>(trec + (L - 1)),
+                      K, D, dst));
     MOE_LAUNCHED();
     if (g->profiling) {
       MOE_CUDA(cudaEventRecord(fe[1], s));
@@ -1288,8 +1312,9 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       token_begin_kernel<<<1, 256, 0, s>>>(g->cursor, g->x_stage, c.max_tokens, D, g->x_cur);
       MOE_LAUNCHED();
       const moe_status st = run_token(0, 0, true);
-      token_end_kernel<<<1, 256, 0, s>>>(g->cursor, g->cur_rec, g->ring, g->out_cur, g->out_stage,
-                                         c.max_tokens, L, D);
+      MOE_CUDA(launch_k(pdl, token_end_kernel, dim3(1), dim3(256), 0, s, g->cursor,
+                        static_cast<const StepRecord*>(g->cur_rec), g->ring,
+                        static_cast<const float*>(g->out_cur), g->out_stage, static_cast<int>(c.max_tokens), L, D));
       MOE_LAUNCHED();
       cudaGraph_t graph_obj = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(s, &graph_obj);

@@ -199,6 +199,7 @@ struct MixParams {
 template <bool kBF16>
 __global__ void __launch_bounds__(256) mix_kernel(MixParams p) {
   pdl_trigger();  // the gate may launch and stage its cache state meanwhile
+  pdl_wait();     // (SM-transfer graphs launch this programmatically after the down pass)
   extern __shared__ float4 smem4[];
   float4* pa = smem4;
   float4* pb = smem4 + p.d / 8;
@@ -312,6 +313,7 @@ constexpr int kGateThreads = 512;  // d=4096: two float4 columns per thread, loa
 
 template <int EM>  // compile-time bound on E (8 for Mixtral) so the accumulators stay in registers
 __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) {
+  pdl_trigger();  // the FFN pass may launch and wait for the decision meanwhile
   __shared__ float z[3][kMaxE];
   __shared__ float red[2][kGateThreads / 32];
   __shared__ __align__(16) LayerState sS, sS1;   // working copies of this / next layer's state
@@ -641,6 +643,8 @@ struct FetchParams {
 };
 
 static __global__ void __launch_bounds__(512) fetch_kernel(FetchParams p) {
+  pdl_trigger();
+  pdl_wait();
   if (p.rec->flags) return;
   // the step's missed experts as one flat range of 16-byte words, so every PCIe read of the
   // step is in flight together (8 per thread before its stores)
@@ -729,6 +733,8 @@ __device__ __forceinline__ float lane_dot_f32_copy(const float* __restrict__ src
 }
 
 static __global__ void __launch_bounds__(256) toy_up_kernel(FfnParams p) {
+  pdl_trigger();
+  pdl_wait();  // before any early exit: a dependent's wait must cover the whole chain
   const int j = blockIdx.y;
   int e;
   if (!ffn_phase_match(p, j, &e)) return;
@@ -775,6 +781,8 @@ static __global__ void __launch_bounds__(256) toy_up_kernel(FfnParams p) {
 // Down projection: y[j][c] = W[c] . act[j]; W = w2 (SwiGLU, [d][f]) or W2t (toy, [d][d]).
 template <bool kBF16>
 __global__ void __launch_bounds__(256) down_kernel(FfnParams p) {
+  pdl_trigger();
+  pdl_wait();
   const int j = blockIdx.y;
   int e;
   if (!ffn_phase_match(p, j, &e)) return;
@@ -812,6 +820,8 @@ __global__ void __launch_bounds__(256) down_kernel(FfnParams p) {
 // Final layer: h_out = h' + sum_j p_j y_j
 static __global__ void finalize_kernel(const float* h_mid, const float* y, const StepRecord* rec, int K,
                                 int d, float* out) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < d) out[i] = combine_elem(h_mid, y, rec, K, d, i);
 }
@@ -821,6 +831,8 @@ static __global__ void set_cursor_kernel(long long* cursor, long long v) { *curs
 
 static __global__ void token_begin_kernel(const long long* cursor, const float* x_stage, int cap,
                                           int D, float* x_cur) {
+  pdl_trigger();
+  pdl_wait();
   const float* src = x_stage + (*cursor % cap) * D;
   for (int i = threadIdx.x; i < D; i += blockDim.x) x_cur[i] = src[i];
 }
@@ -828,6 +840,7 @@ static __global__ void token_begin_kernel(const long long* cursor, const float* 
 static __global__ void token_end_kernel(long long* cursor, const StepRecord* cur_rec,
                                         StepRecord* ring, const float* out_cur, float* out_stage,
                                         int cap, int L, int D) {
+  pdl_wait();
   const long long row = *cursor % cap;
   copy16(ring + row * L, cur_rec, static_cast<int>(sizeof(StepRecord)) * L, threadIdx.x, blockDim.x);
   for (int i = threadIdx.x; i < D; i += blockDim.x) out_stage[row * D + i] = out_cur[i];
