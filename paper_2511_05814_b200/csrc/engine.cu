@@ -314,6 +314,40 @@ moe_status await_mail(moe_engine* g, long long seq, cudaStream_t compute, MailRe
   return MOE_OK;
 }
 
+cudaEvent_t timeline_event(cudaStream_t s) {
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  return e;
+}
+
+long long host_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void write_timeline(moe_engine* g) {
+  if (!g->timeline_path || g->timeline.empty()) return;
+  cudaDeviceSynchronize();
+  FILE* f = fopen(g->timeline_path, "w");
+  if (f) {
+    fprintf(f, "seq,layer,n_demand,copy_start_ms,copy_end_ms,gate_end_ms,layer_done_ms,host_issue_us\n");
+    auto at = [&](cudaEvent_t e) {
+      float ms = -1.f;
+      if (e) cudaEventElapsedTime(&ms, g->timeline_base, e);
+      return ms;
+    };
+    for (const auto& r : g->timeline)
+      fprintf(f, "%lld,%d,%d,%.4f,%.4f,%.4f,%.4f,%.2f\n", r.seq, r.layer, r.n_demand, at(r.copy0),
+              at(r.copy1), at(r.gate), at(r.done), (r.host_issued_ns - r.host_mail_ns) / 1e3);
+    fclose(f);
+  }
+  for (auto& r : g->timeline)
+    for (cudaEvent_t e : {r.copy0, r.copy1, r.gate, r.done})
+      if (e) cudaEventDestroy(e);
+  g->timeline.clear();
+}
+
 cudaEvent_t take_prof_event(moe_engine* g) {
   if (!g->prof_free.empty()) {
     cudaEvent_t e = g->prof_free.back();
@@ -705,6 +739,7 @@ moe_status moe_engine_destroy(moe_engine* g) {
   if (!g) return MOE_OK;
   cudaSetDevice(g->device);
   cudaDeviceSynchronize();
+  write_timeline(g);
   if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);
   for (auto& e : g->busy_events) {
     cudaEventDestroy(e.first);
@@ -1170,6 +1205,12 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       }
       MOE_LAUNCHED();
       if (g->profiling) MOE_CUDA(cudaEventRecord(pe[2], s));
+      const bool tl = g->timeline_path && !g->sm_transfer && !fixed;
+      moe_engine::TimelineRec trc{};
+      if (tl) {
+        if (!g->timeline_base) g->timeline_base = timeline_event(s);
+        trc.gate = timeline_event(s);
+      }
       FfnParams fp{(c.rms_norm && !g->bf16) ? g->h_norm : hm, trec + l, g->states + l,
                    g->pool + static_cast<long long>(l) * g->NB * g->expert_bytes, g->expert_bytes,
                    D, g->f, K, 0, g->act, g->y, nullptr, nullptr};
@@ -1218,11 +1259,22 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       // forward the device's decision for this step (lockstep, one step behind the GPU)
       MailRecord m;
       TRY(await_mail(g, seq, s, &m));
+      if (tl) {
+        trc.host_mail_ns = host_ns();
+        trc.copy0 = timeline_event(g->copy_stream);
+      }
       if (g->debug)
         fprintf(stderr, "[moe] seq=%lld layer=%d demand=%d cancel=%d prefetch=%d\n", m.seq,
                 m.layer, m.n_demand, m.n_cancel, m.n_prefetch);
       DemandPlan plan;
       TRY(handle_mail(g, m, &plan));
+      if (tl) {
+        trc.host_issued_ns = host_ns();
+        trc.copy1 = timeline_event(g->copy_stream);
+        trc.seq = seq;
+        trc.layer = l;
+        trc.n_demand = m.n_demand;
+      }
       g->next_mail = seq + 1;
       g->ctl_h->consumed = seq + 1;
       // phase 1: each missed expert's up runs once its w1|w3 landed (overlapping its w2
@@ -1266,6 +1318,10 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       if (g->profiling) {
         g->prof_pending.push_back(pe);
         g->prof_pending_k.push_back(K);
+      }
+      if (tl) {
+        trc.done = timeline_event(s);
+        g->timeline.push_back(trc);
       }
     }
     float* out = fixed ? g->out_cur : h_out_dev + t * d;

@@ -200,6 +200,17 @@ struct moe_engine {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> free_events;
   bool debug = getenv("MOE_DEBUG") != nullptr;
   unsigned long long* gate_phase_ns = nullptr;  // MOE_GATE_TIMING: per-phase gate kernel time
+  // MOE_TIMELINE=<csv>: per copy-engine step, copy-stream and compute-stream events plus host
+  // times, written at destroy (diagnostics: where the link idles between steps)
+  struct TimelineRec {
+    long long seq;
+    int layer, n_demand;
+    cudaEvent_t copy0, copy1, gate, done;
+    long long host_mail_ns, host_issued_ns;
+  };
+  const char* timeline_path = getenv("MOE_TIMELINE");
+  std::vector<TimelineRec> timeline;
+  cudaEvent_t timeline_base = nullptr;
   int cap_C = 0;  // policy slots allocated per layer (set_mode may use fewer)
   void* ext_store = nullptr;  // caller-provided expert store (shared between replicas)
   int64_t ext_store_bytes = 0;
