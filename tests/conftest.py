@@ -33,3 +33,24 @@ def golden_streams():
         rb = z["rb"][m_off:m_off + T * E].reshape(T, E)
         ev = z["ev"][m_off:m_off + T * E].reshape(T, E)
         yield int(E), int(K), int(C), int(T), int(code), float(df), int(dp), acts, rb, ev
+
+
+def refsuite_calls():
+    """Every distinct moesim.kernels.replay_policy call of the reference's own test suite,
+    with the reference's outputs (tests/golden/make_refsuite_golden.py):
+    yields (acts (T,K) int64, E, C, policy, decay_factor, decay_period, rb (T,E), ev (T,E))."""
+    z = np.load(GOLDEN / "refsuite_replay.npz")
+    meta, dfs = z["meta"], z["decay_factor"]
+    n_out = int((meta[:, 0] * meta[:, 2]).sum())
+    rb_all = np.unpackbits(z["rb"])[:n_out]
+    ev_all = np.unpackbits(z["ev"])[:n_out]
+    acts_all = z["acts"].astype(np.int64)
+    ia = io = 0
+    for (T, K, E, C, pol, dp), df in zip(meta, dfs):
+        T, K, E = int(T), int(K), int(E)
+        acts = acts_all[ia: ia + T * K].reshape(T, K)
+        rb = rb_all[io: io + T * E].reshape(T, E)
+        ev = ev_all[io: io + T * E].reshape(T, E)
+        ia += T * K
+        io += T * E
+        yield acts, E, int(C), int(pol), float(df), int(dp), rb, ev

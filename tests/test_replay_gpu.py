@@ -198,3 +198,27 @@ def test_simulate_on_gpu_layer_independence_and_compulsory(rng):
         simulate(tr, SimConfig(PolicyKind.lru(), 1))
     with pytest.raises(ConfigError):
         simulate(tr, SimConfig(PolicyKind.lru(), 4, layers=(7,)))
+
+
+def test_reference_suite_replay_calls():
+    """Every distinct replay call of the reference's own test suite (26.5 k, all four policies,
+    the reference's outputs recorded by tests/golden/make_refsuite_golden.py), replayed on the
+    GPU in batches of equal-shaped calls (one warp per call): bit-exact."""
+    from collections import defaultdict
+
+    from conftest import refsuite_calls
+
+    groups = defaultdict(list)
+    for acts, E, C, pol, df, dp, rb, ev in refsuite_calls():
+        groups[(acts.shape, E, C, pol, df, dp)].append((acts, rb, ev))
+    n = 0
+    for ((T, K), E, C, pol, df, dp), items in groups.items():
+        if T == 0:
+            n += len(items)
+            continue
+        acts = np.stack([a for a, _, _ in items])
+        grb, gev = kernels.replay_policy_layers(acts, E, C, pol, df, dp)
+        for i, (_, rb, ev) in enumerate(items):
+            assert np.array_equal(grb[i], rb) and np.array_equal(gev[i], ev), (T, K, E, C, pol, df, dp)
+        n += len(items)
+    assert n > 26000
