@@ -54,3 +54,23 @@ def refsuite_calls():
         ia += T * K
         io += T * E
         yield acts, E, int(C), int(pol), float(df), int(dp), rb, ev
+
+
+def refsuite_run_models():
+    """Every distinct moesim.toymoe.run_model config of the reference's own test suite with the
+    reference's traces (tests/golden/make_refsuite_golden.py): yields
+    ((L, E, K, d, alpha, skew, seed, T), acts (T,L,K), guessed (T,L-1,K), actual (T,L-1,K))."""
+    z = np.load(GOLDEN / "refsuite_run_model.npz")
+    ia = ig = 0
+    for row in z["config"]:
+        L, E, K, d = (int(v) for v in row[:4])
+        alpha, skew = float(row[4]), float(row[5])
+        seed, T = int(row[6]), int(row[7])
+        Ts = T if L >= 2 else 0   # the reference returns empty speculation grids (toymoe.py:187-189)
+        na, ng = T * L * K, Ts * max(L - 1, 0) * K
+        acts = z["acts"][ia: ia + na].astype(np.int64).reshape(T, L, K)
+        guessed = z["guessed"][ig: ig + ng].astype(np.int64).reshape(Ts, max(L - 1, 0), K)
+        actual = z["actual"][ig: ig + ng].astype(np.int64).reshape(Ts, max(L - 1, 0), K)
+        ia += na
+        ig += ng
+        yield (L, E, K, d, alpha, skew, seed, T), acts, guessed, actual

@@ -1,10 +1,13 @@
 """Record every `moesim.kernels.replay_policy` call the reference's own pytest suite makes
 (inputs and the reference's outputs, stock numba backend), deduplicated, as a fixture the GPU
-replay is checked against (tests/test_replay_gpu.py::test_reference_suite_replay_calls).
+replay is checked against (tests/test_replay_gpu.py::test_reference_suite_replay_calls); and
+every distinct `moesim.toymoe.run_model(config)` call with its activation / speculation traces
+(tests/test_toymoe_gpu.py::test_reference_suite_run_model_configs).
 
 Runs only where /root/reference exists (the build container); nothing is written there.
 
-python tests/golden/make_refsuite_golden.py   -> tests/golden/refsuite_replay.npz
+python tests/golden/make_refsuite_golden.py   -> tests/golden/refsuite_replay.npz,
+                                                 tests/golden/refsuite_run_model.npz
 """
 import hashlib
 import os
@@ -16,6 +19,7 @@ import numpy as np
 
 REF = Path("/root/reference/pkg")
 OUT = Path(__file__).resolve().parent / "refsuite_replay.npz"
+OUT_RM = Path(__file__).resolve().parent / "refsuite_run_model.npz"
 
 
 def main():
@@ -25,6 +29,7 @@ def main():
     import pytest
 
     seen, calls = set(), []
+    rm_seen, rm_calls = set(), []
 
     class Record:
         def pytest_configure(self, config):
@@ -44,6 +49,22 @@ def main():
                 return rb, ev
 
             k.replay_policy = replay
+            import moesim.toymoe as tm
+
+            stock_rm = tm.run_model
+
+            def run_model(cfg):
+                act, spec = stock_rm(cfg)
+                sh = cfg.shape
+                key = (sh.num_layers, sh.num_experts, sh.top_k, cfg.hidden_dim,
+                       float(cfg.mixing_scale), float(cfg.skew), cfg.seed, cfg.tokens)
+                if key not in rm_seen:
+                    rm_seen.add(key)
+                    rm_calls.append((key, np.asarray(act.activations, np.int64),
+                                     np.asarray(spec.guessed, np.int64), np.asarray(spec.actual, np.int64)))
+                return act, spec
+
+            tm.run_model = run_model
 
     rc = pytest.main([str(REF / "tests"), "-q", "-p", "no:cacheprovider",
                       "--rootdir", tempfile.mkdtemp(prefix="refsuite_")], plugins=[Record()])
@@ -56,6 +77,12 @@ def main():
     np.savez_compressed(OUT, meta=meta, decay_factor=dfs, acts=acts, rb=rb, ev=ev)
     print(f"pytest rc={rc}; {len(calls)} distinct replay calls -> {OUT} "
           f"({OUT.stat().st_size / 1e6:.2f} MB)")
+    keys = np.array([k for k, *_ in rm_calls], np.float64)   # L, E, K, d, alpha, skew, seed, T
+    np.savez_compressed(OUT_RM, config=keys,
+                        acts=np.concatenate([a.reshape(-1) for _, a, _, _ in rm_calls]).astype(np.int16),
+                        guessed=np.concatenate([g.reshape(-1) for _, _, g, _ in rm_calls]).astype(np.int16),
+                        actual=np.concatenate([x.reshape(-1) for *_, x in rm_calls]).astype(np.int16))
+    print(f"{len(rm_calls)} distinct run_model configs -> {OUT_RM}")
 
 
 if __name__ == "__main__":

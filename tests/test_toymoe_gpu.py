@@ -195,3 +195,21 @@ def test_engine_config_errors():
     with pytest.raises(ConfigError):
         OffloadEngine(EngineConfig(num_layers=2, num_experts=8, top_k=2, hidden_dim=8,
                                    expert_kind="toy_tanh", cache_size=2, policy=PolicyKind.opt()))
+
+
+def test_reference_suite_run_model_configs():
+    """Every distinct run_model config the reference's own test suite uses (100: mixing scales
+    0.1 .. 100, skew 0 / 1, 1-6 layers, up to 64 tokens), through the GPU engine: activation and
+    speculation traces identical to the reference's."""
+    from conftest import refsuite_run_models
+
+    n = 0
+    for (L, E, K, d, alpha, skew, seed, T), acts, guessed, actual in refsuite_run_models():
+        cfg = ToyModelConfig(ModelShape(L, E, K), hidden_dim=d, mixing_scale=alpha, skew=skew,
+                             seed=seed, tokens=T)
+        a, s = run_model(cfg)
+        key = (L, E, K, d, alpha, skew, seed, T)
+        assert np.array_equal(a.activations, acts), key
+        assert np.array_equal(s.guessed, guessed) and np.array_equal(s.actual, actual), key
+        n += 1
+    assert n == 100
