@@ -1,0 +1,68 @@
+"""Run test files of the reference's own pytest suite against THIS package's drop-in modules
+(build container only: reads /root/reference, writes nothing there).
+
+`moesim` and its hot-path submodules are aliased to `paper_2511_05814_b200`'s (traces, metrics,
+costmodel, simulate, policies, kernels, errors), so the reference's tests exercise our host
+code: trace / event-log objects and byte-exact JSONL (native formatter), metrics, cost model,
+simulate's validation and layer loop.  There is no GPU here, so the one device seam on these
+paths -- the policy replay behind simulate -- is served by the C oracle (itself pinned by the
+reference's suite, oracle/run_reference_suite.py); the GPU replay is pinned on the B200 by
+tests/test_replay_gpu.py::test_reference_suite_replay_calls.
+
+python tests/refsuite_on_package.py [test files...] [pytest args]
+"""
+import os
+import sys
+import tempfile
+from pathlib import Path
+
+REF = Path("/root/reference/pkg")
+ROOT = Path(__file__).resolve().parents[1]
+DEFAULT = ["test_traces.py", "test_metrics.py", "test_costmodel.py", "test_simulate.py"]
+ALIASED = ["traces", "metrics", "costmodel", "simulate", "policies", "kernels", "errors"]
+
+
+def install_aliases():
+    import importlib
+
+    import numpy as np
+
+    pkg = importlib.import_module("paper_2511_05814_b200")
+    sys.modules["moesim"] = pkg
+    for name in ALIASED:
+        sys.modules[f"moesim.{name}"] = importlib.import_module(f"paper_2511_05814_b200.{name}")
+    import oracle
+    from paper_2511_05814_b200 import kernels
+
+    def replay_layers_host(acts, num_experts, capacity, policy, decay_factor, decay_period):
+        a = np.ascontiguousarray(acts, dtype=np.int64)
+        L, T, _ = a.shape
+        rb = np.zeros((L, T, num_experts), np.uint8)
+        ev = np.zeros_like(rb)
+        for layer in range(L):
+            rb[layer], ev[layer] = oracle.replay_policy(a[layer], num_experts, capacity, policy,
+                                                        decay_factor, decay_period)
+        return rb, ev
+
+    kernels.replay_policy_layers = replay_layers_host
+
+
+def main(argv):
+    if not REF.exists():
+        print("reference not present: nothing to run")
+        return 0
+    os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="numba_"))
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, str(ROOT))
+    files = [a for a in argv if a.endswith(".py")] or DEFAULT
+    rest = [a for a in argv if not a.endswith(".py")]
+    import pytest
+
+    install_aliases()   # before the reference's conftest imports moesim
+    args = [str(REF / "tests" / f) for f in files] + ["-q", "-p", "no:cacheprovider",
+                                                      "--rootdir", tempfile.mkdtemp(prefix="refpkg_")]
+    return pytest.main(args + rest)
+
+
+if __name__ == "__main__":
+    sys.exit(main(sys.argv[1:]))
