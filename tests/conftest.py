@@ -74,3 +74,29 @@ def refsuite_run_models():
         ia += na
         ig += ng
         yield (L, E, K, d, alpha, skew, seed, T), acts, guessed, actual
+
+
+def refsuite_policy_steps():
+    """Every distinct moesim.policies.policy_step call of the reference's suite, with the
+    reference's result (state + outcome) or the name of the error it raised."""
+    import gzip
+    import json
+
+    with gzip.open(GOLDEN / "refsuite_policy_step.jsonl.gz", "rt") as f:
+        for line in f:
+            yield json.loads(line)
+
+
+def refsuite_tracegen_calls():
+    """Every distinct gen_zipf / gen_markov call of the reference's suite with its trace:
+    yields (meta dict, acts (T, L, K))."""
+    z = np.load(GOLDEN / "refsuite_tracegen.npz")
+    i = 0
+    for m in z["meta"]:
+        kind, L, E, K, T = (int(v) for v in m[:5])
+        meta = dict(kind="zipf" if kind == 0 else "markov", L=L, E=E, K=K, T=T, skew=float(m[5]),
+                    per_layer_permutation=bool(int(m[6])), seed=int(m[7]), repeat_prob=float(m[8]),
+                    base_tokens=int(m[10]), base_seed=int(m[11]))
+        n = T * L * K
+        yield meta, z["acts"][i: i + n].astype(np.int64).reshape(T, L, K)
+        i += n

@@ -2,14 +2,21 @@
 (inputs and the reference's outputs, stock numba backend), deduplicated, as a fixture the GPU
 replay is checked against (tests/test_replay_gpu.py::test_reference_suite_replay_calls); and
 every distinct `moesim.toymoe.run_model(config)` call with its activation / speculation traces
-(tests/test_toymoe_gpu.py::test_reference_suite_run_model_configs).
+(tests/test_toymoe_gpu.py::test_reference_suite_run_model_configs); every distinct
+`moesim.policies.policy_step` call with its result or error (tests/test_replay_gpu.py::
+test_reference_suite_policy_steps); every distinct `gen_zipf` / `gen_markov` call with its trace
+(tests/test_tracegen.py::test_reference_suite_tracegen_calls).
 
 Runs only where /root/reference exists (the build container); nothing is written there.
 
 python tests/golden/make_refsuite_golden.py   -> tests/golden/refsuite_replay.npz,
-                                                 tests/golden/refsuite_run_model.npz
+                                                 tests/golden/refsuite_run_model.npz,
+                                                 tests/golden/refsuite_policy_step.jsonl.gz,
+                                                 tests/golden/refsuite_tracegen.npz
 """
+import gzip
 import hashlib
+import json
 import os
 import sys
 import tempfile
@@ -20,6 +27,14 @@ import numpy as np
 REF = Path("/root/reference/pkg")
 OUT = Path(__file__).resolve().parent / "refsuite_replay.npz"
 OUT_RM = Path(__file__).resolve().parent / "refsuite_run_model.npz"
+OUT_PS = Path(__file__).resolve().parent / "refsuite_policy_step.jsonl.gz"
+OUT_TG = Path(__file__).resolve().parent / "refsuite_tracegen.npz"
+
+
+def _state(st):
+    return {"capacity": st.capacity, "resident": sorted(int(e) for e in st.resident),
+            "recency": [int(e) for e in st.recency],
+            "freq": sorted([int(e), float(f)] for e, f in st.freq.items()), "step": int(st.step)}
 
 
 def main():
@@ -30,6 +45,8 @@ def main():
 
     seen, calls = set(), []
     rm_seen, rm_calls = set(), []
+    ps_seen, ps_calls = set(), []
+    tg_seen, tg_calls = set(), []
 
     class Record:
         def pytest_configure(self, config):
@@ -65,6 +82,58 @@ def main():
                 return act, spec
 
             tm.run_model = run_model
+            import moesim.policies as pm
+
+            stock_ps = pm.policy_step
+
+            def policy_step(state, kind, activated, future=None):
+                rec = {"state": _state(state), "kind": str(kind), "activated": [int(e) for e in activated],
+                       "future": None if future is None else [sorted(int(e) for e in f) for f in future]}
+                try:
+                    st2, out = stock_ps(state, kind, activated, future)
+                    rec["result"] = {"state": _state(st2), **{
+                        k: sorted(int(e) for e in getattr(out, k))
+                        for k in ("hits", "misses", "evicted", "loaded", "resident_before", "resident_after")}}
+                except Exception as exc:  # the reference's validation errors are part of the contract
+                    rec["error"] = type(exc).__name__
+                    st2 = out = None
+                key = json.dumps(rec, sort_keys=True)
+                if key not in ps_seen:
+                    ps_seen.add(key)
+                    ps_calls.append(rec)
+                if st2 is None:
+                    raise exc_of(rec["error"])
+                return st2, out
+
+            def exc_of(name):
+                from moesim import errors
+
+                return getattr(errors, name, ValueError)("recorded")
+
+            pm.policy_step = policy_step
+            import moesim.tracegen as tg
+
+            for fname in ("gen_zipf", "gen_markov"):
+                stock_g = getattr(tg, fname)
+
+                def gen(params, _stock=stock_g, _name=fname):
+                    tr = _stock(params)
+                    sh = params.shape
+                    if _name == "gen_zipf":
+                        meta = (0, sh.num_layers, sh.num_experts, sh.top_k, params.num_tokens,
+                                float(params.skew_exponent), int(params.per_layer_permutation),
+                                params.seed, 0.0, 0.0, 1, 0)
+                    else:
+                        b = params.base
+                        meta = (1, sh.num_layers, sh.num_experts, sh.top_k, params.num_tokens,
+                                float(b.skew_exponent), int(b.per_layer_permutation), params.seed,
+                                float(params.repeat_prob), 0.0, b.num_tokens, b.seed)
+                    if meta not in tg_seen:
+                        tg_seen.add(meta)
+                        tg_calls.append((meta, np.asarray(tr.activations, np.int64)))
+                    return tr
+
+                setattr(tg, fname, gen)
 
     rc = pytest.main([str(REF / "tests"), "-q", "-p", "no:cacheprovider",
                       "--rootdir", tempfile.mkdtemp(prefix="refsuite_")], plugins=[Record()])
@@ -83,6 +152,13 @@ def main():
                         guessed=np.concatenate([g.reshape(-1) for _, _, g, _ in rm_calls]).astype(np.int16),
                         actual=np.concatenate([x.reshape(-1) for *_, x in rm_calls]).astype(np.int16))
     print(f"{len(rm_calls)} distinct run_model configs -> {OUT_RM}")
+    with open(OUT_PS, "wb") as raw, gzip.GzipFile(fileobj=raw, mode="wb", mtime=0) as f:
+        for rec in ps_calls:
+            f.write((json.dumps(rec, sort_keys=True) + "\n").encode())
+    print(f"{len(ps_calls)} distinct policy_step calls -> {OUT_PS} ({OUT_PS.stat().st_size / 1e6:.2f} MB)")
+    np.savez_compressed(OUT_TG, meta=np.array([m for m, _ in tg_calls], np.float64),
+                        acts=np.concatenate([a.reshape(-1) for _, a in tg_calls]).astype(np.int16))
+    print(f"{len(tg_calls)} distinct tracegen calls -> {OUT_TG} ({OUT_TG.stat().st_size / 1e6:.2f} MB)")
 
 
 if __name__ == "__main__":

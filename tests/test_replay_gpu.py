@@ -222,3 +222,34 @@ def test_reference_suite_replay_calls():
             assert np.array_equal(grb[i], rb) and np.array_equal(gev[i], ev), (T, K, E, C, pol, df, dp)
         n += len(items)
     assert n > 26000
+
+
+def test_reference_suite_policy_steps():
+    """Every distinct policy_step call of the reference's own test suite (5,084: all four
+    policies, KATs, validation errors), through the GPU step: identical state, outcome sets,
+    and the same error class where the reference raised one."""
+    from conftest import refsuite_policy_steps
+
+    from paper_2511_05814_b200 import errors
+
+    n = 0
+    for rec in refsuite_policy_steps():
+        s = rec["state"]
+        st = CacheState(capacity=s["capacity"], resident=frozenset(s["resident"]),
+                        recency=tuple(s["recency"]), freq={e: f for e, f in s["freq"]}, step=s["step"])
+        fut = None if rec["future"] is None else [frozenset(f) for f in rec["future"]]
+        kind = PolicyKind.parse(rec["kind"])
+        if "error" in rec:
+            with pytest.raises(getattr(errors, rec["error"], Exception)):
+                policy_step(st, kind, rec["activated"], fut)
+        else:
+            st2, out = policy_step(st, kind, rec["activated"], fut)
+            r = rec["result"]
+            assert st2.capacity == r["state"]["capacity"] and st2.step == r["state"]["step"], rec
+            assert sorted(st2.resident) == r["state"]["resident"], rec
+            assert list(st2.recency) == r["state"]["recency"], rec
+            assert sorted([e, f] for e, f in st2.freq.items()) == r["state"]["freq"], rec
+            for k in ("hits", "misses", "evicted", "loaded", "resident_before", "resident_after"):
+                assert sorted(getattr(out, k)) == r[k], (k, rec)
+        n += 1
+    assert n > 5000
