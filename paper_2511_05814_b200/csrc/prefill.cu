@@ -319,6 +319,7 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
     pp.K = K;
     pp.C = c.cache_size;
     pp.NB = c.cache_size + (c.prefetch ? g->S : 0);
+    pp.pool_nb = g->NB;  // set_mode may run fewer buffers than allocated
     pp.policy = c.policy;
     pp.decay_factor = c.decay_factor;
     pp.decay_period = c.decay_period;

@@ -209,6 +209,7 @@ struct PfPlanParams {
   StepRecord* ring;
   long long tok0;
   int max_tokens, L, layer, T, E, K, C, NB, policy;
+  int pool_nb;         // buffers allocated per layer (the pool's layer stride) >= NB in use
   double decay_factor;
   long long decay_period;
   LayerState* state;
@@ -525,11 +526,11 @@ __global__ void __launch_bounds__(256) pf_plan_kernel(PfPlanParams p) {
     int b_map = 0;
     long long buf_index;
     if (tid < nres) {
-      buf_index = static_cast<long long>(p.layer) * p.NB + buf_before[e];
+      buf_index = static_cast<long long>(p.layer) * p.pool_nb + buf_before[e];
     } else {
       const int dst = M.load_dst[tid - nres];
       if (dst >= 0) {
-        buf_index = static_cast<long long>(p.layer) * p.NB + dst;
+        buf_index = static_cast<long long>(p.layer) * p.pool_nb + dst;
       } else {
         b_map = 1;
         buf_index = e;

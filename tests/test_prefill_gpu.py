@@ -222,3 +222,51 @@ def test_prefill_single_token_and_nonfinite():
     ref_out, ref_acts = ref_for(cfg, 9).decode(X[:1])
     assert np.array_equal(rec["acts"], ref_acts)
     assert np.abs(out1 - ref_out).max() / np.abs(ref_out).max() < 1e-2
+
+
+@pytest.mark.parametrize("compress", [0, 1])
+def test_prefill_is_deterministic_across_runs(compress):
+    """The same tokens prefilled from a cold cache three times on one engine -- fresh, after a
+    reset, after decode traffic in another mode -- give identical records and outputs."""
+    cfg = small_cfg(cache_size=6, policy=PolicyKind.lru(), prefetch="early", compress=compress)
+    T = 200
+    X = oracle.MixtralRef.inputs(11, T, cfg.hidden_dim)
+    runs = []
+    with OffloadEngine(cfg) as eng:
+        eng.init_random(11)
+        for r in range(3):
+            eng.set_mode(policy=PolicyKind.lru(), cache_size=4, prefetch="off")
+            t0 = eng.tokens_done
+            out = eng.prefill(X)
+            runs.append((eng.records(t0, T), out))
+            if r == 1:
+                eng.set_mode(policy=PolicyKind.lfu(), cache_size=6, prefetch="early")
+                eng.decode(X[:16])
+    for rec, out in runs[1:]:
+        for k in ("acts", "resident_before", "evicted", "guessed"):
+            assert np.array_equal(rec[k], runs[0][0][k]), k
+        assert np.array_equal(out, runs[0][1])
+
+
+@pytest.mark.parametrize("compress", [0, 1])
+def test_prefill_in_a_smaller_mode_than_allocated_matches_oracle(compress):
+    """An engine allocated for C=6 + prefetch staging, switched (set_mode) to LRU C=4 without
+    prefetch -- the bench's configs[3] setup -- prefills against the oracle like a C=4 engine
+    (the pool keeps its allocated layer stride)."""
+    cfg = small_cfg(cache_size=6, policy=PolicyKind.lru(), prefetch="early", compress=compress)
+    T = 160
+    X = oracle.MixtralRef.inputs(21, T, cfg.hidden_dim)
+    with OffloadEngine(cfg) as eng:
+        eng.init_random(21)
+        eng.set_mode(policy=PolicyKind.lfu(), cache_size=6, prefetch="early")
+        eng.decode(X[:24])                   # fills every buffer of the allocation
+        eng.set_mode(policy=PolicyKind.lru(), cache_size=4, prefetch="off")
+        t0 = eng.tokens_done
+        out = eng.prefill(X)
+        rec = eng.records(t0, T)
+    ref_cfg = small_cfg(cache_size=4, policy=PolicyKind.lru())
+    ref_out, ref_acts, _, gaps = oracle.mixtral_prefill(ref_for(ref_cfg, 21), X, return_gaps=True)
+    diff = _check_selections(rec["acts"], ref_acts, gaps)
+    ok = ~diff.any(axis=1)
+    assert np.abs(out[ok] - ref_out[ok]).max() / np.abs(ref_out[ok]).max() < 1e-2
+    _check_trace(ref_cfg, rec)
