@@ -194,11 +194,6 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot) {
   return before;
 }
 
-__device__ __forceinline__ uint32_t get3(uint64_t lo, uint64_t hi, int p) {
-  const uint64_t v = p >= 64 ? hi >> (p - 64) : (p == 0 ? lo : (lo >> p) | (hi << (64 - p)));
-  return static_cast<uint32_t>(v & 7u);
-}
-
 __device__ __forceinline__ void store_out(uint16_t* out, uint64_t first, int cnt, const uint32_t (&o)[16]) {
   if (cnt == 32) {
     uint4* op = reinterpret_cast<uint4*>(out + first);
@@ -217,7 +212,25 @@ __device__ __forceinline__ uint32_t bf16_word(uint32_t b8, uint32_t ex) {
   return ((b8 & 0x80u) << 8) | ((ex & 0xFFu) << 7) | (b8 & 0x7Fu);
 }
 
+// bf16 words of 4 weights from their sign+mantissa bytes B and exponent bytes X, packed in
+// 32-bit words, as two 32-bit output words (weights 0,1 and 2,3): per byte, the high half
+// is sign | ex >> 1, the low half ex & 1 | mantissa; byte permutes interleave them.
+__device__ __forceinline__ void bf16x4(uint32_t B, uint32_t X, uint32_t& o01, uint32_t& o23) {
+  const uint32_t H = (B & 0x80808080u) | ((X >> 1) & 0x7F7F7F7Fu);
+  const uint32_t L = (B & 0x7F7F7F7Fu) | ((X << 7) & 0x80808080u);
+  o01 = __byte_perm(L, H, 0x5140);
+  o23 = __byte_perm(L, H, 0x7362);
+}
+
+// four 2-bit codes (one code byte) spread to the low bits of four bytes
+__device__ __forceinline__ uint32_t spread2(uint32_t cb) {
+  uint32_t s = (cb | (cb << 12)) & 0x000F000Fu;
+  return (s | (s << 6)) & 0x03030303u;
+}
+
 // One CTA per chunk, 32 consecutive weights per thread; escapes ranked by block scans.
+// Mode 23 decodes four weights per step in byte lanes (the exponents of a code byte by one
+// subtraction, the bf16 words by byte permutes) and patches the level-1 escapes in place.
 template <int K>
 __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restrict__ part,
                                                           uint16_t* __restrict__ out) {
@@ -230,7 +243,8 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
   const int cnt = active ? static_cast<int>(h.n - first < 32 ? h.n - first : 32) : 0;
   uint32_t lo[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   uint64_t c0 = 0, c1 = 0;  // K-bit codes 0..15 / 16..31 (mode 23: all 32 2-bit codes in c0)
-  uint32_t escm = 0;
+  uint32_t escm = 0;        // modes 3 / 4: bit j = weight j escapes to a byte
+  uint64_t zm = 0;          // mode 23: bit 2j = weight j escapes to level 2
   if (active) {
     const uint4* lp = reinterpret_cast<const uint4*>(part + h.low_off + first);
     const uint4 l0 = lp[0], l1 = lp[1];
@@ -239,9 +253,8 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
     if constexpr (K == kMode23) {
       const uint2 q = *reinterpret_cast<const uint2*>(part + h.code_off + first / 4);
       c0 = (static_cast<uint64_t>(q.y) << 32) | q.x;
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < cnt && !((c0 >> (2 * j)) & 3u)) escm |= 1u << j;
+      zm = ~(c0 | (c0 >> 1)) & 0x5555555555555555ull;
+      if (cnt < 32) zm &= (1ull << (2 * cnt)) - 1ull;
     } else if constexpr (K == 4) {
       const uint4 q = *reinterpret_cast<const uint4*>(part + h.code_off + first / 2);
       c0 = (static_cast<uint64_t>(q.y) << 32) | q.x;
@@ -260,46 +273,71 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
       }
     }
   }
-  const int n1 = __popc(escm);
+  const int n1 = K == kMode23 ? __popcll(zm) : __popc(escm);
   const int before1 = block_exclusive_scan(n1, warp_tot);
   uint32_t o[16];
   if constexpr (K == kMode23) {
-    // level-2 codes of this thread: n1 consecutive 3-bit codes from index l2_off + before1
+    // level-2 codes of this thread: n1 consecutive 3-bit codes from index l2_off + before1,
+    // held in a 128-bit shift register (r0 low)
     const uint64_t bit = (static_cast<uint64_t>(ce.l2_off) + before1) * 3;
     const uint32_t* wp = reinterpret_cast<const uint32_t*>(part + h.l2_off) + (bit >> 5);
-    uint64_t wlo = 0, whi = 0;
-    const int sh = static_cast<int>(bit & 31);
+    uint64_t r0 = 0, r1 = 0;
     if (n1) {
-      wlo = (static_cast<uint64_t>(wp[1]) << 32) | wp[0];
-      whi = (static_cast<uint64_t>(wp[3]) << 32) | wp[2];
+      const uint64_t wlo = (static_cast<uint64_t>(wp[1]) << 32) | wp[0];
+      const uint64_t whi = (static_cast<uint64_t>(wp[3]) << 32) | wp[2];
+      const int sh = static_cast<int>(bit & 31);
+      r0 = sh ? (wlo >> sh) | (whi << (64 - sh)) : wlo;
+      r1 = whi >> sh;
     }
+    // byte escapes = zero 3-bit fields among the first n1 (fields 0..20 in r0, 21.. after it)
     int n2 = 0;
-    for (int k = 0; k < n1; ++k) n2 += get3(wlo, whi, sh + 3 * k) == 0u;
+    if (n1) {
+      constexpr uint64_t kField = 0x1249249249249249ull;  // bit 3i, i = 0..20
+      const int f0 = n1 < 21 ? n1 : 21, f1 = n1 - f0;
+      const uint64_t a = r0, b = (r0 >> 63) | (r1 << 1);
+      const uint64_t m0 = f0 == 21 ? kField : kField & ((1ull << (3 * f0)) - 1ull);
+      const uint64_t m1 = f1 <= 0 ? 0ull : kField & ((1ull << (3 * f1)) - 1ull);
+      n2 = __popcll(~(a | (a >> 1) | (a >> 2)) & m0) + __popcll(~(b | (b >> 1) | (b >> 2)) & m1);
+    }
     const int before2 = block_exclusive_scan(n2, warp_tot);
     if (!active) return;
     const uint8_t* esc = part + h.esc_off + ce.esc_off + before2;
-    const uint32_t win = ce.win;
-    int k = 0, e = 0;
+    const uint32_t win = ce.win, base = ce.base, w2 = win > 2u ? win - 2u : 0u;
+    const uint32_t E0x4 = (base + 1u - win) * 0x01010101u;
+    // exponent bytes of the thread's 32 weights in shared memory ([group][thread] words, so
+    // the word accesses are conflict-free), escapes patched byte-wise, then the bf16 words
+    __shared__ uint32_t xs[8 * kThreads];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const uint32_t b8 = (lo[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-      const uint32_t cc = static_cast<uint32_t>((c0 >> (2 * j)) & 3u);
-      uint32_t ex = static_cast<uint32_t>(ce.base) + 1u - cc - win;
-      if ((escm >> j) & 1u) {
-        const uint32_t c2 = get3(wlo, whi, sh + 3 * k);
-        ++k;
-        if (c2) {
-          const uint32_t r = c2 - 1u + (win > 2u ? win - 2u : 0u);
-          ex = static_cast<uint32_t>(ce.base) - (r < win ? r : r + 3u);
-        } else {
-          ex = esc[e];
-          ++e;
-        }
+    for (int g = 0; g < 8; ++g)
+      xs[g * kThreads + threadIdx.x] = E0x4 - spread2(static_cast<uint32_t>(c0 >> (8 * g)) & 0xFFu);
+    uint8_t* xb = reinterpret_cast<uint8_t*>(xs) + threadIdx.x * 4;
+    // escape positions as a 32-bit mask (even bits of zm gathered)
+    uint64_t x = zm;
+    x = (x | (x >> 1)) & 0x3333333333333333ull;
+    x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
+    uint32_t em = static_cast<uint32_t>(x | (x >> 16));
+    uint32_t q0 = static_cast<uint32_t>(r0), q1 = static_cast<uint32_t>(r0 >> 32),
+             q2 = static_cast<uint32_t>(r1), q3 = static_cast<uint32_t>(r1 >> 32);
+    for (; em; em &= em - 1u) {
+      const int j = __ffs(em) - 1;
+      const uint32_t c2 = q0 & 7u;
+      q0 = __funnelshift_r(q0, q1, 3);
+      q1 = __funnelshift_r(q1, q2, 3);
+      q2 = __funnelshift_r(q2, q3, 3);
+      q3 >>= 3;
+      uint32_t ex;
+      if (c2) {
+        const uint32_t r = c2 - 1u + w2;
+        ex = base - (r < win ? r : r + 3u);
+      } else {
+        ex = *esc++;
       }
-      const uint32_t w = bf16_word(b8, ex);
-      if (j & 1) o[j >> 1] |= w << 16;
-      else o[j >> 1] = w;
+      xb[(j >> 2) * kThreads * 4 + (j & 3)] = static_cast<uint8_t>(ex);
     }
+#pragma unroll
+    for (int g = 0; g < 8; ++g) bf16x4(lo[g], xs[g * kThreads + threadIdx.x], o[2 * g], o[2 * g + 1]);
   } else {
     if (!active) return;
     const uint8_t* esc = part + h.esc_off + ce.esc_off + before1;
