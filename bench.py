@@ -278,10 +278,12 @@ def committed_ffn_traffic():
 # ---- CPU path (oracle port of the reference, test-infrastructure only) -------------------
 
 def cpu_reference_sample(seed: int, tokens: int, layers: int, warmup: int = 1,
-                         shape=(L, E, K, D, F)) -> dict:
-    """Time the oracle port (numpy fp64, reference `h @ W` layout, all host threads) on the
-    first `tokens` tokens of the same stream through `layers` layers; return tokens/s scaled
-    to the full model depth.  Weights are materialised (untimed) by a first pass."""
+                         shape=(L, E, K, D, F), layout: str = "ref") -> dict:
+    """Time the oracle port on the first `tokens` tokens of the same stream through `layers`
+    layers; return tokens/s scaled to the full model depth.  layout "ref": the reference's
+    arithmetic (numpy fp64, `h @ W`, BASELINE.md variant (i)); "dev": the tuned variant (ii),
+    fp32 `W h` GEMVs in the weights' row-major (nn.Linear) layout.  All host BLAS threads.
+    Weights are materialised (untimed) by a first pass."""
     import numpy as np
 
     import oracle
@@ -289,7 +291,7 @@ def cpu_reference_sample(seed: int, tokens: int, layers: int, warmup: int = 1,
 
     L, E, K, D, F = shape
     alpha = 0.1 * math.sqrt(16 / D)
-    ref = oracle.MixtralRef(L, E, K, D, F, alpha, seed=seed, layout="ref",
+    ref = oracle.MixtralRef(L, E, K, D, F, alpha, seed=seed, layout=layout,
                             layers=list(range(layers)), rms_norm=True)
     X = oracle.MixtralRef.inputs(seed, tokens + warmup, D)
     t_gen = time.perf_counter()
@@ -302,8 +304,9 @@ def cpu_reference_sample(seed: int, tokens: int, layers: int, warmup: int = 1,
     per_token = dt / tokens * (L / layers)
     return {"value": 1.0 / per_token, "unit": "tokens/s", "cores": os.cpu_count(),
             "kind": "port",
-            "sample": f"{tokens} tokens x {layers} of {L} layers (numpy fp64 `h @ W`, "
-                      f"{os.cpu_count()} BLAS threads), scaled by {L}/{layers}; "
+            "sample": f"{tokens} tokens x {layers} of {L} layers ("
+                      + ("numpy fp64 `h @ W`" if layout == "ref" else "numpy fp32 `W h`, row-major weights")
+                      + f", {os.cpu_count()} BLAS threads), scaled by {L}/{layers}; "
                       f"{dt:.1f} s timed, {t_gen:.1f} s untimed weight materialisation",
             "seconds_timed": dt}
 
@@ -423,14 +426,15 @@ def run_ours(args, world, rank, local):
                   max_tokens=4096, device=gpu, store_layers=store_layers,
                   prefetch_buffers=pf_bufs, compress=compress)
     D, F, EB = cfg.hidden_dim, cfg.ffn_dim, cfg.expert_bytes
-    cpu = None
+    cpu = cpu32 = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        if args.model == "mixtral_8x7b":
-            cpu = cpu_reference_sample(args.seed, args.cpu_sample_tokens, args.cpu_sample_layers)
-        else:  # configs[4]: a bounded sample (fp64 8x22B experts are 2.4 GB each)
-            cpu = cpu_reference_sample(args.seed, 16, 1, shape=(base_cfg.num_layers, base_cfg.num_experts,
-                                                              base_cfg.top_k, base_cfg.hidden_dim,
-                                                              base_cfg.ffn_dim))
+        shape = (base_cfg.num_layers, base_cfg.num_experts, base_cfg.top_k, base_cfg.hidden_dim,
+                 base_cfg.ffn_dim)
+        # (i) the reference's arithmetic (the baseline); (ii) a tuned fp32 port beside it
+        # (report both).  configs[4] is bounded to 16 tokens (2.4 GB fp64 experts)
+        ntok = args.cpu_sample_tokens if args.model == "mixtral_8x7b" else 16
+        cpu = cpu_reference_sample(args.seed, ntok, args.cpu_sample_layers, shape=shape)
+        cpu32 = cpu_reference_sample(args.seed, ntok, args.cpu_sample_layers, shape=shape, layout="dev")
     pcie_peak = h2d_peak_gbs(dev)
 
     t_setup = time.perf_counter()
@@ -643,6 +647,9 @@ def run_ours(args, world, rank, local):
     }
     if cpu:
         line["speedup_vs_cpu_port"] = head["tokens_per_s"] / cpu["value"]
+    if cpu32:
+        line["cpu_baseline_fp32"] = cpu32
+        line["speedup_vs_cpu_port_fp32"] = head["tokens_per_s"] / cpu32["value"]
     if trace_driven:
         line["trace_driven"] = trace_driven
     if tiny:
