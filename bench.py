@@ -823,6 +823,7 @@ def run_prefill(args, eng, inputs, base, stream, world, pcie_peak):
     }
     if not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_prefill_sample(args.seed, P, X)
+        out["cpu_baseline_fp32"] = cpu_prefill_sample(args.seed, P, X, layout="dev")
     if args.prefill_decode > 0:
         xs = torch.stack([hash_weights(args.seed, tensor_id(5, base + 200000 + t), 1.0, Dd, "f32")
                           for t in range(args.prefill_decode)])
@@ -841,27 +842,33 @@ def run_prefill(args, eng, inputs, base, stream, world, pcie_peak):
     return out
 
 
-def cpu_prefill_sample(seed, P, X, layers=1):
-    """configs[3] CPU side: the oracle's batched prefill restatement (numpy fp64, the
-    reference's `h @ W` layout, all host threads) over the same P tokens on `layers` of the 32
-    layers, scaled by 32 / layers; the experts are materialised untimed first."""
+def cpu_prefill_sample(seed, P, X, layers=1, layout="ref"):
+    """configs[3] CPU side: the oracle's batched prefill restatement over the same P tokens on
+    `layers` of the 32 layers, scaled by 32 / layers, all host threads; layout "ref": numpy
+    fp64 in the reference's `h @ W` layout (variant (i)), "dev": the tuned fp32 port (ii).
+    The experts are materialised untimed first."""
     import oracle
+    from oracle.model import mixtral_prefill_fp32
 
     alpha = 0.1 * math.sqrt(16 / D)
-    ref = oracle.MixtralRef(L, E, K, D, F, alpha, seed=seed, layout="ref",
+    ref = oracle.MixtralRef(L, E, K, D, F, alpha, seed=seed, layout=layout,
                             layers=list(range(layers)), rms_norm=True)
     t_gen = time.perf_counter()
     ref.materialize()
     t_gen = time.perf_counter() - t_gen
     x = X.cpu().numpy()
     t0 = time.perf_counter()
-    oracle.mixtral_prefill(ref, x)
+    if layout == "ref":
+        oracle.mixtral_prefill(ref, x)
+    else:
+        mixtral_prefill_fp32(ref, x)
     dt = time.perf_counter() - t0
     per_batch = dt * (L / layers)
+    what = ("oracle.mixtral_prefill, numpy fp64 batched GEMMs" if layout == "ref" else
+            "oracle.model.mixtral_prefill_fp32, numpy fp32 sgemm on row-major weights")
     return {"value": P / per_batch, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{P} tokens x {layers} of {L} layers (oracle.mixtral_prefill, numpy fp64 "
-                      f"batched GEMMs), scaled by {L}/{layers}; {dt:.1f} s timed, {t_gen:.1f} s "
-                      "untimed weight materialisation"}
+            "sample": f"{P} tokens x {layers} of {L} layers ({what}), scaled by {L}/{layers}; "
+                      f"{dt:.1f} s timed, {t_gen:.1f} s untimed weight materialisation"}
 
 
 def isolated_gemm(Dd, Ff, m=128):

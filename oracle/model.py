@@ -277,6 +277,40 @@ def mixtral_prefill(ref: "MixtralRef", X: np.ndarray, return_gaps: bool = False)
     return x, acts, guessed
 
 
+def mixtral_prefill_fp32(ref: "MixtralRef", X: np.ndarray):
+    """The batched prefill as a tuned fp32 CPU port (the cpu_baseline_fp32 leg of bench.py,
+    BASELINE.md variant (ii)): row-major (nn.Linear-layout) fp32 weights, BLAS sgemm over the
+    token rows of each expert, same routing.  Returns outputs (T, d)."""
+    assert ref.layout != "ref"
+    T, d = X.shape
+    E, K = ref.E, ref.K
+    x = X.astype(np.float32)
+    one = np.float32(1.0)
+    for l in ref.layers:
+        M, gw, gb = ref.dense(l)
+        h = x + np.float32(ref.alpha) * (x @ M.T)
+        hn = h / np.sqrt(np.mean(h * h, axis=1, keepdims=True) + np.float32(ref.rms_eps)) if ref.rms_norm else h
+        z = hn @ gw.T + gb
+        if not np.isfinite(z).all():
+            raise FloatingPointError("gate logits are not finite")
+        sel = np.argsort(-z, axis=1, kind="stable")[:, :K]
+        zmax = z.max(axis=1, keepdims=True)
+        p = np.exp(z - zmax)
+        p /= p.sum(axis=1, keepdims=True)
+        w = np.take_along_axis(p, sel, 1)
+        out = h.copy()
+        for e in range(E):
+            rows, slots = np.nonzero(sel == e)
+            if rows.size == 0:
+                continue
+            w1, w3, w2 = ref.expert(l, e)
+            a1, a3 = hn[rows] @ w1.T, hn[rows] @ w3.T
+            act = a1 / (one + np.exp(-a1)) * a3
+            out[rows] += w[rows, slots][:, None] * (act @ w2.T)
+        x = out
+    return x
+
+
 def replay_layers(acts: np.ndarray, E: int, C: int, policy: int, df=1.0, dp=1):
     """Per-layer replay of a (T, L, K) activation grid with the C oracle."""
     T, L, K = acts.shape
