@@ -1108,11 +1108,9 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
     MOE_LAUNCHED();
     return MOE_OK;
   };
-  auto launch_down = [&](FfnParams fp, int only, int row0 = 0, int nrows = 0) -> moe_status {
+  auto launch_down = [&](FfnParams fp, int only) -> moe_status {
     if (g->bf16) {
       StreamParams sp{};
-      sp.row0 = row0;
-      sp.nrows = nrows;
       sp.d = D;
       sp.f = g->f;
       sp.K = K;
@@ -1294,29 +1292,19 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
           TRY(launch_ffn(fp, i));
           TRY(prof_end(fev));
           if (plan.comp[i]) {
-            // w2 arrives in row pieces, decoded as they land; the rows of all but the last piece
-            // are reduced as soon as those are decoded, so the step's tail after the last
-            // landing is one piece's decode + down
-            const int NP = moe_engine::kCodedParts, prow = D / moe_engine::kCodedBParts;
-            for (int q = 1; q < NP; ++q) {
+            for (int q = 1; q < moe_engine::kCodedParts; ++q) {
               MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_part[i][q], 0));
               TRY(xc::decode(plan.land[i] + coff, plan.part[i][q].hdr,
                              reinterpret_cast<uint16_t*>(plan.dst[i] + g->coded_part_out_off(q)), s));
               coff += static_cast<long long>(plan.part[i][q].size);
-              if (q == NP - 2 || q == NP - 1) {
-                if (q == NP - 1) MOE_CUDA(cudaEventRecord(plan.free_ev[i], s));
-                const int r0 = q == NP - 1 ? (NP - 2) * prow : 0;
-                TRY(prof_begin(fev));
-                TRY(launch_down(fp, i, r0, q == NP - 1 ? prow : (NP - 2) * prow));
-                TRY(prof_end(fev));
-              }
             }
+            MOE_CUDA(cudaEventRecord(plan.free_ev[i], s));
           } else {
             MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_b[i], 0));
-            TRY(prof_begin(fev));
-            TRY(launch_down(fp, i));
-            TRY(prof_end(fev));
           }
+          TRY(prof_begin(fev));
+          TRY(launch_down(fp, i));
+          TRY(prof_end(fev));
         }
       } else if (plan.n > 0) {
         MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_b[plan.n - 1], 0));

@@ -58,9 +58,6 @@ struct StreamParams {
   // UP: scale applied to xin while staging (1/rms(h') from the gate), or nullptr
   const float* xscale;
   int stream_only;         // microbenchmark: consumers release stages without computing
-  // DOWN: output rows [row0, row0 + nrows) only (nrows 0: all d); a coded expert's w2 arrives
-  // in row pieces and each piece's rows are reduced as soon as it is decoded
-  int row0, nrows;
 };
 
 // Which experts this launch covers: (selection slot j, weight block), in ascending expert
@@ -98,8 +95,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
   static_assert(RPB * WPR == kStreamWarps, "RPB must divide the consumer warp count");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = MODE == kModeDown ? p.f : p.d;  // row length
-  const int R = MODE == kModeUp ? p.f : (MODE == kModeDown && p.nrows > 0 ? p.nrows : p.d);  // rows
-  const int roff = MODE == kModeDown ? p.row0 : 0;  // first row of this launch
+  const int R = MODE == kModeUp ? p.f : p.d;    // rows per matrix
   const int cb = p.cb, ncb = p.ncb, S = p.stages;
   const uint32_t slice = static_cast<uint32_t>(cb) * 2;   // bytes per row slice
   const uint32_t stage_bytes = slice * RPB * NM;
@@ -133,8 +129,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
     W[0] = reinterpret_cast<const uint16_t*>(blk[a]);                 // w1 [f][d]
     W[1] = W[0] + static_cast<size_t>(p.f) * p.d;                      // w3 [f][d]
   } else {
-    W[0] = reinterpret_cast<const uint16_t*>(blk[a]) + 2 * static_cast<size_t>(p.f) * p.d +
-           static_cast<size_t>(roff) * p.f;                                              // w2 [d][f]
+    W[0] = reinterpret_cast<const uint16_t*>(blk[a]) + 2 * static_cast<size_t>(p.f) * p.d;  // w2 [d][f]
   }
 
   uint8_t* stage_base = smem;
@@ -242,7 +237,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (c == ncb - 1) {
-      const int r = (rb0 + it / ncb) * RPB + row_in_block + roff;
+      const int r = (rb0 + it / ncb) * RPB + row_in_block;
       float v[NM];
 #pragma unroll
       for (int m = 0; m < NM; ++m) {
