@@ -85,21 +85,20 @@ __device__ __forceinline__ double warp_max(double v) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
   return v;
 }
+// 64-bit warp min / max as two 32-bit redux.sync steps: the extreme high word, then the
+// extreme low word among the lanes holding it (exactly the 64-bit extreme; 2 instructions in
+// place of a 5-level shuffle tree -- these sit on the gate's and the replay's serial path)
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    uint64_t w = __shfl_xor_sync(FULL, v, o);
-    v = w < v ? w : v;
-  }
-  return v;
+  const uint32_t hi = static_cast<uint32_t>(v >> 32);
+  const uint32_t mh = __reduce_min_sync(FULL, hi);
+  const uint32_t ml = __reduce_min_sync(FULL, hi == mh ? static_cast<uint32_t>(v) : 0xFFFFFFFFu);
+  return (static_cast<uint64_t>(mh) << 32) | ml;
 }
 __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    uint64_t w = __shfl_xor_sync(FULL, v, o);
-    v = w > v ? w : v;
-  }
-  return v;
+  const uint32_t hi = static_cast<uint32_t>(v >> 32);
+  const uint32_t mh = __reduce_max_sync(FULL, hi);
+  const uint32_t ml = __reduce_max_sync(FULL, hi == mh ? static_cast<uint32_t>(v) : 0u);
+  return (static_cast<uint64_t>(mh) << 32) | ml;
 }
 
 // Order-preserving map of a finite float/double onto unsigned integers, with -0 == +0
