@@ -80,6 +80,9 @@ def parse_args():
                         "markov:<repeat_prob>; LRU and LFU on each; '' = skip")
     p.add_argument("--tiny-tokens", type=int, default=1024,
                    help="configs[0]: tiny toy-MoE decode (L=4,E=8,K=2,d=256), LRU C=2; 0 = skip")
+    p.add_argument("--replay-streams", type=int, default=2048,
+                   help="SURVEY 8f.1 replay sweep: independent layer streams (0 = skip)")
+    p.add_argument("--replay-tokens", type=int, default=8192)
     p.add_argument("--shared-store", action="store_true",
                    help="host experts in a node-shared segment (automatic when WORLD_SIZE > 1)")
     return p.parse_args()
@@ -563,6 +566,7 @@ def run_ours(args, world, rank, local):
     gemm_iso = isolated_gemm(D, F) if rank == 0 and args.prefill_tokens > 0 else None
     gemm_iso_t = isolated_gemm(D, F, 1024) if rank == 0 and args.prefill_tokens > 0 else None
     tiny = run_tiny(args) if rank == 0 and world == 1 and args.tiny_tokens > 0 else None
+    replay = run_replay(args) if rank == 0 and world == 1 and args.replay_streams > 0 else None
     if store is not None:
         barrier(world)
         store.close()
@@ -654,6 +658,8 @@ def run_ours(args, world, rank, local):
         line["trace_driven"] = trace_driven
     if tiny:
         line["tiny"] = tiny
+    if replay:
+        line["replay"] = replay
     if prefill:
         tf_peak = float(peaks.get("bf16_tflops", 1590.0))
         for rec in [prefill["gemm"]] + [r for r in (gemm_iso, gemm_iso_t) if r]:
@@ -730,6 +736,75 @@ def run_tiny(args):
                              "kind": "port",
                              "sample": f"oracle toy_run_model (numpy fp64, toymoe.py:159-190) + "
                                        f"policy replay, {T} tokens"}}
+
+
+def run_replay(args):
+    """the offline policy replay (K7, kernels.replay_policy / simulate's layer
+    loop) as a sweep workload -- `replay_streams` independent Zipf layer streams of T steps,
+    each replayed under LRU / LFU / LFU-aged at C = 2, 4, 6 (one warp per stream, inputs resident
+    in HBM) -- beside the oracle's C replay (the reference algorithm, kernels.py:60-147) on all
+    host threads.  Decisions are checked equal on a sample."""
+    import concurrent.futures as cf
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_2511_05814_b200 import _native
+    from paper_2511_05814_b200.tracegen import ZipfParams, gen_zipf
+    from paper_2511_05814_b200.traces import ModelShape
+
+    S, T, Er, Kr = args.replay_streams, args.replay_tokens, 8, 2
+    tr = gen_zipf(ZipfParams(ModelShape(S, Er, Kr), T, skew_exponent=1.0, seed=args.seed))
+    acts = np.ascontiguousarray(np.transpose(tr.activations, (1, 0, 2)))          # (S, T, K)
+    lib = _native.lib()
+    d_acts = torch.from_numpy(acts).cuda()
+    rb = torch.empty((S, T, Er), dtype=torch.uint8, device="cuda")
+    ev = torch.empty_like(rb)
+    configs = [(0, 1.0, 1), (1, 1.0, 1), (2, 0.5, 16)]
+    caps = (2, 4, 6)
+    stream = torch.cuda.current_stream()
+    sp = _native.stream_ptr()
+
+    def one(code, df, dp, C):
+        _native.check(lib.moe_replay_policy_layers(d_acts.data_ptr(), S, T, Kr, Er, C, code, df, dp,
+                                                   rb.data_ptr(), ev.data_ptr(), sp))
+
+    for code, df, dp in configs:       # warm-up
+        one(code, df, dp, 4)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for code, df, dp in configs:
+        for C in caps:
+            one(code, df, dp, C)
+    b.record(stream)
+    torch.cuda.synchronize()
+    gpu_s = a.elapsed_time(b) / 1e3
+    steps = S * T * len(configs) * len(caps)
+    # the last launch (LFU-aged, C = 6) against the oracle on a sample of streams
+    grb = rb.cpu().numpy()
+    ok = all(np.array_equal(grb[i], oracle.replay_policy(acts[i], Er, 6, 2, 0.5, 16)[0])
+             for i in range(0, S, max(1, S // 16)))
+    # CPU: the oracle's C replay, one stream per task, all host threads (ctypes drops the GIL)
+    ncpu = os.cpu_count() or 1
+    cpu_streams = S
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(ncpu) as ex:
+        for code, df, dp in configs:
+            for C in caps:
+                list(ex.map(lambda i: oracle.replay_policy(acts[i], Er, C, code, df, dp), range(cpu_streams)))
+    cpu_s = time.perf_counter() - t0
+    cpu_steps = cpu_streams * T * len(configs) * len(caps)
+    return {"workload": f"SURVEY 8f.1 offline replay sweep: {S} Zipf(1.0) layer streams x {T} steps "
+                        f"(E=8, K=2) x {{lru, lfu, lfu-aged:0.5:16}} x C in {{2,4,6}}",
+            "steps": steps, "gpu_ms": gpu_s * 1e3, "steps_per_s": steps / gpu_s,
+            "decisions_equal_oracle_sample": bool(ok),
+            "cpu_baseline": {"value": cpu_steps / cpu_s, "unit": "steps/s", "cores": ncpu,
+                             "kind": "port", "sample": f"oracle C replay (kernels.py:60-147), "
+                                                       f"{cpu_streams} streams x 9 configs, {ncpu} threads"},
+            "reference_published": "numba kernel ~25 M steps/s, one stream, 'typical machine' (pkg/README.md:144-145)"}
 
 
 def run_trace_driven(args, eng, inputs, stream, world):

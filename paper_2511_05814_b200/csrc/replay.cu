@@ -94,6 +94,71 @@ __global__ void __launch_bounds__(128) replay_kernel(const int64_t* __restrict__
   if (!ok && lane == 0) atomicExch(err, 1);
 }
 
+// Same replay with the activation rows staged 32 steps at a time (lane i loads row t0 + i in
+// one coalesced read, each step broadcasts its row by shuffle): the step chain no longer waits
+// on a global load every few steps.  K is a template constant (ids stay in registers).
+template <int EPL, int KK>
+__global__ void __launch_bounds__(128) replay_kernel_staged(const int64_t* __restrict__ acts, int L,
+                                                            long long T, int E, int C, int policy,
+                                                            double df, long long dp,
+                                                            uint8_t* __restrict__ rb_out,
+                                                            uint8_t* __restrict__ ev_out,
+                                                            int32_t* __restrict__ nu_scratch,
+                                                            int* __restrict__ err) {
+  const int layer = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (layer >= L) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t* a = acts + static_cast<long long>(layer) * T * KK;
+  uint8_t* rb = rb_out + static_cast<long long>(layer) * T * E;
+  uint8_t* ev = ev_out + static_cast<long long>(layer) * T * E;
+  int32_t* nu = nu_scratch ? nu_scratch + static_cast<long long>(layer) * T * E : nullptr;
+  if (policy == MOE_P_OPT) {
+    fill_next_use<EPL>(a, T, KK, E, nu);
+    __syncwarp();
+  }
+  WarpCacheState<EPL> st;
+  st.resident = 0;
+#pragma unroll
+  for (int i = 0; i < EPL; ++i) {
+    st.freq[i] = 0.0;
+    st.last_touch[i] = -1;
+  }
+  bool ok = true;
+  int64_t mine[KK];
+  auto load = [&](long long t0) {
+#pragma unroll
+    for (int j = 0; j < KK; ++j) mine[j] = t0 + lane < T ? a[(t0 + lane) * KK + j] : 0;
+  };
+  load(0);
+  for (long long t0 = 0; t0 < T; t0 += 32) {
+    int64_t cur[KK];
+#pragma unroll
+    for (int j = 0; j < KK; ++j) cur[j] = mine[j];
+    if (t0 + 32 < T) load(t0 + 32);  // next chunk in flight while this one is replayed
+    const int n = T - t0 < 32 ? static_cast<int>(T - t0) : 32;
+    for (int u = 0; u < n; ++u) {
+      const long long t = t0 + u;
+      int64_t row[KK];
+#pragma unroll
+      for (int j = 0; j < KK; ++j) row[j] = __shfl_sync(FULL, cur[j], u);
+      uint32_t rbb, evb;
+      const bool step_ok = warp_policy_step<EPL>(
+          st, E, C, policy, df, dp, t, [&](int j) { return row[j]; }, KK,
+          [&](int i) { return static_cast<long long>(nu[t * E + i * 32 + lane]); }, rbb, evb);
+      ok = ok && step_ok;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        const int e = i * 32 + lane;
+        if (e < E) {
+          rb[t * E + e] = static_cast<uint8_t>((rbb >> i) & 1u);
+          ev[t * E + e] = static_cast<uint8_t>((evb >> i) & 1u);
+        }
+      }
+    }
+  }
+  if (!ok && lane == 0) atomicExch(err, 1);
+}
+
 template <int EPL>
 __global__ void policy_step_kernel(uint8_t* resident, int64_t* last_touch, double* freq,
                                    long long step, int E, int C, int policy, double df,
@@ -217,12 +282,23 @@ moe_status moe_replay_policy_layers(const int64_t* acts_dev, int32_t L, int64_t 
     MOE_CUDA(cudaMallocAsync(&nu, sizeof(int32_t) * static_cast<size_t>(L) * T * E, s));
   const int threads = 128;
   const int blocks = (L * 32 + threads - 1) / threads;
+#define STAGED(EPL_, KK_)                                                                        \
+  replay_kernel_staged<EPL_, KK_><<<blocks, threads, 0, s>>>(acts_dev, L, T, E, C, policy,         \
+                                                             decay_factor, decay_period,           \
+                                                             resident_before_dev, evicted_dev, nu, err)
 #define LAUNCH(EPL_)                                                                      \
-  replay_kernel<EPL_><<<blocks, threads, 0, s>>>(acts_dev, L, T, K, E, C, policy,         \
-                                                 decay_factor, decay_period,              \
-                                                 resident_before_dev, evicted_dev, nu, err)
+  do {                                                                                    \
+    if (K == 1) STAGED(EPL_, 1);                                                          \
+    else if (K == 2) STAGED(EPL_, 2);                                                     \
+    else if (K == 4) STAGED(EPL_, 4);                                                     \
+    else                                                                                  \
+      replay_kernel<EPL_><<<blocks, threads, 0, s>>>(acts_dev, L, T, K, E, C, policy,     \
+                                                     decay_factor, decay_period,          \
+                                                     resident_before_dev, evicted_dev, nu, err); \
+  } while (0)
   MOE_EPL_DISPATCH(E, LAUNCH);
 #undef LAUNCH
+#undef STAGED
   MOE_LAUNCHED();
   if (nu) MOE_CUDA(cudaFreeAsync(nu, s));
   return check_err_flag(s);
