@@ -4,7 +4,7 @@
 # shares, not absolute times, carry over to the full bench (see profiles/README.md).
 TAG=${1:-r1}
 mkdir -p gpurun_out
-CMD="python bench.py --layers 2 --steps 2 --warmup 1 --variants lru --e2e-steps 0 --no-cpu-baseline --prefill-tokens 0 --trace-variants '' --tiny-tokens 0"
+CMD="python bench.py --layers 2 --steps 2 --warmup 1 --variants lru --e2e-steps 0 --no-cpu-baseline --prefill-tokens 0 --trace-variants '' --tiny-tokens 0 --replay-streams 0"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv bash -c "$CMD" \
   > gpurun_out/ncu_launch_${TAG}.log 2>&1
