@@ -582,6 +582,24 @@ def run_ours(args, world, rank, local):
     ffn_all_gbs = (ktimes["ffn_expert_runs"] * EB / (ktimes["ffn_ms"] / 1e3) / 1e9
                    if ktimes["ffn_ms"] > 0 else None)
     traffic = committed_ffn_traffic() if args.model == "mixtral_8x7b" else None
+    xb, xms, xkms = ktimes.get("xdec_bytes", 0), ktimes.get("xdec_ms", 0.0), ktimes.get("xdec_kernel_ms", 0.0)
+    roofline_decode = None
+    if xb and xms > 0:
+        roofline_decode = {
+            "kernel": "xc::decode_kernel<23>: exponent-coded expert parts -> bf16 in the cache buffer",
+            "bound": "hbm", "achieved": xb / (xms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": xb / (xms / 1e3) / 1e9 / hbm_peak,
+            "achieved_in_kernel": xb / (xkms / 1e3) / 1e9 if xkms > 0 else None,
+            "frac_in_kernel": xb / (xkms / 1e3) / 1e9 / hbm_peak if xkms > 0 else None,
+            "launches": ktimes["xdec_launches"], "bytes_per_launch": xb / max(1, ktimes["xdec_launches"]),
+            "algorithmic_bytes": "coded part read + bf16 weights written (~3.35 B / weight)",
+            "traffic": 338.8e6, "traffic_unit": "DRAM bytes of one w1|w3-part launch (ncu --set full: "
+                                                "157.95 MB read + 180.8 MB written; algorithmic 392.8 MB; "
+                                                "profiles/ncu_xc_decode_r1.md)",
+            "note": "ALU-bound in practice (ncu: ALU pipe 73 %, DRAM 34 %); overlapped with the H2D "
+                    "copies except for the step's last w2 piece",
+            "peak_source": peaks.get("source", "MEASURED_PEAKS.json hbm_gbs"),
+        }
     line = {
         "metric": METRIC,
         "value": head["tokens_per_s"],
@@ -618,7 +636,7 @@ def run_ours(args, world, rank, local):
                  "unit": "GB/s", "frac": head["h2d_GBps"] / pcie_peak,
                  "copy_engine_GBps_while_busy": head["demand_copy_GBps"],
                  "peak_source": "measured here: 1 GiB pinned cudaMemcpyAsync, best of 5"},
-        "roofline": {
+        "roofline_ffn": {
             "kernel": "expert FFN: stream_gemv_kernel up (w1|w3) + down (w2), bulk-copy pipelines",
             "bound": "hbm", "achieved": ffn_gbs, "peak": hbm_peak, "unit": "GB/s",
             "frac": ffn_gbs / hbm_peak if ffn_gbs else None,
@@ -642,13 +660,23 @@ def run_ours(args, world, rank, local):
             "algorithmic_bytes_per_expert": EB,
             "peak_source": peaks.get("source", "MEASURED_PEAKS.json hbm_gbs"),
         },
+        "roofline_decode": roofline_decode,
         "kernel_ms_per_step": {k: ktimes[k] / args.steps for k in ("mix_ms", "gate_ms", "ffn_ms",
-                                                                 "finalize_ms")},
+                                                                 "finalize_ms", "xdec_ms",
+                                                                 "ffn_kernel_ms", "xdec_kernel_ms")},
         "gpu_launches": launches_timed,
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
+    # the dominant kernel = the larger in-kernel device time over the timed region
+    ffn_k, dec_k = ktimes.get("ffn_kernel_ms", 0.0), ktimes.get("xdec_kernel_ms", 0.0)
+    dom = "decode" if roofline_decode and dec_k > ffn_k else "ffn"
+    line["roofline"] = dict(roofline_decode if dom == "decode" else line["roofline_ffn"])
+    line["roofline"]["dominant_by"] = (f"in-kernel device time in the timed region: expert FFN "
+                                       f"{ffn_k / args.steps:.2f} ms/step, exponent decode "
+                                       f"{dec_k / args.steps:.2f} ms/step; the other kernel's object "
+                                       f"is roofline_{'ffn' if dom == 'decode' else 'decode'}")
     if cpu:
         line["speedup_vs_cpu_port"] = head["tokens_per_s"] / cpu["value"]
     if cpu32:

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define MOE_ABI_VERSION 2
+#define MOE_ABI_VERSION 3
 
 typedef int32_t moe_status;
 enum {
@@ -239,6 +239,11 @@ typedef struct {
                                the FFN launches that processed >= 1 expert: excludes launch
                                latency and the host-side gaps the events see */
   double gemm_kernel_ms;    /* the same in-kernel span summed over the prefill GEMM launches */
+  /* decode: exponent-decode launches of coded demand / adopted experts (ABI 3) */
+  double xdec_ms;           /* summed CUDA-event time */
+  double xdec_kernel_ms;    /* summed in-kernel span (globaltimer) */
+  int64_t xdec_bytes;       /* algorithmic bytes: coded part read + bf16 weights written */
+  int64_t xdec_launches;
 } moe_kernel_times;
 moe_status moe_engine_profile(moe_engine* eng, int32_t enable);
 /* Resolves outstanding events (synchronises) and returns the running totals. */

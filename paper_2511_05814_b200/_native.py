@@ -72,7 +72,9 @@ class KernelTimesC(ctypes.Structure):
         ("ffn_active_launches", ctypes.c_int64), ("gemm_ms", ctypes.c_double),
         ("gemm_launches", ctypes.c_int64), ("gemm_flops", ctypes.c_double),
         ("gemm_bytes", ctypes.c_int64), ("prefill_ms", ctypes.c_double),
-        ("ffn_kernel_ms", ctypes.c_double), ("gemm_kernel_ms", ctypes.c_double)]
+        ("ffn_kernel_ms", ctypes.c_double), ("gemm_kernel_ms", ctypes.c_double),
+        ("xdec_ms", ctypes.c_double), ("xdec_kernel_ms", ctypes.c_double),
+        ("xdec_bytes", ctypes.c_int64), ("xdec_launches", ctypes.c_int64)]
 
 
 _P = ctypes.c_void_p

@@ -405,6 +405,25 @@ void resolve_profile(moe_engine* g) {
     g->prof_free.push_back(e[1]);
   }
   g->prof_ffn.clear();
+  if (!g->prof_dec.empty()) {
+    std::vector<long long> ds(2 * g->prof_dec.size(), 0);
+    if (g->prof_dec_dev) {
+      cudaMemcpy(ds.data(), g->prof_dec_dev, sizeof(long long) * ds.size(), cudaMemcpyDeviceToHost);
+      cudaMemset(g->prof_dec_dev, 0, sizeof(long long) * ds.size());
+    }
+    for (size_t i = 0; i < g->prof_dec.size(); ++i) {
+      auto& e = g->prof_dec[i];
+      k.xdec_ms += elapsed(e[0], e[1]);
+      k.xdec_bytes += g->prof_dec_bytes[i];
+      k.xdec_launches += 1;
+      const long long t0 = 0x7fffffffffffffffll - ds[2 * i], t1 = ds[2 * i + 1];
+      if (ds[2 * i] > 0 && t1 > t0) k.xdec_kernel_ms += (t1 - t0) / 1e6;
+      g->prof_free.push_back(e[0]);
+      g->prof_free.push_back(e[1]);
+    }
+    g->prof_dec.clear();
+    g->prof_dec_bytes.clear();
+  }
   for (auto& e : g->prof_final) {
     k.finalize_ms += elapsed(e[0], e[1]);
     k.finalize_launches += 1;
@@ -760,6 +779,9 @@ moe_status moe_engine_destroy(moe_engine* g) {
   for (auto& a : g->prof_ffn)
     for (auto e : a) cudaEventDestroy(e);
   if (g->prof_bytes_dev) cudaFree(g->prof_bytes_dev);
+  for (auto& a : g->prof_dec)
+    for (auto e : a) cudaEventDestroy(e);
+  if (g->prof_dec_dev) cudaFree(g->prof_dec_dev);
   if (g->pf) prefill_release(g->pf);
   if (g->cstore && !g->cstore_external) cudaFreeHost(g->cstore);
   if (g->cstore && g->cstore_external && g->cstore_registered) cudaHostUnregister(g->cstore);
@@ -1082,6 +1104,27 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
     }
     return MOE_OK;
   };
+  // exponent decode of a coded part, with an event pair and an in-kernel span when profiling
+  auto xdecode = [&](const char* src, const xc::PartHeader& h, char* dst) -> moe_status {
+    long long* slot = nullptr;
+    std::array<cudaEvent_t, 2> ev{};
+    if (g->profiling && g->prof_dec.size() < static_cast<size_t>(moe_engine::kProfSlots)) {
+      if (!g->prof_dec_dev) {
+        MOE_CUDA(cudaMalloc(&g->prof_dec_dev, 2 * sizeof(long long) * moe_engine::kProfSlots));
+        MOE_CUDA(cudaMemset(g->prof_dec_dev, 0, 2 * sizeof(long long) * moe_engine::kProfSlots));
+      }
+      slot = g->prof_dec_dev + 2 * g->prof_dec.size();
+      ev = {take_prof_event(g), take_prof_event(g)};
+      MOE_CUDA(cudaEventRecord(ev[0], s));
+    }
+    TRY(xc::decode(src, h, reinterpret_cast<uint16_t*>(dst), s, slot));
+    if (slot) {
+      MOE_CUDA(cudaEventRecord(ev[1], s));
+      g->prof_dec.push_back(ev);
+      g->prof_dec_bytes.push_back(static_cast<long long>(h.total) + static_cast<long long>(h.n) * 2);
+    }
+    return MOE_OK;
+  };
   auto launch_ffn = [&](FfnParams fp, int only) -> moe_status {
     if (g->bf16) {
       StreamParams sp{};
@@ -1285,7 +1328,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
           MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_a[i], 0));
           long long coff = 0;
           if (plan.comp[i]) {
-            TRY(xc::decode(plan.land[i], plan.part[i][0].hdr, reinterpret_cast<uint16_t*>(plan.dst[i]), s));
+            TRY(xdecode(plan.land[i], plan.part[i][0].hdr, plan.dst[i]));
             coff = static_cast<long long>(plan.part[i][0].size);
           }
           TRY(prof_begin(fev));
@@ -1294,8 +1337,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
           if (plan.comp[i]) {
             for (int q = 1; q < moe_engine::kCodedParts; ++q) {
               MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_part[i][q], 0));
-              TRY(xc::decode(plan.land[i] + coff, plan.part[i][q].hdr,
-                             reinterpret_cast<uint16_t*>(plan.dst[i] + g->coded_part_out_off(q)), s));
+              TRY(xdecode(plan.land[i] + coff, plan.part[i][q].hdr, plan.dst[i] + g->coded_part_out_off(q)));
               coff += static_cast<long long>(plan.part[i][q].size);
             }
             MOE_CUDA(cudaEventRecord(plan.free_ev[i], s));

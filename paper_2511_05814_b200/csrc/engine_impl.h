@@ -221,6 +221,9 @@ struct moe_engine {
   std::vector<std::array<cudaEvent_t, 3>> prof_pending;  // before mix, after mix, after gate
   std::vector<std::array<cudaEvent_t, 2>> prof_ffn;      // around each expert-FFN launch group
   long long* prof_bytes_dev = nullptr;                    // per FFN launch: bytes streamed
+  std::vector<std::array<cudaEvent_t, 2>> prof_dec;      // around each exponent-decode launch
+  std::vector<long long> prof_dec_bytes;                 // its algorithmic bytes
+  long long* prof_dec_dev = nullptr;                     // its in-kernel span slots [2]
   static constexpr int kProfSlots = 1 << 16;
   std::vector<std::array<cudaEvent_t, 2>> prof_final;
   std::vector<int> prof_pending_k;

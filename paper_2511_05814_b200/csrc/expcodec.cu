@@ -233,8 +233,14 @@ __device__ __forceinline__ uint32_t spread2(uint32_t cb) {
 // subtraction, the bf16 words by byte permutes) and patches the level-1 escapes in place.
 template <int K>
 __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restrict__ part,
-                                                          uint16_t* __restrict__ out) {
+                                                          uint16_t* __restrict__ out,
+                                                          long long* __restrict__ prof) {
   __shared__ int warp_tot[kThreads / 32];
+  if (prof && threadIdx.x == 0) {  // in-kernel span: max(LLONG_MAX - CTA start), max(end)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&prof[0], 0x7fffffffffffffffll - static_cast<long long>(t));
+  }
   const PartHeader& h = *reinterpret_cast<const PartHeader*>(part);
   const uint32_t c = blockIdx.x;
   const ChunkEntry ce = reinterpret_cast<const ChunkEntry*>(part + align16(sizeof(PartHeader)))[c];
@@ -357,19 +363,25 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
     }
   }
   store_out(out, first, cnt, o);
+  if (prof && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&prof[1], static_cast<long long>(t));
+  }
 }
 
-moe_status decode(const void* part_dev, const PartHeader& h, uint16_t* out_dev, cudaStream_t s) {
+moe_status decode(const void* part_dev, const PartHeader& h, uint16_t* out_dev, cudaStream_t s,
+                  long long* prof) {
   MOE_REQUIRE(h.magic == kMagic && (h.kbits == 3 || h.kbits == 4 || h.kbits == kMode23),
               "not an exponent-coded part");
   if (h.n == 0) return MOE_OK;
   const uint8_t* p = static_cast<const uint8_t*>(part_dev);
   if (h.kbits == 3)
-    decode_kernel<3><<<h.nch, kThreads, 0, s>>>(p, out_dev);
+    decode_kernel<3><<<h.nch, kThreads, 0, s>>>(p, out_dev, prof);
   else if (h.kbits == 4)
-    decode_kernel<4><<<h.nch, kThreads, 0, s>>>(p, out_dev);
+    decode_kernel<4><<<h.nch, kThreads, 0, s>>>(p, out_dev, prof);
   else
-    decode_kernel<kMode23><<<h.nch, kThreads, 0, s>>>(p, out_dev);
+    decode_kernel<kMode23><<<h.nch, kThreads, 0, s>>>(p, out_dev, prof);
   MOE_LAUNCHED();
   return MOE_OK;
 }

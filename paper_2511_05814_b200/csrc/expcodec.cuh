@@ -51,8 +51,10 @@ inline __host__ __device__ uint64_t align16(uint64_t x) { return (x + 15) & ~uin
 // multi-threaded over chunks
 uint64_t encoded_size(const uint16_t* in, uint64_t n, int mode);
 uint64_t encode(const uint16_t* in, uint64_t n, int mode, uint8_t* out);
-// device: decode a part (already in HBM) into n bf16 words, on stream s
-moe_status decode(const void* part_dev, const PartHeader& h, uint16_t* out_dev, cudaStream_t s);
+// device: decode a part (already in HBM) into n bf16 words, on stream s; `prof` (optional,
+// 2 zeroed int64) receives the launch's in-kernel span (LLONG_MAX - first CTA start, last end)
+moe_status decode(const void* part_dev, const PartHeader& h, uint16_t* out_dev, cudaStream_t s,
+                  long long* prof = nullptr);
 
 }  // namespace xc
 }  // namespace moe
