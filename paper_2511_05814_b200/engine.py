@@ -56,7 +56,8 @@ class EngineConfig:
     transfer: str = "auto"               # "auto" | "copy_engine" | "sm" (see moeb200.h)
     store_layers: int = 0                # host store depth (0 = num_layers; else layers alias l % S)
     prefetch_buffers: int = 0            # staging buffers per layer with prefetch (0 = top_k)
-    compress: bool = False               # exponent-coded (lossless) demand / prefill transfers
+    compress: int = 0                    # exponent-coded (lossless) demand / prefill transfers:
+                                         # 0 raw, 1 raw + coded host stores, 2 coded store only
 
     @staticmethod
     def mixtral_8x7b(**kw) -> "EngineConfig":
@@ -161,7 +162,7 @@ class OffloadEngine:
                                                        int(init_experts)))
 
     def coded_size(self) -> int:
-        """Bytes of the exponent-coded store (compress=True; raw experts already written)."""
+        """Bytes of the exponent-coded store (compress=1; raw experts already written)."""
         n = ctypes.c_int64()
         _native.check(self._lib.moe_engine_coded_size(self._h, ctypes.byref(n)))
         return n.value
