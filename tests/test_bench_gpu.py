@@ -1,0 +1,38 @@
+"""bench.py end to end on a B200 at reduced size: one JSON line carrying the driver contract's
+keys (value, e2e, roofline, cpu_baseline, clocks, gpu_launches) and every section."""
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+pytestmark = pytest.mark.gpu
+
+
+def test_bench_reduced_run_prints_contract_line():
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--layers", "2", "--steps", "3", "--warmup", "3",
+           "--variants", "lru,lfu+prefetch,lfu@2", "--e2e-steps", "3", "--cpu-sample-tokens", "2",
+           "--prefill-tokens", "64", "--prefill-decode", "4", "--tiny-tokens", "64",
+           "--trace-variants", "zipf:1.0", "--replay-streams", "64", "--replay-tokens", "256"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "roofline",
+              "roofline_ffn", "cpu_baseline", "cpu_baseline_fp32", "e2e", "gpu_launches", "clocks",
+              "pcie", "variants", "prefill", "tiny", "trace_driven", "replay", "kernel_timing"):
+        assert k in d, k
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in d["roofline"], k
+    assert {"value", "unit", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
+    assert set(d["variants"]) == {"lru", "lfu+prefetch", "lfu@2"}
+    assert all(v["check_hits_from_records"] for v in d["variants"].values())
+    assert d["tiny"]["trace_equals_oracle"] and d["replay"]["decisions_equal_oracle_sample"]
+    assert d["prefill"]["prefill_tokens_per_s"] > 0
