@@ -309,13 +309,18 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
     if (!active) return;
     const uint8_t* esc = part + h.esc_off + ce.esc_off + before2;
     const uint32_t win = ce.win, base = ce.base, w2 = win > 2u ? win - 2u : 0u;
-    const uint32_t E0x4 = (base + 1u - win) * 0x01010101u;
+    // level-1 exponents four at a time, carry-free: ex = (base - win) - (c - 1) per byte, a zero
+    // (escape) code first raised to 1 (base - win <= 255 even when base + 1 - win = 256)
+    const uint32_t Em1x4 = (base - win) * 0x01010101u;
     // exponent bytes of the thread's 32 weights in shared memory ([group][thread] words, so
     // the word accesses are conflict-free), escapes patched byte-wise, then the bf16 words
     __shared__ uint32_t xs[8 * kThreads];
 #pragma unroll
-    for (int g = 0; g < 8; ++g)
-      xs[g * kThreads + threadIdx.x] = E0x4 - spread2(static_cast<uint32_t>(c0 >> (8 * g)) & 0xFFu);
+    for (int g = 0; g < 8; ++g) {
+      const uint32_t s1 = spread2(static_cast<uint32_t>(c0 >> (8 * g)) & 0xFFu);
+      const uint32_t z1 = (~(s1 + 0x7F7F7F7Fu) & 0x80808080u) >> 7;  // 0x01 where the code is 0
+      xs[g * kThreads + threadIdx.x] = Em1x4 - ((s1 | z1) - 0x01010101u);
+    }
     uint8_t* xb = reinterpret_cast<uint8_t*>(xs) + threadIdx.x * 4;
     // escape positions as a 32-bit mask (even bits of zm gathered)
     uint64_t x = zm;

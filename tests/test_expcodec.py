@@ -91,6 +91,12 @@ def _cases():
     o[::4096] = 0x4780                                                      # windows 5..7
     o[4096 * 2 + 1::4096] = 0x7F00                                          # 2^127: window 7, escapes
     yield "outliers", o
+    # exponents 253..255 dominate (Inf / NaN payloads, huge values) so the level-1 window is 0
+    # and base + 1 - window = 256: byte-lane arithmetic must not carry across weights
+    hi = rng.integers(0, 1 << 7, 4096 * 3, dtype=np.uint16) | (rng.integers(253, 256, 4096 * 3).astype(np.uint16) << 7)
+    hi |= (rng.integers(0, 2, 4096 * 3).astype(np.uint16) << 15)
+    hi[::5] = (hi[::5] & 0x807F) | (rng.integers(0, 250, hi[::5].size).astype(np.uint16) << 7)  # escapes
+    yield "top_exponents", hi
 
 
 @pytest.mark.gpu
