@@ -905,9 +905,15 @@ def run_prefill(args, eng, inputs, base, stream, world, pcie_peak):
     P, Dd = args.prefill_tokens, inputs.shape[1]
     X = torch.stack([hash_weights(args.seed, tensor_id(5, base + 100000 + t), 1.0, Dd, "f32")
                      for t in range(P)])
+    # warm-up: the first prefill on an engine allocates its batch buffers (~3 GB) and builds
+    # the GEMM tile tables -- ~0.1 s that is not part of a prefill's steady-state cost
     eng.set_mode(policy=PolicyKind.lru(), cache_size=args.cache_size, prefetch="off")
-    eng.profile(True)
-    k0, s0 = eng.kernel_times(), eng.stats()
+    eng.prefill_device(X)
+    torch.cuda.synchronize()
+    eng.sync()
+    # timed: cold cache, no per-launch events
+    eng.set_mode(policy=PolicyKind.lru(), cache_size=args.cache_size, prefetch="off")
+    s0 = eng.stats()
     barrier(world)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -917,14 +923,23 @@ def run_prefill(args, eng, inputs, base, stream, world, pcie_peak):
     torch.cuda.synchronize()
     ms_p = max_over_ranks(a.elapsed_time(b), world)
     eng.sync()
-    k1, s1 = eng.kernel_times(), eng.stats()
+    s1 = eng.stats()
+    # GEMM timings: the same prefill replayed from the same cold state with per-launch events
+    eng.set_mode(policy=PolicyKind.lru(), cache_size=args.cache_size, prefetch="off")
+    eng.profile(True)
+    k0 = eng.kernel_times()
+    eng.prefill_device(X)
+    torch.cuda.synchronize()
+    eng.sync()
+    k1 = eng.kernel_times()
     eng.profile(False)
     k = {n: k1[n] - k0[n] for n in k1}
     nbytes = s1["prefill_bytes"] - s0["prefill_bytes"]
     hits, misses = s1["hits"] - s0["hits"], s1["misses"] - s0["misses"]
     out = {
         "workload": f"configs[3]: prefill {P} tokens (one batch) + decode, LRU cache "
-                    f"{args.cache_size}/layer, cold start",
+                    f"{args.cache_size}/layer, cold start (after one untimed warm-up prefill; "
+                    "GEMM timings from a profiled replay)",
         "prefill_tokens": P, "prefill_ms": ms_p,
         "prefill_tokens_per_s": sum_over_ranks(P / (ms_p / 1e3), world),
         "prefill_hit_rate": hits / max(1, hits + misses),
