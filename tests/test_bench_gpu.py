@@ -36,3 +36,16 @@ def test_bench_reduced_run_prints_contract_line():
     assert all(v["check_hits_from_records"] for v in d["variants"].values())
     assert d["tiny"]["trace_equals_oracle"] and d["replay"]["decisions_equal_oracle_sample"]
     assert d["prefill"]["prefill_tokens_per_s"] > 0
+
+
+def test_bench_8x22b_shape_reduced():
+    """configs[4]'s bench path (Mixtral-8x22B shape, LFU + prefetch default) on 2 layers."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--model", "mixtral_8x22b", "--layers", "2",
+           "--steps", "3", "--warmup", "3", "--e2e-steps", "2", "--cpu-sample-tokens", "2",
+           "--prefill-tokens", "0", "--tiny-tokens", "0", "--trace-variants", "", "--replay-streams", "0"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["config"]["workload"].startswith("configs[4]") and d["value"] > 0
+    assert list(d["variants"]) == ["lfu+prefetch"]
+    assert d["variants"]["lfu+prefetch"]["prefetch_issued"] > 0
