@@ -1104,8 +1104,9 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
     }
     return MOE_OK;
   };
-  // exponent decode of a coded part, with an event pair and an in-kernel span when profiling
-  auto xdecode = [&](const char* src, const xc::PartHeader& h, char* dst) -> moe_status {
+  // exponent decode of n coded parts in one launch, with an event pair and an in-kernel span
+  // when profiling
+  auto xdecode_n = [&](const char* const* src, const xc::PartHeader* h, char* const* dst, int n) -> moe_status {
     long long* slot = nullptr;
     std::array<cudaEvent_t, 2> ev{};
     if (g->profiling && g->prof_dec.size() < static_cast<size_t>(moe_engine::kProfSlots)) {
@@ -1117,13 +1118,24 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       ev = {take_prof_event(g), take_prof_event(g)};
       MOE_CUDA(cudaEventRecord(ev[0], s));
     }
-    TRY(xc::decode(src, h, reinterpret_cast<uint16_t*>(dst), s, slot));
+    const void* ps[xc::kMaxBatch];
+    uint16_t* os[xc::kMaxBatch];
+    long long bytes = 0;
+    for (int i = 0; i < n; ++i) {
+      ps[i] = src[i];
+      os[i] = reinterpret_cast<uint16_t*>(dst[i]);
+      bytes += static_cast<long long>(h[i].total) + static_cast<long long>(h[i].n) * 2;
+    }
+    TRY(xc::decode_batch(ps, h, os, n, s, slot));
     if (slot) {
       MOE_CUDA(cudaEventRecord(ev[1], s));
       g->prof_dec.push_back(ev);
-      g->prof_dec_bytes.push_back(static_cast<long long>(h.total) + static_cast<long long>(h.n) * 2);
+      g->prof_dec_bytes.push_back(bytes);
     }
     return MOE_OK;
+  };
+  auto xdecode = [&](const char* src, const xc::PartHeader& h, char* dst) -> moe_status {
+    return xdecode_n(&src, &h, &dst, 1);
   };
   auto launch_ffn = [&](FfnParams fp, int only) -> moe_status {
     if (g->bf16) {
@@ -1335,10 +1347,24 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
           TRY(launch_ffn(fp, i));
           TRY(prof_end(fev));
           if (plan.comp[i]) {
-            for (int q = 1; q < moe_engine::kCodedParts; ++q) {
+            // w2 pieces 1..3 decode in one launch once the third has landed (overlapping the
+            // last piece's copy), the last piece on its own after it lands
+            const int NP = moe_engine::kCodedParts;
+            const char* src[xc::kMaxBatch];
+            char* dst[xc::kMaxBatch];
+            xc::PartHeader hh[xc::kMaxBatch];
+            int nb = 0;
+            for (int q = 1; q < NP; ++q) {
               MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_part[i][q], 0));
-              TRY(xdecode(plan.land[i] + coff, plan.part[i][q].hdr, plan.dst[i] + g->coded_part_out_off(q)));
+              src[nb] = plan.land[i] + coff;
+              dst[nb] = plan.dst[i] + g->coded_part_out_off(q);
+              hh[nb] = plan.part[i][q].hdr;
+              ++nb;
               coff += static_cast<long long>(plan.part[i][q].size);
+              if (q == NP - 2 || q == NP - 1) {
+                TRY(xdecode_n(src, hh, dst, nb));
+                nb = 0;
+              }
             }
             MOE_CUDA(cudaEventRecord(plan.free_ev[i], s));
           } else {

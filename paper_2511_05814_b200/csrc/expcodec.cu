@@ -232,17 +232,28 @@ __device__ __forceinline__ uint32_t spread2(uint32_t cb) {
 // Mode 23 decodes four weights per step in byte lanes (the exponents of a code byte by one
 // subtraction, the bf16 words by byte permutes) and patches the level-1 escapes in place.
 template <int K>
-__global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restrict__ part,
-                                                          uint16_t* __restrict__ out,
+__global__ void __launch_bounds__(kThreads) decode_kernel(const PartBatch pb,
                                                           long long* __restrict__ prof) {
   __shared__ int warp_tot[kThreads / 32];
+  // which part of the batch this CTA decodes (parts laid out back to back in the grid);
+  // constant-indexed parameter reads only (no local copy of the batch)
+  const uint8_t* part = pb.part[0];
+  uint16_t* out = pb.out[0];
+  uint32_t pstart = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxBatch; ++q)
+    if (q < pb.n && blockIdx.x >= pb.start[q]) {
+      part = pb.part[q];
+      out = pb.out[q];
+      pstart = pb.start[q];
+    }
   if (prof && threadIdx.x == 0) {  // in-kernel span: max(LLONG_MAX - CTA start), max(end)
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMax(&prof[0], 0x7fffffffffffffffll - static_cast<long long>(t));
   }
   const PartHeader& h = *reinterpret_cast<const PartHeader*>(part);
-  const uint32_t c = blockIdx.x;
+  const uint32_t c = blockIdx.x - pstart;
   const ChunkEntry ce = reinterpret_cast<const ChunkEntry*>(part + align16(sizeof(PartHeader)))[c];
   const uint64_t first = static_cast<uint64_t>(c) * kChunk + threadIdx.x * 32ull;
   const bool active = first < h.n;
@@ -375,20 +386,40 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restr
   }
 }
 
-moe_status decode(const void* part_dev, const PartHeader& h, uint16_t* out_dev, cudaStream_t s,
-                  long long* prof) {
-  MOE_REQUIRE(h.magic == kMagic && (h.kbits == 3 || h.kbits == 4 || h.kbits == kMode23),
-              "not an exponent-coded part");
-  if (h.n == 0) return MOE_OK;
-  const uint8_t* p = static_cast<const uint8_t*>(part_dev);
-  if (h.kbits == 3)
-    decode_kernel<3><<<h.nch, kThreads, 0, s>>>(p, out_dev, prof);
-  else if (h.kbits == 4)
-    decode_kernel<4><<<h.nch, kThreads, 0, s>>>(p, out_dev, prof);
+moe_status decode_batch(const void* const* parts_dev, const PartHeader* hs, uint16_t* const* outs_dev,
+                        int n, cudaStream_t s, long long* prof) {
+  MOE_REQUIRE(n >= 1 && n <= kMaxBatch, "1..%d parts per decode launch, got %d", kMaxBatch, n);
+  PartBatch pb{};
+  uint32_t grid = 0;
+  int kb = 0, m = 0;
+  for (int i = 0; i < n; ++i) {
+    const PartHeader& h = hs[i];
+    MOE_REQUIRE(h.magic == kMagic && (h.kbits == 3 || h.kbits == 4 || h.kbits == kMode23),
+                "not an exponent-coded part");
+    if (h.n == 0) continue;
+    MOE_REQUIRE(kb == 0 || static_cast<int>(h.kbits) == kb, "parts of one launch share a code mode");
+    kb = static_cast<int>(h.kbits);
+    pb.part[m] = static_cast<const uint8_t*>(parts_dev[i]);
+    pb.out[m] = outs_dev[i];
+    pb.start[m] = grid;
+    grid += h.nch;
+    ++m;
+  }
+  if (m == 0) return MOE_OK;
+  pb.n = m;
+  if (kb == 3)
+    decode_kernel<3><<<grid, kThreads, 0, s>>>(pb, prof);
+  else if (kb == 4)
+    decode_kernel<4><<<grid, kThreads, 0, s>>>(pb, prof);
   else
-    decode_kernel<kMode23><<<h.nch, kThreads, 0, s>>>(p, out_dev, prof);
+    decode_kernel<kMode23><<<grid, kThreads, 0, s>>>(pb, prof);
   MOE_LAUNCHED();
   return MOE_OK;
+}
+
+moe_status decode(const void* part_dev, const PartHeader& h, uint16_t* out_dev, cudaStream_t s,
+                  long long* prof) {
+  return decode_batch(&part_dev, &h, &out_dev, 1, s, prof);
 }
 
 }  // namespace xc

@@ -55,6 +55,16 @@ uint64_t encode(const uint16_t* in, uint64_t n, int mode, uint8_t* out);
 // 2 zeroed int64) receives the launch's in-kernel span (LLONG_MAX - first CTA start, last end)
 moe_status decode(const void* part_dev, const PartHeader& h, uint16_t* out_dev, cudaStream_t s,
                   long long* prof = nullptr);
+// up to kMaxBatch parts of one code mode in a single launch (their chunks back to back)
+constexpr int kMaxBatch = 4;
+struct PartBatch {
+  const uint8_t* part[kMaxBatch];
+  uint16_t* out[kMaxBatch];
+  uint32_t start[kMaxBatch];  // first CTA of each part
+  int n;
+};
+moe_status decode_batch(const void* const* parts_dev, const PartHeader* hs, uint16_t* const* outs_dev,
+                        int n, cudaStream_t s, long long* prof = nullptr);
 
 }  // namespace xc
 }  // namespace moe
