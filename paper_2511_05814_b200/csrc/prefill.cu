@@ -452,11 +452,22 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
         TRY(xc::decode(land, cp[0].hdr, reinterpret_cast<uint16_t*>(dest[i]), s));
         TRY(ffn(1 + i, m.load_rows[i], 1));
         long long coff = static_cast<long long>(cp[0].size);
+        // w2 pieces 1..3 in one launch once the third has landed, the last on its own
+        const void* src[xc::kMaxBatch];
+        uint16_t* dst[xc::kMaxBatch];
+        xc::PartHeader hh[xc::kMaxBatch];
+        int nb = 0;
         for (int q = 1; q < NP; ++q) {
           MOE_CUDA(cudaStreamWaitEvent(s, pf->ev[i * NP + q], 0));
-          TRY(xc::decode(land + coff, cp[q].hdr,
-                         reinterpret_cast<uint16_t*>(dest[i] + g->coded_part_out_off(q)), s));
+          src[nb] = land + coff;
+          dst[nb] = reinterpret_cast<uint16_t*>(dest[i] + g->coded_part_out_off(q));
+          hh[nb] = cp[q].hdr;
+          ++nb;
           coff += static_cast<long long>(cp[q].size);
+          if (q == NP - 2 || q == NP - 1) {
+            TRY(xc::decode_batch(src, hh, dst, nb, s));
+            nb = 0;
+          }
         }
         MOE_CUDA(cudaEventRecord(g->cstage_free[slot], s));
         if (i + nslots < m.n_loads) TRY(issue_coded(i + nslots));
