@@ -5,14 +5,17 @@ every distinct `moesim.toymoe.run_model(config)` call with its activation / spec
 (tests/test_toymoe_gpu.py::test_reference_suite_run_model_configs); every distinct
 `moesim.policies.policy_step` call with its result or error (tests/test_replay_gpu.py::
 test_reference_suite_policy_steps); every distinct `gen_zipf` / `gen_markov` call with its trace
-(tests/test_tracegen.py::test_reference_suite_tracegen_calls).
+(tests/test_tracegen.py::test_reference_suite_tracegen_calls); every gate_select /
+speculate_next / forward_token call with its result or error
+(tests/test_toymoe_gpu.py::test_reference_suite_model_api_calls).
 
 Runs only where /root/reference exists (the build container); nothing is written there.
 
 python tests/golden/make_refsuite_golden.py   -> tests/golden/refsuite_replay.npz,
                                                  tests/golden/refsuite_run_model.npz,
                                                  tests/golden/refsuite_policy_step.jsonl.gz,
-                                                 tests/golden/refsuite_tracegen.npz
+                                                 tests/golden/refsuite_tracegen.npz,
+                                                 tests/golden/refsuite_toymoe_calls.json.gz
 """
 import gzip
 import hashlib
@@ -29,6 +32,7 @@ OUT = Path(__file__).resolve().parent / "refsuite_replay.npz"
 OUT_RM = Path(__file__).resolve().parent / "refsuite_run_model.npz"
 OUT_PS = Path(__file__).resolve().parent / "refsuite_policy_step.jsonl.gz"
 OUT_TG = Path(__file__).resolve().parent / "refsuite_tracegen.npz"
+OUT_TM = Path(__file__).resolve().parent / "refsuite_toymoe_calls.json.gz"
 
 
 def _state(st):
@@ -47,6 +51,7 @@ def main():
     rm_seen, rm_calls = set(), []
     ps_seen, ps_calls = set(), []
     tg_seen, tg_calls = set(), []
+    tm_calls = []
 
     class Record:
         def pytest_configure(self, config):
@@ -111,6 +116,50 @@ def main():
                 return getattr(errors, name, ValueError)("recorded")
 
             pm.policy_step = policy_step
+            def record_call(kind, args, fn):
+                rec = {"kind": kind, **args}
+                try:
+                    res = fn()
+                except Exception as exc:
+                    rec["error"] = type(exc).__name__
+                    tm_calls.append(rec)
+                    raise
+                if kind == "gate_select":
+                    rec["result"] = [[int(e), float(p)] for e, p in res]
+                elif kind == "speculate_next":
+                    rec["result"] = sorted(int(e) for e in res)
+                else:
+                    rec["result"] = {"values": [float(v) for v in res[0].values], "layer": int(res[0].layer),
+                                     "selected": sorted(int(e) for e in res[1])}
+                tm_calls.append(rec)
+                return res
+
+            def gate_args(h, gate, k):
+                return {"h": [float(v) for v in h.values], "h_layer": int(h.layer),
+                        "w": np.asarray(gate.weights, np.float64).tolist(),
+                        "b": None if gate.bias is None else np.asarray(gate.bias, np.float64).tolist(), "k": int(k)}
+
+            stock_gs, stock_sn, stock_ft = tm.gate_select, tm.speculate_next, tm.forward_token
+            tm.gate_select = lambda h, gate, k: record_call("gate_select", gate_args(h, gate, k),
+                                                            lambda: stock_gs(h, gate, k))
+            tm.speculate_next = lambda h, gate, k: record_call("speculate_next", gate_args(h, gate, k),
+                                                               lambda: stock_sn(h, gate, k))
+
+            def forward_token(model, h_in, layer):
+                c = model.config
+                args = {"config": [c.shape.num_layers, c.shape.num_experts, c.shape.top_k, c.hidden_dim,
+                                   float(c.mixing_scale), float(c.skew), c.seed, c.tokens],
+                        "h": [float(v) for v in h_in.values], "h_layer": int(h_in.layer), "layer": int(layer),
+                        # the model's actual arrays (tests may hand-build or alter them)
+                        "weights": {"gate_w": [np.asarray(g.weights, np.float64).tolist() for g in model.gates],
+                                    "gate_b": [None if g.bias is None else np.asarray(g.bias, np.float64).tolist()
+                                               for g in model.gates],
+                                    "mixing": np.asarray(model.mixing, np.float64).tolist(),
+                                    "w1": np.asarray(model.expert_w1, np.float64).tolist(),
+                                    "w2": np.asarray(model.expert_w2, np.float64).tolist()}}
+                return record_call("forward_token", args, lambda: stock_ft(model, h_in, layer))
+
+            tm.forward_token = forward_token
             import moesim.tracegen as tg
 
             for fname in ("gen_zipf", "gen_markov"):
@@ -159,6 +208,9 @@ def main():
     np.savez_compressed(OUT_TG, meta=np.array([m for m, _ in tg_calls], np.float64),
                         acts=np.concatenate([a.reshape(-1) for _, a in tg_calls]).astype(np.int16))
     print(f"{len(tg_calls)} distinct tracegen calls -> {OUT_TG} ({OUT_TG.stat().st_size / 1e6:.2f} MB)")
+    with open(OUT_TM, "wb") as raw, gzip.GzipFile(fileobj=raw, mode="wb", mtime=0) as f:
+        f.write(json.dumps(tm_calls, sort_keys=True).encode())
+    print(f"{len(tm_calls)} gate_select / speculate_next / forward_token calls -> {OUT_TM}")
 
 
 if __name__ == "__main__":

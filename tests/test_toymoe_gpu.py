@@ -213,3 +213,52 @@ def test_reference_suite_run_model_configs():
         assert np.array_equal(s.guessed, guessed) and np.array_equal(s.actual, actual), key
         n += 1
     assert n == 100
+
+
+def test_reference_suite_model_api_calls():
+    """Every gate_select / speculate_next / forward_token call of the reference's own test suite
+    (tests/golden/refsuite_toymoe_calls.json.gz, the reference's results and errors recorded):
+    same ids / selected sets, probabilities and hidden states within 1e-12 relative (fp64 on the
+    device vs numpy's BLAS summation order), the same exception classes."""
+    from paper_2511_05814_b200 import errors
+
+    import gzip
+
+    with gzip.open(GOLDEN / "refsuite_toymoe_calls.json.gz", "rt") as f:
+        calls = json.load(f)
+    assert len(calls) >= 13
+    for rec in calls:
+        h = HiddenState(np.array(rec["h"], dtype=np.float64), rec["h_layer"])
+        if rec["kind"] == "forward_token":
+            L, E, K, d, alpha, skew, seed, T = rec["config"]
+            model, _ = ToyMoeModel.build(ToyModelConfig(ModelShape(int(L), int(E), int(K)), hidden_dim=int(d),
+                                                        mixing_scale=alpha, skew=skew, seed=int(seed),
+                                                        tokens=int(T)))
+            w = rec["weights"]   # the arrays the reference test actually used
+            model.gates = tuple(GatingNetwork(np.array(gw), None if gb is None else np.array(gb))
+                                for gw, gb in zip(w["gate_w"], w["gate_b"]))
+            model.mixing = np.array(w["mixing"])
+            model.expert_w1 = np.array(w["w1"])
+            model.expert_w2 = np.array(w["w2"])
+            call = lambda: forward_token(model, h, rec["layer"])  # noqa: E731
+        else:
+            gate = GatingNetwork(np.array(rec["w"], dtype=np.float64),
+                                 None if rec["b"] is None else np.array(rec["b"], dtype=np.float64))
+            fn = gate_select if rec["kind"] == "gate_select" else speculate_next
+            call = lambda: fn(h, gate, rec["k"])  # noqa: E731
+        if "error" in rec:
+            exc = getattr(errors, rec["error"], None) or {"FloatingPointError": FloatingPointError,
+                                                          "ValueError": ValueError}.get(rec["error"], Exception)
+            with pytest.raises(exc):
+                call()
+            continue
+        got = call()
+        if rec["kind"] == "gate_select":
+            assert [e for e, _ in got] == [e for e, _ in rec["result"]], rec
+            np.testing.assert_allclose([p for _, p in got], [p for _, p in rec["result"]], rtol=1e-12)
+        elif rec["kind"] == "speculate_next":
+            assert sorted(got) == rec["result"], rec
+        else:
+            out, sel = got
+            assert sorted(sel) == rec["result"]["selected"] and out.layer == rec["result"]["layer"]
+            np.testing.assert_allclose(out.values, rec["result"]["values"], rtol=1e-12, atol=1e-12)
