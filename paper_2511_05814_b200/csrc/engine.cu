@@ -459,11 +459,11 @@ struct CodedEntry {
 constexpr uint64_t kCodedMagic = 0x4d4f45584332ull;  // "MOEXC2"
 
 // Sizes of every part from the raw store (the layout of a coded segment).  Parts of an expert:
-// w1|w3, then kCodedBParts row pieces of w2, contiguous.
+// w1|w3, then kCodedBParts row pieces of w2 (the last short), contiguous.
 void part_span(const moe_engine* g, int part, long long* first, long long* n) {
-  const long long na = 2ll * g->f * g->dpad, pb = 1ll * (g->dpad / moe_engine::kCodedBParts) * g->f;
-  *first = part == 0 ? 0 : na + (part - 1) * pb;
-  *n = part == 0 ? na : pb;
+  const long long na = 2ll * g->f * g->dpad;
+  *first = part == 0 ? 0 : na + 1ll * g->coded_piece_row0(part) * g->f;
+  *n = part == 0 ? na : 1ll * g->coded_piece_rows(part) * g->f;
 }
 
 // Raw bf16 words of expert e of a layer whose blocks start at `raw_layer` ([E][expert]).
@@ -506,8 +506,8 @@ void write_seg_table(moe_engine* g, char* seg) {
 }
 
 moe_status plan_coded(moe_engine* g) {
-  MOE_REQUIRE(g->dpad % moe_engine::kCodedBParts == 0, "compressed transfers need hidden_dim %% %d == 0",
-              moe_engine::kCodedBParts);
+  MOE_REQUIRE(g->coded_head_rows() >= 32 && g->coded_piece_rows(moe_engine::kCodedBParts) >= 32,
+              "compressed transfers need hidden_dim >= 256");
   MOE_REQUIRE(!g->coded_only, "a coded-only engine has no raw store to plan from");
   const int E = g->cfg.num_experts, NP = moe_engine::kCodedParts;
   const size_t n = static_cast<size_t>(g->SL) * E * NP;

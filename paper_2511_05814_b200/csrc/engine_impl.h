@@ -155,10 +155,17 @@ struct moe_engine {
   const CPart* coded_parts(int layer, int expert) const {
     return &ctab[(static_cast<size_t>(layer % SL) * cfg.num_experts + expert) * kCodedParts];
   }
+  // w2 row pieces: the first kCodedBParts - 1 equal, the last short (~1/8 of w2), since only
+  // the last is decoded and reduced after a step's final byte lands
+  int coded_head_rows() const { return dpad * 7 / 24 / 32 * 32; }
+  int coded_piece_row0(int p) const { return (p - 1) * coded_head_rows(); }  // p = 1..kCodedBParts
+  int coded_piece_rows(int p) const {
+    return p < kCodedBParts ? coded_head_rows() : dpad - (kCodedBParts - 1) * coded_head_rows();
+  }
   // decoded bytes of part p and its offset in the expert block
   long long coded_part_out_off(int p) const {
-    const long long a = 2ll * f * dpad * 2, pb = 1ll * (dpad / kCodedBParts) * f * 2;
-    return p == 0 ? 0 : a + (p - 1) * pb;
+    const long long a = 2ll * f * dpad * 2;
+    return p == 0 ? 0 : a + 1ll * coded_piece_row0(p) * f * 2;
   }
   char* cstore = nullptr;                 // pinned host (private) or a registered shared segment
   bool cstore_external = false;
