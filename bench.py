@@ -14,8 +14,9 @@ e2e      the same decode through the public API (OffloadEngine.decode on a host 
          H2D of the token's input and D2H of its output inside the timed region; the timed
          tokens replayed from the same cold + warm-up cache state (identical misses).
 reference arm (--impl reference): the oracle port of the reference path (numpy fp64 in the
-         reference's `h @ W` layout, all host threads) on the same config, per-token time
-         sampled on a bounded subset of layers and scaled by L / L_sample.
+         reference's `h @ W` layout, all host threads) on the same config and token stream:
+         32 tokens through the first 8 of the 32 layers (every layer does identical work),
+         best of 3, per-token time scaled by L / 8 (`layers_sampled`, `scale` say so).
 
 Run: python bench.py [--gpus N --steps K --warmup W]; multi-GPU via torch.distributed.run
 (independent request streams, one engine per GPU, no collective on the hot path).
@@ -41,6 +42,41 @@ METRIC = "decode tokens/s per GPU and cache hit rate (LRU vs LFU vs prefetch) at
 L, E, K, D, F = 32, 8, 2, 4096, 14336
 EXPERT_BYTES = 3 * F * D * 2                       # 352,321,536
 HBM_BYTES_PER_TOKEN = L * (2 * D * D + 2 * D * E + K * 3 * D * F * 2)  # 23,624,417,792
+# (L, E, K, d, f) of the two benchmarked shapes (BASELINE.json configs[1] / [4])
+MODELS = {"mixtral_8x7b": (32, 8, 2, 4096, 14336), "mixtral_8x22b": (56, 8, 2, 6144, 16384)}
+TIE_TOL = 1e-3   # top-k logit margin below which a selection is a stated near-tie (north star)
+
+
+def workload_config(model: str, world: int, cache_size: int, policy: str) -> dict:
+    """The workload both arms run, key for key (only the line's impl / dtype differ).  The
+    synthetic model's departures from SURVEY 8d's literal recipe are part of the workload."""
+    Lm, Em, Km, Dm, Fm = MODELS[model]
+    hbm = Lm * (2 * Dm * Dm + 2 * Dm * Em + Km * 3 * Dm * Fm * 2)
+    return {
+        "workload": f"{'configs[4]' if model == 'mixtral_8x22b' else 'configs[1]'}: {model}-shaped "
+                    f"batch-1 decode, {policy} cache {cache_size}/layer, experts in host DRAM",
+        "model": f"{model}-shape (L={Lm},E={Em},K={Km},d={Dm},f={Fm}), random-init",
+        "global_batch": world, "seq_len": 1, "parallelism": f"replicas x{world}",
+        "cache_size": cache_size, "policy": policy,
+        "l2": f"inputs larger than L2: each step streams >= {hbm / 1e9:.1f} GB of weights "
+              "(mixing + 2 experts per layer) through HBM",
+        "tokens": "counter-hash N(0,1)-shaped f32 inputs, one independent token per step",
+        "synthetic_model": {
+            "weights": "counter-hash Irwin-Hall (sum of 4 uniforms, bell-shaped) bf16, std as SURVEY 8d",
+            "gate_bias_std": "0.25 (SURVEY 8d: 1.0 -- bias-dominated routing under RMSNorm, DESIGN 5)",
+            "rms_norm": "unit-scale RMSNorm (eps 1e-5) before gate and experts (not in toymoe; "
+                        "a 32-layer SwiGLU residual overflows without it, DESIGN 5)",
+            "routing": "softmax over E, top-k by logit (ties to the lower id), unrenormalised "
+                       "(toymoe.py:93-115)",
+            "host_store": ("one node-shared pinned copy per node, page-locked by every replica"
+                           if world > 1 else "one pinned host copy for the GPU"),
+        },
+    }
+
+
+def fp64_layer_bytes(shape) -> int:
+    _, Em, _, Dm, Fm = shape
+    return Em * 3 * Dm * Fm * 8 + Dm * Dm * 8 + 2 * Em * Dm * 8
 
 
 def parse_args():
@@ -55,11 +91,14 @@ def parse_args():
                    help="headline = the first; policy[+prefetch][@cache_size]. Default: configs[1] "
                         "and [2] (LRU, LFU, LFU+prefetch at C=4; LFU, LFU+prefetch at C=2 and 6) "
                         "for 8x7B, configs[4] (LFU+prefetch at C=4) for 8x22B")
-    p.add_argument("--e2e-steps", type=int, default=16,
-                   help="tokens replayed through the public API (<= --steps; same stream and "
-                        "starting cache state as the timed region)")
-    p.add_argument("--cpu-sample-tokens", type=int, default=16)
-    p.add_argument("--cpu-sample-layers", type=int, default=1)
+    p.add_argument("--e2e-steps", type=int, default=-1,
+                   help="tokens replayed through the public API (-1 = all --steps timed tokens, "
+                        "0 = skip; same stream and starting cache state as the timed region)")
+    p.add_argument("--cpu-sample-tokens", type=int, default=32)
+    p.add_argument("--cpu-sample-layers", type=int, default=8,
+                   help="layers the CPU path times (fp64 experts of 8 layers: 90 GB for 8x7B; "
+                        "clamped to what fits in 45%% of free host RAM)")
+    p.add_argument("--cpu-repeats", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--layers", type=int, default=0,
                    help="fewer layers than the model (invalidates the headline; diagnostics)")
@@ -85,6 +124,9 @@ def parse_args():
     p.add_argument("--replay-tokens", type=int, default=8192)
     p.add_argument("--shared-store", action="store_true",
                    help="host experts in a node-shared segment (automatic when WORLD_SIZE > 1)")
+    p.add_argument("--section-8x22b", type=int, default=1,
+                   help="configs[4] section after the configs[1] run: 8x22B engine in a child "
+                        "bench (LFU + prefetch, C=4), summarised in the line (0 = skip)")
     return p.parse_args()
 
 
@@ -280,78 +322,71 @@ def committed_ffn_traffic():
 
 # ---- CPU path (oracle port of the reference, test-infrastructure only) -------------------
 
-def cpu_reference_sample(seed: int, tokens: int, layers: int, warmup: int = 1,
-                         shape=(L, E, K, D, F), layout: str = "ref") -> dict:
-    """Time the oracle port on the first `tokens` tokens of the same stream through `layers`
-    layers; return tokens/s scaled to the full model depth.  layout "ref": the reference's
-    arithmetic (numpy fp64, `h @ W`, BASELINE.md variant (i)); "dev": the tuned variant (ii),
-    fp32 `W h` GEMVs in the weights' row-major (nn.Linear) layout.  All host BLAS threads.
-    Weights are materialised (untimed) by a first pass."""
+def cpu_reference_sample(seed: int, tokens: int, layers: int, warmup: int, shape=(L, E, K, D, F),
+                         layout: str = "ref", repeats: int = 3, cache_size: int = 4,
+                         policy: int = 0, t_base: int = 0):
+    """Time the oracle port on the stream's timed tokens [warmup, warmup + tokens) through the
+    first `layers` layers, token-major like run_model (toymoe.py:175-185) plus the policy
+    replay (kernels.py:60-147); best of `repeats`; tokens/s scaled to the full depth by
+    L / layers (every layer does identical work).  layout "ref": the reference's arithmetic
+    (numpy fp64, `h @ W`, BASELINE.md variant (i)); "dev": the tuned variant (ii), fp32 `W h`
+    GEMVs on the weights' row-major (nn.Linear) layout.  All host BLAS threads.  The weights
+    are materialised first (untimed).  Returns (baseline dict, acts (tokens, layers, K))."""
     import numpy as np
 
     import oracle
     from oracle.model import replay_layers
 
-    L, E, K, D, F = shape
-    alpha = 0.1 * math.sqrt(16 / D)
-    ref = oracle.MixtralRef(L, E, K, D, F, alpha, seed=seed, layout=layout,
+    Ls, Es, Ks, Ds, Fs = shape
+    per = fp64_layer_bytes(shape) * (1.0 if layout == "ref" else 0.5)
+    layers = max(1, min(layers, Ls, int(0.45 * host_available_bytes() // per)))
+    alpha = 0.1 * math.sqrt(16 / Ds)
+    ref = oracle.MixtralRef(Ls, Es, Ks, Ds, Fs, alpha, seed=seed, layout=layout,
                             layers=list(range(layers)), rms_norm=True)
-    X = oracle.MixtralRef.inputs(seed, tokens + warmup, D)
+    X = oracle.MixtralRef.inputs(seed, tokens, Ds, t0=t_base + warmup)
     t_gen = time.perf_counter()
-    ref.decode(X[: tokens + warmup])          # materialises exactly the experts it routes to
+    ref.materialize()
     t_gen = time.perf_counter() - t_gen
-    t0 = time.perf_counter()
-    _, acts = ref.decode(X[warmup: warmup + tokens])
-    replay_layers(acts, E, 4, 0)               # the policy step of the reference (numba-like)
-    dt = time.perf_counter() - t0
-    per_token = dt / tokens * (L / layers)
-    return {"value": 1.0 / per_token, "unit": "tokens/s", "cores": os.cpu_count(),
-            "kind": "port",
-            "sample": f"{tokens} tokens x {layers} of {L} layers ("
-                      + ("numpy fp64 `h @ W`" if layout == "ref" else "numpy fp32 `W h`, row-major weights")
-                      + f", {os.cpu_count()} BLAS threads), scaled by {L}/{layers}; "
-                      f"{dt:.1f} s timed, {t_gen:.1f} s untimed weight materialisation",
-            "seconds_timed": dt}
+    times, acts = [], None
+    for _ in range(max(1, repeats)):
+        t0 = time.perf_counter()
+        _, acts = ref.decode(X)
+        replay_layers(acts, Es, cache_size, policy)
+        times.append(time.perf_counter() - t0)
+    del ref
+    best = min(times)
+    per_token = best / tokens * (Ls / layers)
+    what = "numpy fp64 `h @ W`" if layout == "ref" else "numpy fp32 `W h`, row-major weights"
+    return ({"value": 1.0 / per_token, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+             "sample": f"{tokens} tokens x {layers} of {Ls} layers ({what}, {os.cpu_count()} BLAS "
+                       f"threads) + the policy replay, best of {len(times)}, scaled by {Ls}/{layers}",
+             "layers_sampled": layers, "scale": Ls / layers, "tokens": tokens,
+             "repeats": len(times), "best_s": best, "seconds_timed": sum(times),
+             "materialise_s_untimed": t_gen}, acts)
 
 
 def run_reference(args, world, rank, local):
     """--impl reference: the reference's CPU path (oracle port) on the same config."""
     if rank != 0:
         return
-    import numpy as np  # noqa: F401
-
-    import oracle
-    from oracle.model import replay_layers
-
-    alpha = 0.1 * math.sqrt(16 / D)
-    layers = args.cpu_sample_layers
-    ref = oracle.MixtralRef(L, E, K, D, F, alpha, seed=args.seed, layout="ref",
-                            layers=list(range(layers)), rms_norm=True)
-    n = args.warmup + args.steps
-    X = oracle.MixtralRef.inputs(args.seed, n, D)
-    ref.decode(X[: args.warmup])             # warm-up steps (materialise weights, untimed)
-    ref.decode(X[args.warmup:])              # make sure every expert the timed steps use exists
-    t0 = time.perf_counter()
-    _, acts = ref.decode(X[args.warmup:])
-    replay_layers(acts, E, args.cache_size, 0)
-    dt = time.perf_counter() - t0
-    per_token = dt / args.steps * (L / layers)
-    value = 1.0 / per_token
+    shape = MODELS[args.model]
+    policy = "lfu+prefetch" if args.model == "mixtral_8x22b" else "lru"
+    cpu, _ = cpu_reference_sample(args.seed, args.cpu_sample_tokens, args.cpu_sample_layers,
+                                  args.warmup, shape=shape, repeats=args.cpu_repeats,
+                                  cache_size=args.cache_size, policy=1 if policy.startswith("lfu") else 0)
+    value = cpu["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_token * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "Mixtral-8x7B-shaped batch-1 decode, LRU cache 4/layer",
-                   "model": "mixtral-8x7b-shape (L=32,E=8,K=2,d=4096,f=14336), random-init",
-                   "cache_size": args.cache_size, "policy": "lru"},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(),
-                         "kind": "port",
-                         "sample": f"{args.steps} tokens x {layers} of {L} layers per run, "
-                                   f"scaled by {L}/{layers} (oracle/model.py MixtralRef, "
-                                   "numpy fp64 reference layout)"},
+        "config": workload_config(args.model, world, args.cache_size, policy),
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "note": f"each step = {cpu['tokens']} timed tokens x {cpu['layers_sampled']} layers on the "
+                f"host (the driver's --steps/--warmup size nothing here); value = tokens/s of the "
+                f"full {shape[0]}-layer model from the measured per-layer time (x {cpu['scale']:g})",
     }
     print(json.dumps(line), flush=True)
 
@@ -366,6 +401,57 @@ def speculation_precision(rec) -> float:
         return None
     tp = sum(len(set(g[t, l]) & set(a[t, l])) for t in range(g.shape[0]) for l in range(g.shape[1]))
     return tp / g.size
+
+
+def early_precision(rec, early):
+    """Precision of the early guesses the prefetch acted on: |early(t, l) & acts(t, l+1)| / K,
+    the reference's speculation precision (metrics.py:217-249) applied to gate_{l+1}(h'_l)."""
+    a = rec["acts"][:, 1:, :]
+    if early is None or early.size == 0:
+        return None
+    tp = sum(len(set(early[t, l]) & set(a[t, l])) for t in range(a.shape[0]) for l in range(a.shape[1]))
+    return tp / early.size
+
+
+def variant_parity(rec, gaps, early, s0, s1, policy, csize, nb, n_exp):
+    """Parity of one timed variant, checked here against the oracle (bench's checker role):
+    the live cache trace against the C oracle's replay of the engine's own selections
+    (kernels.py:60-147); with prefetch, the issued / used decisions against
+    oracle.prefetch_oracle; the selections' near-tie margins as the engine recorded them."""
+    import numpy as np
+
+    from oracle.model import prefetch_oracle, replay_layers
+
+    code, df, dp = policy.device_params()
+    rb, ev = replay_layers(rec["acts"], n_exp, csize, code, df, dp)
+    out = {"trace_equals_oracle_replay": bool(
+               np.array_equal(rec["resident_before"], np.transpose(rb, (1, 0, 2)))
+               and np.array_equal(rec["evicted"], np.transpose(ev, (1, 0, 2)))),
+           "near_ties_lt_1e-3": int((gaps < TIE_TOL).sum()),
+           "min_topk_gap": float(np.nanmin(gaps)) if gaps.size else None,
+           "steps": int(gaps.size)}
+    if early is not None:
+        issued, used = prefetch_oracle(rec["acts"], early, rec["resident_before"], nb)
+        out["prefetch_issued_used_equal_oracle"] = bool(
+            int(issued.sum()) == s1["prefetch_issued"] - s0["prefetch_issued"]
+            and int(used.sum()) == s1["prefetch_used"] - s0["prefetch_used"])
+    return out
+
+
+def fp64_selection_check(head_rec, head_gaps, cpu_acts):
+    """The headline's expert selections against the fp64 oracle's on the same tokens: the CPU
+    baseline decoded the headline's timed tokens through the first layers in the reference's
+    arithmetic, so its selections are compared step by step (toymoe.py:114 order)."""
+    import numpy as np
+
+    n = min(head_rec["acts"].shape[0], cpu_acts.shape[0])
+    ls = cpu_acts.shape[1]
+    eng = head_rec["acts"][:n, :ls]
+    diff = (eng != cpu_acts[:n]).any(-1)
+    near = head_gaps[:n, :ls] < TIE_TOL
+    return {"tokens": n, "layers": ls, "steps": int(n * ls), "equal_steps": int((~diff).sum()),
+            "mismatches": int(diff.sum()), "mismatches_at_near_ties": int((diff & near).sum()),
+            "all_equal": bool(not diff.any())}
 
 
 def parse_variant(v: str, default_c: int):
@@ -429,15 +515,20 @@ def run_ours(args, world, rank, local):
                   max_tokens=4096, device=gpu, store_layers=store_layers,
                   prefetch_buffers=pf_bufs, compress=compress)
     D, F, EB = cfg.hidden_dim, cfg.ffn_dim, cfg.expert_bytes
-    cpu = cpu32 = None
+    cpu = cpu32 = cpu_acts = None
+    head_policy, _, _ = parsed[0]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        shape = (base_cfg.num_layers, base_cfg.num_experts, base_cfg.top_k, base_cfg.hidden_dim,
-                 base_cfg.ffn_dim)
+        shape = MODELS[args.model]
         # (i) the reference's arithmetic (the baseline); (ii) a tuned fp32 port beside it
-        # (report both).  configs[4] is bounded to 16 tokens (2.4 GB fp64 experts)
-        ntok = args.cpu_sample_tokens if args.model == "mixtral_8x7b" else 16
-        cpu = cpu_reference_sample(args.seed, ntok, args.cpu_sample_layers, shape=shape)
-        cpu32 = cpu_reference_sample(args.seed, ntok, args.cpu_sample_layers, shape=shape, layout="dev")
+        # (report both).  Same token stream as the engine's timed tokens: the
+        # fp64 selections double as a full-scale parity check of the headline's first layers
+        code = head_policy.device_params()[0]
+        cpu, cpu_acts = cpu_reference_sample(args.seed, args.cpu_sample_tokens, args.cpu_sample_layers,
+                                             args.warmup, shape=shape, repeats=args.cpu_repeats,
+                                             cache_size=parsed[0][1], policy=code)
+        cpu32, _ = cpu_reference_sample(args.seed, args.cpu_sample_tokens, args.cpu_sample_layers,
+                                        args.warmup, shape=shape, layout="dev",
+                                        repeats=args.cpu_repeats, cache_size=parsed[0][1], policy=code)
     pcie_peak = h2d_peak_gbs(dev)
 
     t_setup = time.perf_counter()
@@ -533,6 +624,12 @@ def run_ours(args, world, rank, local):
         demand_link = s1["demand_link_bytes"] - s0["demand_link_bytes"]
         busy = s1["copy_busy_ms"] - s0["copy_busy_ms"]
         rec = eng.records(t0_tok + args.warmup, args.steps)
+        gaps = eng.record_gaps(t0_tok + args.warmup, args.steps)
+        early = eng.record_early_guesses(t0_tok + args.warmup, args.steps) if prefetch else None
+        nb = csize + ((cfg.prefetch_buffers or cfg.top_k) if prefetch else 0)
+        par = variant_parity(rec, gaps, early, s0, s1, policy, csize, nb, cfg.num_experts)
+        if headline:
+            head_rec, head_gaps = rec, gaps
         results[v] = {
             "policy": str(policy), "cache_size": csize, "prefetch": prefetch,
             "tokens_per_s": tps,
@@ -549,14 +646,17 @@ def run_ours(args, world, rank, local):
             "prefetch_used": s1["prefetch_used"] - s0["prefetch_used"],
             "prefetch_wasted_bytes": s1["prefetch_wasted_bytes"] - s0["prefetch_wasted_bytes"],
             "speculation_precision": speculation_precision(rec),
+            "early_guess_precision": early_precision(rec, early) if prefetch else None,
             "check_hits_from_records": int(sum(
                 int(rec["resident_before"][t, l, rec["acts"][t, l]].sum())
                 for t in range(args.steps) for l in range(nl))) == hits,
+            "parity": par,
         }
-        if headline and args.e2e_steps > 0:
+        ne = args.steps if args.e2e_steps < 0 else min(args.e2e_steps, args.steps)
+        if headline and ne > 0:
             # public API, host buffers: H2D of the input and D2H of the output every step, on the
-            # same token stream from the same (cold + warm-up) cache state as the timed region
-            ne = min(args.e2e_steps, args.steps)
+            # same token stream from the same (cold + warm-up) cache state as the timed region:
+            # exactly the timed tokens, so its misses and copies are the headline's
             xs = inputs[args.warmup: args.warmup + ne].cpu().numpy()
             eng.reset()
             eng.decode_device(inputs[: args.warmup])
@@ -568,7 +668,8 @@ def run_ours(args, world, rank, local):
                 eng.decode(xs[i: i + 1])
             e_tps, _, _ = replicas.reduce_timing((time.perf_counter() - t0) * 1e3, ne, world)
             e2e = {"value": e_tps, "unit": "tokens/s",
-                   "h2d_bytes_per_step": D * 4, "d2h_bytes_per_step": D * 4}
+                   "h2d_bytes_per_step": D * 4, "d2h_bytes_per_step": D * 4,
+                   "tokens": ne, "same_tokens_as_timed_region": ne == args.steps}
     trace_driven = run_trace_driven(args, eng, inputs, stream, world) if args.trace_variants else None
     prefill = None
     if args.prefill_tokens > 0:
@@ -627,16 +728,9 @@ def run_ours(args, world, rank, local):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (counter-hash random-init weights and token inputs)",
-        "config": {
-            "workload": f"{'configs[4]' if args.model == 'mixtral_8x22b' else 'configs[1]'}: "
-                        f"{args.model}-shaped bf16 batch-1 decode, {variants[0]} cache "
-                        f"{head['cache_size']}/layer, experts in pinned host DRAM",
-            "model": f"{args.model}-shape (L={nl},E={cfg.num_experts},K={cfg.top_k},d={D},f={F}),"
-                     " random-init",
-            "global_batch": world, "seq_len": 1, "parallelism": f"replicas x{world}",
-            "cache_size": head["cache_size"], "policy": variants[0],
-            "l2": "inputs larger than L2: each step streams >=23.6 GB of weights through HBM",
-            "setup_s": round(t_setup, 1), "shared_store": store is not None,
+        "config": workload_config(args.model, world, head["cache_size"], variants[0]),
+        "engine": {
+            "layers_run": nl, "setup_s": round(t_setup, 1), "shared_store": store is not None,
             "host_store_layers": cfg.host_store_layers,
             "expert_transfer": ("exponent-coded bf16, lossless (csrc/expcodec.cuh), "
                                 f"{compressed_ratio:.3f} of the raw bytes"
@@ -682,10 +776,6 @@ def run_ours(args, world, rank, local):
         "kernel_ms_per_step": {k: ktimes[k] / args.steps for k in ("mix_ms", "gate_ms", "ffn_ms",
                                                                  "finalize_ms", "xdec_ms",
                                                                  "ffn_kernel_ms", "xdec_kernel_ms")},
-        "gpu_launches": launches_timed,
-        "clocks": clocks,
-        "e2e": e2e,
-        "cpu_baseline": cpu,
     }
     # the dominant kernel = the larger in-kernel device time over the timed region
     ffn_k, dec_k = ktimes.get("ffn_kernel_ms", 0.0), ktimes.get("xdec_kernel_ms", 0.0)
@@ -695,8 +785,6 @@ def run_ours(args, world, rank, local):
                                        f"{ffn_k / args.steps:.2f} ms/step, exponent decode "
                                        f"{dec_k / args.steps:.2f} ms/step; the other kernel's object "
                                        f"is roofline_{'ffn' if dom == 'decode' else 'decode'}")
-    if cpu:
-        line["speedup_vs_cpu_port"] = head["tokens_per_s"] / cpu["value"]
     if cpu32:
         line["cpu_baseline_fp32"] = cpu32
         line["speedup_vs_cpu_port_fp32"] = head["tokens_per_s"] / cpu32["value"]
@@ -720,7 +808,77 @@ def run_ours(args, world, rank, local):
         prefill["gemm_isolated"] = gemm_iso
         prefill["gemm_isolated_tensor_bound"] = gemm_iso_t
         line["prefill"] = prefill
+    # ---- the line's tail: the driver keeps the end of stdout, so the contract keys and the
+    # metric's comparison table come last, compact
+    roof = line.pop("roofline")
+    line["roofline"] = {k: roof[k] for k in ("kernel", "bound", "achieved", "peak", "unit", "frac",
+                                             "traffic", "achieved_in_kernel", "frac_in_kernel")
+                        if k in roof}
+    line["roofline"]["detail"] = "roofline_decode / roofline_ffn above"
+    line["cpu_baseline"] = cpu
+    line["e2e"] = e2e
+    line["clocks"] = clocks
+    line["gpu_launches"] = launches_timed
+    pars = [r["parity"] for r in results.values()]
+    parity = {
+        "traces_equal_oracle_replay_all_variants": all(p["trace_equals_oracle_replay"] for p in pars),
+        "prefetch_issued_used_equal_oracle": all(p.get("prefetch_issued_used_equal_oracle", True)
+                                                 for p in pars),
+        "near_ties_lt_1e-3": sum(p["near_ties_lt_1e-3"] for p in pars),
+        "steps_checked": sum(p["steps"] for p in pars),
+        "min_topk_gap": min(p["min_topk_gap"] for p in pars),
+    }
+    if cpu_acts is not None:
+        parity["fp64_selections_headline"] = fp64_selection_check(head_rec, head_gaps, cpu_acts)
+    parity["full_depth_tests"] = ("tests/test_fullscale_gpu.py: configs[1] 32 layers and the "
+                                  "configs[4] shape vs the fp64 oracle")
+    line["variants_summary"] = {
+        v: {"tok_s": round(r["tokens_per_s"], 3), "hit": round(r["hit_rate"], 4),
+            "pcie_frac": round(r["pcie_frac_of_measured_h2d_peak"], 3),
+            "pcie_bound_tok_s": round(r["pcie_bound_tokens_per_s"], 2),
+            "spec_prec": None if r["speculation_precision"] is None else round(r["speculation_precision"], 3),
+            **({"early_prec": round(r["early_guess_precision"], 3),
+                "pf_issued": r["prefetch_issued"], "pf_used": r["prefetch_used"],
+                "pf_wasted_GB": round(r["prefetch_wasted_bytes"] / 1e9, 2)} if r["prefetch"] else {})}
+        for v, r in results.items()}
+    line["parity"] = parity
+    if cpu:
+        line["speedup_vs_cpu_port"] = head["tokens_per_s"] / cpu["value"]
+    if args.model == "mixtral_8x7b" and args.section_8x22b and world == 1:
+        line["mixtral_8x22b"] = run_8x22b_section(args)
     print(json.dumps(line), flush=True)
+
+
+def run_8x22b_section(args):
+    """configs[4] in a child bench process (its own engine, host store and fp64 sample; the
+    parent's 8x7B engine and stores are already released): LFU + prefetch at C = 4, the child's
+    full line kept in its `detail`, the comparison numbers summarised here."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--model", "mixtral_8x22b",
+           "--steps", str(args.steps), "--warmup", str(args.warmup), "--seed", str(args.seed),
+           "--cpu-sample-layers", str(min(2, args.cpu_sample_layers)), "--cpu-sample-tokens", "16",
+           "--cpu-repeats", "1",
+           "--prefill-tokens", "0", "--tiny-tokens", "0", "--replay-streams", "0",
+           "--trace-variants", "", "--section-8x22b", "0"]
+    if args.layers:
+        cmd += ["--layers", str(args.layers)]
+    if args.no_cpu_baseline:
+        cmd += ["--no-cpu-baseline"]
+    t0 = time.perf_counter()
+    out = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
+    wall = time.perf_counter() - t0
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    if out.returncode != 0 or not lines:
+        return {"error": f"rc={out.returncode}: {out.stderr[-400:]}"}
+    d = json.loads(lines[-1])
+    v = d["variants"][next(iter(d["variants"]))]
+    return {"workload": d["config"]["workload"], "tok_s": d["value"],
+            "e2e_tok_s": (d.get("e2e") or {}).get("value"), "hit": round(d["hit_rate"], 4),
+            "pcie_frac": round(d["pcie"]["frac"], 3),
+            "cpu_tok_s": (d.get("cpu_baseline") or {}).get("value"),
+            "speedup_vs_cpu_port": d.get("speedup_vs_cpu_port"),
+            "host_store_layers": d["engine"]["host_store_layers"], "setup_s": d["engine"]["setup_s"],
+            "pf_issued": v["prefetch_issued"], "pf_used": v["prefetch_used"],
+            "parity": d["parity"], "child_wall_s": round(wall, 1)}
 
 
 def run_tiny(args):

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define MOE_ABI_VERSION 3
+#define MOE_ABI_VERSION 4
 
 typedef int32_t moe_status;
 enum {
@@ -288,6 +288,17 @@ moe_status moe_engine_sync(moe_engine* eng);
 moe_status moe_engine_records(moe_engine* eng, int64_t t0, int64_t T, int64_t* acts,
                               int64_t* guessed, uint8_t* resident_before, uint8_t* evicted,
                               float* probs);
+
+/* Per-step margins and early guesses of the same steps (ABI 4); either output may be NULL.
+ *   gaps (T, L) f32: the route logit of the K-th selected expert minus the largest unselected
+ *     logit (toymoe.py:99-115 ranks by logit desc, ties to the lower id; a margin below the fp
+ *     tolerance marks a selection the fp64 reference could order differently).  +inf when
+ *     K == E, NaN for trace-driven steps.
+ *   early (T, L-1, K) int64: the early guess for layer l+1 made at step (t, l) (gate_{l+1} on
+ *     h'_l, ascending) that drove its speculative prefetch; -1 with prefetch off or in a
+ *     prefill. */
+moe_status moe_engine_record_gaps(moe_engine* eng, int64_t t0, int64_t T, float* gaps,
+                                  int64_t* early);
 
 moe_status moe_engine_stats(moe_engine* eng, moe_stats* out);
 

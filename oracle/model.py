@@ -217,6 +217,85 @@ class MixtralRef:
         return np.stack(outs) if outs else np.zeros((0, self.d)), acts
 
 
+def decode_layerwise(ref: "MixtralRef", X: np.ndarray, forced=None, tol: float = 1e-3,
+                     keep_weights: bool = False):
+    """MixtralRef.decode reordered layer-major, for full-depth parity at Mixtral scale.
+
+    Tokens are independent inputs (the reference model has no attention: run_model runs each
+    token through all layers on its own, toymoe.py:175-185), so evaluating layer l for all T
+    tokens before layer l+1 gives exactly MixtralRef.decode's arithmetic per token, while only
+    one layer's fp64 experts are alive at a time (8x7B: 11.3 GB instead of 361 GB); each
+    expert's token rows go through it as one fp64 GEMM.
+
+    forced: optional (T, L, K) selections of the system under test (ascending ids).  Where the
+    oracle's own k-th/(k+1)-th logit gap is below `tol` and its selection differs from the
+    forced one, the oracle adopts the forced set for that (t, l) -- a teacher-forced near-tie --
+    so a tie resolved the other way does not make the rest of the token incomparable.  A
+    disagreement with a gap >= tol is never forced: it stays in the returned acts and the
+    caller's equality check fails on it.
+
+    Returns dict: outs (T, d) fp64, acts (T, L, K) sorted, gaps (T, L) route margins,
+    guessed (T, L-1, K) sorted reference-definition guesses (toymoe.py:178-180), guess_gaps
+    (T, L-1), forced_ties = [(t, l, gap)] where the forced set was adopted."""
+    assert ref.layout == "ref"
+    T, d = X.shape
+    L, E, K = len(ref.layers), ref.E, ref.K
+    h = X.astype(np.float64)
+    acts = np.zeros((T, L, K), np.int64)
+    gaps = np.full((T, L), np.inf)
+    guessed = np.zeros((T, max(L - 1, 0), K), np.int64)
+    guess_gaps = np.full((T, max(L - 1, 0)), np.inf)
+    forced_ties = []
+    ar = np.arange(E)
+    for i, l in enumerate(ref.layers):
+        M, gw, gb = ref.dense(l)
+        if i >= 1:   # the reference guess for layer l is gate_l on the previous output
+            zg = np.stack([ref._norm(r) for r in h]) @ gw + gb
+            for t in range(T):
+                order = np.lexsort((ar, -zg[t]))
+                guessed[t, i - 1] = np.sort(order[:K])
+                if K < E:
+                    guess_gaps[t, i - 1] = zg[t, order[K - 1]] - zg[t, order[K]]
+        hm = h + ref.alpha * (h @ M)
+        hn = np.stack([ref._norm(r) for r in hm])
+        z = hn @ gw + gb
+        if not np.isfinite(z).all():
+            raise FloatingPointError("gate logits are not finite")
+        sel = np.zeros((T, K), np.int64)
+        for t in range(T):
+            order = np.lexsort((ar, -z[t]))
+            s = order[:K]
+            if K < E:
+                gaps[t, i] = z[t, order[K - 1]] - z[t, order[K]]
+            if forced is not None and gaps[t, i] < tol:
+                f = np.asarray(forced[t, i], np.int64)
+                if not np.array_equal(np.sort(s), np.sort(f)):
+                    s = f[np.lexsort((f, -z[t, f]))]   # the forced set, in logit order
+                    forced_ties.append((t, l, float(gaps[t, i])))
+            sel[t] = s
+        p = np.stack([softmax(zt) for zt in z])
+        w = np.take_along_axis(p, sel, 1)
+        if ref.renormalize:
+            w = w / w.sum(1, keepdims=True)
+        out = hm.copy()
+        for e in range(E):
+            rows, slots = np.nonzero(sel == e)
+            if rows.size == 0:
+                continue
+            w1, w3, w2 = ref.expert(l, e)
+            a1, a3 = hn[rows] @ w1, hn[rows] @ w3
+            y = (a1 / (1.0 + np.exp(-a1)) * a3) @ w2
+            out[rows] += w[rows, slots][:, None] * y
+        acts[:, i] = np.sort(sel, axis=1)
+        h = out
+        if not keep_weights:   # one layer's fp64 weights alive at a time
+            ref._dense.pop(l, None)
+            for e in range(E):
+                ref._experts.pop((l % ref.store_layers, e), None)
+    return {"outs": h, "acts": acts, "gaps": gaps, "guessed": guessed, "guess_gaps": guess_gaps,
+            "forced_ties": forced_ties}
+
+
 def bf16_round(a) -> np.ndarray:
     """Round to bf16 (nearest even) through f32, returned widened to f32: the engine's
     __floats2bfloat162_rn on an f32 value."""
@@ -380,3 +459,34 @@ def gen_trace(kind, L, E, K, T, skew, per_layer_permutation, repeat_prob, seed):
             ud = rng.random((T, K))
             acts[:, l] = sample_layer(weights[l], T, K, ud, repeat_prob, ur)
     return acts
+
+
+def prefetch_oracle(acts: np.ndarray, early: np.ndarray, resident_before: np.ndarray, nb: int):
+    """The engine's speculative-prefetch rule restated for its decision counts (the
+    reference models prefetch only as a cost, costmodel.py:114-132 "every guess is loaded";
+    the engine loads only guesses that are not already cached).
+
+    At step (t, l), l < L-1, the early guess for layer l+1 (top-k of gate_{l+1} on h'_l,
+    ascending) is walked in order: a guess g already resident in layer l+1 (resident_before
+    [t, l+1, g]) is skipped; otherwise it is staged if layer l+1 still has a buffer that is
+    neither held by a resident expert nor staged in this step (nb = cache size + staging
+    buffers; gate_cache_kernel's prefetch loop).  At step (t, l+1) every miss whose expert was
+    staged adopts its buffer (used); the other staged buffers are cancelled (wasted).
+
+    acts (T, L, K) ascending; early (T, L-1, K); resident_before (T, L, E) (engine layout).
+    Returns (issued (T, L), used (T, L)) counts indexed by the step the prefetch serves."""
+    T, L, K = acts.shape
+    issued = np.zeros((T, L), np.int64)
+    used = np.zeros((T, L), np.int64)
+    for t in range(T):
+        for l in range(L - 1):
+            res = resident_before[t, l + 1]
+            free = nb - int(res.sum())
+            staged = []
+            for g in early[t, l]:
+                if g < 0 or res[g] or len(staged) >= free:
+                    continue
+                staged.append(int(g))
+            issued[t, l + 1] = len(staged)
+            used[t, l + 1] = sum(1 for e in acts[t, l + 1] if not res[e] and int(e) in staged)
+    return issued, used

@@ -29,7 +29,7 @@ EXPORTED = (
     "moe_engine_create", "moe_engine_create_ex", "moe_engine_destroy", "moe_engine_set_dense_f32",
     "moe_engine_set_toy_expert_f32", "moe_engine_init_random", "moe_engine_expert_host_ptr",
     "moe_engine_dense_host", "moe_engine_reset", "moe_engine_decode", "moe_engine_prefill", "moe_engine_sync",
-    "moe_engine_records", "moe_engine_stats", "moe_engine_set_mode", "moe_engine_profile",
+    "moe_engine_records", "moe_engine_record_gaps", "moe_engine_stats", "moe_engine_set_mode", "moe_engine_profile",
     "moe_engine_kernel_times", "moe_microbench_gemv",
     "moe_hash_weights_bf16", "moe_hash_weights_f32",
     "moe_tc_grouped_gemm_bf16", "moe_tc_grouped_swiglu_bf16",
@@ -103,6 +103,7 @@ _SIGNATURES = {
     "moe_engine_prefill": ([_P, _P, _I64, _P, _P], _I32),
     "moe_engine_sync": ([_P], _I32),
     "moe_engine_records": ([_P, _I64, _I64, _P, _P, _P, _P, _P], _I32),
+    "moe_engine_record_gaps": ([_P, _I64, _I64, _P, _P], _I32),
     "moe_engine_stats": ([_P, ctypes.POINTER(StatsC)], _I32),
     "moe_engine_set_mode": ([_P, _I32, _F64, _I64, _I32, _I32], _I32),
     "moe_engine_profile": ([_P, _I32], _I32),

@@ -41,6 +41,25 @@ inline void once_per_device(std::atomic<uint64_t>& done, F f) {
     }                                                                             \
   } while (0)
 
+// Run the rest of the scope on `dev` and give the calling thread its own current device back
+// on exit: an ABI call on an engine never leaves the caller's device switched.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t status = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) status = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+#define MOE_ON_DEVICE(dev)                 \
+  ::moe::DeviceGuard moe_device_guard_(dev); \
+  MOE_CUDA(moe_device_guard_.status)
+
 // Check the launch that just happened and count it.
 #define MOE_LAUNCHED()                                                            \
   do {                                                                            \

@@ -679,7 +679,7 @@ namespace {
 moe_status create_resources(moe_engine* g) {
   const moe_engine_config& c = g->cfg;
   const int L = c.num_layers, E = c.num_experts, K = c.top_k, D = g->dpad;
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   const size_t msz = g->bf16 ? 2 : 4;
   TRY(alloc_device(reinterpret_cast<void**>(&g->pool), static_cast<size_t>(L) * g->NB * g->expert_bytes));
   TRY(alloc_device(&g->mixing, static_cast<size_t>(L) * D * D * msz));
@@ -756,7 +756,7 @@ extern "C" {
 
 moe_status moe_engine_destroy(moe_engine* g) {
   if (!g) return MOE_OK;
-  cudaSetDevice(g->device);
+  ::moe::DeviceGuard moe_device_guard_(g->device);
   cudaDeviceSynchronize();
   write_timeline(g);
   if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);
@@ -820,7 +820,7 @@ moe_status moe_engine_set_dense_f32(moe_engine* g, int32_t layer, const float* m
                                     const float* gate_w, const float* gate_b) {
   MOE_REQUIRE(g && layer >= 0 && layer < g->cfg.num_layers, "layer %d out of range", layer);
   MOE_REQUIRE(!g->bf16, "set_dense_f32 is for the f32 (toy) engine");
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   const int d = g->d, D = g->dpad, E = g->cfg.num_experts;
   // device layout: M_dev[j][i] = M_ref[i][j]; W_dev[e][i] = W_ref[i][e]; zero padding
   std::vector<float> mt(static_cast<size_t>(D) * D, 0.f), gw(static_cast<size_t>(E) * D, 0.f);
@@ -863,7 +863,7 @@ moe_status moe_engine_init_random(moe_engine* g, uint64_t seed, float gate_bias_
                                   int32_t init_experts) {
   MOE_REQUIRE(g, "null engine");
   MOE_REQUIRE(g->bf16, "init_random synthesises Mixtral-shaped (SwiGLU bf16) weights");
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   const int L = g->cfg.num_layers, E = g->cfg.num_experts, d = g->d, f = g->f;
   cudaStream_t s = g->copy_stream;
   // std = float(1 / sqrt(n)) rounded once from double (the oracle uses the same rule)
@@ -942,7 +942,7 @@ moe_status moe_engine_coded_size(moe_engine* g, int64_t* bytes) {
 moe_status moe_engine_attach_coded(moe_engine* g, void* seg, int64_t seg_bytes, int32_t build) {
   MOE_REQUIRE(g && seg, "null argument");
   MOE_REQUIRE(g->cfg.compress, "the engine was created with compress = 0");
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   char* base = static_cast<char*>(seg);
   if (build) {
     if (g->ctab.empty()) TRY(plan_coded(g));
@@ -987,7 +987,7 @@ moe_status moe_engine_expert_host_ptr(moe_engine* g, int32_t layer, int32_t expe
 moe_status moe_engine_dense_host(moe_engine* g, int32_t layer, void* mixing, float* gate_w,
                                  float* gate_b) {
   MOE_REQUIRE(g && layer >= 0 && layer < g->cfg.num_layers, "layer %d out of range", layer);
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   const int D = g->dpad, E = g->cfg.num_experts;
   const size_t msz = g->bf16 ? 2 : 4;
   if (mixing)
@@ -1004,7 +1004,7 @@ moe_status moe_engine_dense_host(moe_engine* g, int32_t layer, void* mixing, flo
 
 moe_status moe_engine_reset(moe_engine* g) {
   MOE_REQUIRE(g, "null engine");
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   MOE_CUDA(cudaDeviceSynchronize());
   MOE_CUDA(cudaStreamSynchronize(g->copy_stream));
   g->jobs.clear();
@@ -1024,7 +1024,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
                                     float* h_out_dev, const int32_t* routing_dev, void* stream) {
   MOE_REQUIRE(g, "null engine");
   MOE_REQUIRE(T >= 0, "negative token count");
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   cudaStream_t s = as_stream(stream);
   const moe_engine_config& c = g->cfg;
   const int L = c.num_layers, K = c.top_k, D = g->dpad, d = g->d;
@@ -1483,7 +1483,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
 
 moe_status moe_engine_sync(moe_engine* g) {
   MOE_REQUIRE(g, "null engine");
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   MOE_CUDA(cudaDeviceSynchronize());
   int h = 0;
   MOE_CUDA(cudaMemcpy(&h, g->err, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1512,7 +1512,7 @@ moe_status moe_engine_records(moe_engine* g, int64_t t0, int64_t T, int64_t* act
               (long long)t0, (long long)(t0 + T));
   MOE_REQUIRE(g->tokens_done - t0 <= c.max_tokens, "tokens [%lld, ...) left the record ring",
               (long long)t0);
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   MOE_CUDA(cudaDeviceSynchronize());
   const int L = c.num_layers, K = c.top_k, E = c.num_experts;
   std::vector<StepRecord> buf(static_cast<size_t>(L));
@@ -1531,6 +1531,32 @@ moe_status moe_engine_records(moe_engine* g, int64_t t0, int64_t T, int64_t* act
         if (resident_before) resident_before[(t * L + l) * E + e] = (r.rb >> e) & 1u;
         if (evicted) evicted[(t * L + l) * E + e] = (r.ev >> e) & 1u;
       }
+    }
+  }
+  return MOE_OK;
+}
+
+moe_status moe_engine_record_gaps(moe_engine* g, int64_t t0, int64_t T, float* gaps,
+                                  int64_t* early) {
+  MOE_REQUIRE(g, "null engine");
+  const moe_engine_config& c = g->cfg;
+  MOE_REQUIRE(t0 >= 0 && T >= 0 && t0 + T <= g->tokens_done, "tokens [%lld, %lld) not decoded",
+              (long long)t0, (long long)(t0 + T));
+  MOE_REQUIRE(g->tokens_done - t0 <= c.max_tokens, "tokens [%lld, ...) left the record ring",
+              (long long)t0);
+  MOE_ON_DEVICE(g->device);
+  MOE_CUDA(cudaDeviceSynchronize());
+  const int L = c.num_layers;
+  std::vector<StepRecord> buf(static_cast<size_t>(L));
+  for (int64_t t = 0; t < T; ++t) {
+    const long long tok = t0 + t;
+    MOE_CUDA(cudaMemcpy(buf.data(), g->ring + (tok % c.max_tokens) * L, sizeof(StepRecord) * L,
+                        cudaMemcpyDeviceToHost));
+    for (int l = 0; l < L; ++l) {
+      if (gaps) gaps[t * L + l] = buf[l].gap;
+      if (early && l + 1 < L)
+        for (int j = 0; j < c.top_k; ++j)
+          early[(t * (L - 1) + l) * c.top_k + j] = buf[l].early[j];
     }
   }
   return MOE_OK;
@@ -1570,7 +1596,7 @@ moe_status moe_engine_profile(moe_engine* g, int32_t enable) {
 
 moe_status moe_engine_kernel_times(moe_engine* g, moe_kernel_times* out) {
   MOE_REQUIRE(g && out, "null argument");
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   MOE_CUDA(cudaDeviceSynchronize());
   resolve_profile(g);
   *out = g->ktimes;
@@ -1579,7 +1605,7 @@ moe_status moe_engine_kernel_times(moe_engine* g, moe_kernel_times* out) {
 
 moe_status moe_engine_stats(moe_engine* g, moe_stats* out) {
   MOE_REQUIRE(g && out, "null argument");
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   MOE_CUDA(cudaDeviceSynchronize());
   MOE_CUDA(cudaStreamSynchronize(g->copy_stream));
   DeviceStats ds{};

@@ -33,8 +33,12 @@ struct StepRecord {
   int32_t guess[kMaxK];  // reference-definition guess, ascending (toymoe.py:178-180)
   uint32_t rb, ev;       // resident_before / evicted masks (kernels.py:98-99, 132-134)
   uint32_t flags;        // bit0 non-finite logits, bit1 policy failure
-  uint32_t pad;
+  float gap;             // route logit of the K-th selection minus the best unselected one
+                         // (near-tie margin; +inf when K == E, NaN under forced routing)
+  int32_t early[kMaxK];  // early guess for layer l+1 (gate_{l+1} on h'_l, ascending) that
+                         // drove this step's speculative prefetch; -1 when prefetch is off
 };
+static_assert(sizeof(StepRecord) % 16 == 0, "records are copied with 16-byte stores");
 
 // Mailbox entry the gate kernel hands to the host transfer thread (mapped pinned memory).
 // The device decides everything (which experts, which buffers); the host only forwards
@@ -274,6 +278,17 @@ __device__ __forceinline__ void warp_topk(float z, bool valid, int K, int* out) 
   }
 }
 
+// Near-tie margin of a top-k selection: z of the K-th selected lane minus the largest z
+// among the unselected valid lanes (toymoe.py:114's order; +inf when every lane is taken).
+__device__ __forceinline__ float topk_gap(float z, bool valid, const int* sel, int K) {
+  const int lane = threadIdx.x & 31;
+  bool taken = false;
+  for (int j = 0; j < K; ++j) taken = taken || sel[j] == lane;
+  const float zk = __shfl_sync(FULL, z, sel[K - 1] & 31);
+  const float next = warp_max(valid && !taken ? z : -INFINITY);
+  return zk - next;
+}
+
 __device__ __forceinline__ void sort_small(int* v, int n) {
   for (int i = 1; i < n; ++i) {
     const int key = v[i];
@@ -437,6 +452,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
   } else {
     warp_topk(zr, valid && finite, p.K, sel);
   }
+  const float gap = p.forced ? NAN : topk_gap(zr, valid, sel, p.K);
   const bool go = finite && routed_ok;
   float psel[kMaxK];
   float ssel = 0.f;
@@ -492,10 +508,12 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
       rec->prob[j] = psel[j];
       rec->acts[j] = acts[j];
       rec->guess[j] = do_guess ? gs[j] : -1;
+      rec->early[j] = do_prefetch ? pf[j] : -1;
     }
     rec->rb = rb;
     rec->ev = ev;
     rec->flags = flags;
+    rec->gap = gap;
     if (flags) atomicOr(p.err, static_cast<int>(flags));
     int nd = 0, nc = 0, np = 0;
     if (go && ok) {

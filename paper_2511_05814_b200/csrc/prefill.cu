@@ -199,7 +199,7 @@ extern "C" moe_status moe_engine_prefill_routed(moe_engine* g, const float* h_in
   if (T64 == 0) return MOE_OK;
   MOE_REQUIRE(g->d % tc::BN == 0 && g->f % (tc::BN / 2) == 0,
               "prefill needs hidden_dim %% 256 == 0 and ffn_dim %% 128 == 0 (got %d, %d)", g->d, g->f);
-  MOE_CUDA(cudaSetDevice(g->device));
+  MOE_ON_DEVICE(g->device);
   MOE_REQUIRE(pf_plan_smem(static_cast<int>(T64), c.top_k) <= 160 * 1024,
               "prefill of %lld tokens exceeds the plan kernel's staging (split the batch)", (long long)T64);
   static std::atomic<uint64_t> plan_attr{0};

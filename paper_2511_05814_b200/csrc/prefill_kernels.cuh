@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(256) pf_gate_kernel(PfGateParams p) {
     routed_ok = load_forced(p.forced + (static_cast<size_t>(t) * p.L + p.layer) * p.K, p.K, p.E, sel);
   else
     warp_topk(zr, valid && finite, p.K, sel);
+  const float gap = p.forced ? NAN : topk_gap(zr, valid, sel, p.K);
   float psel[kMaxK], ssel = 0.f;
   for (int j = 0; j < p.K; ++j) {
     psel[j] = __shfl_sync(FULL, prob, sel[j] & 31);
@@ -195,11 +196,13 @@ __global__ void __launch_bounds__(256) pf_gate_kernel(PfGateParams p) {
       rec->prob[j] = psel[j];
       rec->acts[j] = acts[j];
       rec->guess[j] = do_guess ? gs[j] : -1;
+      rec->early[j] = -1;
     }
     rec->rb = 0;
     rec->ev = 0;
     const uint32_t fl = (finite ? 0u : 1u) | (routed_ok ? 0u : 4u);
     rec->flags = fl;
+    rec->gap = gap;
     if (fl) atomicOr(p.err, static_cast<int>(fl));
     p.inv[t] = inv_mid;
   }

@@ -134,6 +134,7 @@ class OffloadEngine:
                     ctypes.byref(c), store.address, store.nbytes, ctypes.byref(handle)))
         self._h = handle
         self.tokens_done = 0
+        self._inflight = []   # tensors enqueued work still reads / writes (cleared at sync)
 
     # -- lifetime --
     def close(self) -> None:
@@ -248,15 +249,35 @@ class OffloadEngine:
         d = self.config.hidden_dim
         if h_in.dtype != torch.float32 or h_in.device.type != "cuda" or h_in.dim() != 2 or h_in.shape[1] != d:
             raise ConfigError(f"h_in must be a (T, {d}) float32 CUDA tensor")
+        return self._enqueue(self._lib.moe_engine_decode_routed, h_in, h_out, stream, routing)
+
+    def _stream(self, stream):
+        """The stream work is enqueued on: the caller's, else torch's current stream of the
+        ENGINE's device (not of whatever device the calling thread has current)."""
+        import torch
+
+        return stream if stream is not None else torch.cuda.current_stream(self._dev)
+
+    def _enqueue(self, fn, h_in, h_out, stream, routing):
+        """Launch fn on the engine's device and keep every tensor the enqueued kernels read or
+        write alive until they ran: record_stream() for the caching allocator (the tensors may
+        come from another stream) plus a per-call reference list cleared at sync()."""
+        import torch
+
         h_in = h_in.contiguous()
         T = h_in.shape[0]
-        if h_out is None:
-            h_out = torch.empty_like(h_in)
-        r = self._routing(routing, T)
-        _native.check(self._lib.moe_engine_decode_routed(
-            self._h, h_in.data_ptr(), T, h_out.data_ptr(), r.data_ptr() if r is not None else None,
-            _native.stream_ptr(stream)))
-        self._keep = r  # the device routing must outlive the enqueued work
+        with torch.cuda.device(self._dev):
+            s = self._stream(stream)
+            if h_out is None:
+                h_out = torch.empty_like(h_in)
+            r = self._routing(routing, T)
+            _native.check(fn(self._h, h_in.data_ptr(), T, h_out.data_ptr(),
+                             r.data_ptr() if r is not None else None, int(s.cuda_stream)))
+            live = [x for x in (h_in, h_out, r) if x is not None]
+            if s != torch.cuda.current_stream(self._dev):
+                for x in live:
+                    x.record_stream(s)
+            self._inflight.extend(live)
         self.tokens_done += T
         return h_out
 
@@ -269,17 +290,7 @@ class OffloadEngine:
         d = self.config.hidden_dim
         if h_in.dtype != torch.float32 or h_in.device.type != "cuda" or h_in.dim() != 2 or h_in.shape[1] != d:
             raise ConfigError(f"h_in must be a (T, {d}) float32 CUDA tensor")
-        h_in = h_in.contiguous()
-        T = h_in.shape[0]
-        if h_out is None:
-            h_out = torch.empty_like(h_in)
-        r = self._routing(routing, T)
-        _native.check(self._lib.moe_engine_prefill_routed(
-            self._h, h_in.data_ptr(), T, h_out.data_ptr(), r.data_ptr() if r is not None else None,
-            _native.stream_ptr(stream)))
-        self._keep = r
-        self.tokens_done += T
-        return h_out
+        return self._enqueue(self._lib.moe_engine_prefill_routed, h_in, h_out, stream, routing)
 
     def _host_io(self, h_in):
         """Stage a host (T, d) array in reusable pinned buffers: returns (device input, pinned
@@ -297,7 +308,8 @@ class OffloadEngine:
             self._pin_rows = rows
         self._pin_in[:T].numpy()[:] = a
         x = self._dev_in[:T]
-        x.copy_(self._pin_in[:T], non_blocking=True)
+        with torch.cuda.device(self._dev):
+            x.copy_(self._pin_in[:T], non_blocking=True)
         return x, self._dev_out[:T], self._pin_out[:T]
 
     def _run_host(self, fn, h_in, routing) -> np.ndarray:
@@ -306,9 +318,12 @@ class OffloadEngine:
             if a.shape[1] != self.config.hidden_dim:
                 raise ConfigError(f"h_in must be (T, {self.config.hidden_dim})")
             return np.zeros((0, self.config.hidden_dim), np.float32)
+        import torch
+
         x, y, out = self._host_io(h_in)
         fn(x, h_out=y, routing=routing)
-        out.copy_(y, non_blocking=True)
+        with torch.cuda.device(self._dev):
+            out.copy_(y, non_blocking=True)
         self.sync()  # synchronises the device (and reports non-finite gates)
         return out.numpy().copy()
 
@@ -340,13 +355,13 @@ class OffloadEngine:
         return {name: getattr(k, name) for name, _ in _native.KernelTimesC._fields_}
 
     def sync(self) -> None:
-        _native.check(self._lib.moe_engine_sync(self._h))
+        st = self._lib.moe_engine_sync(self._h)   # device-wide synchronize, then error check
+        self._inflight.clear()
+        _native.check(st)
 
     def decode(self, h_in, routing=None) -> np.ndarray:
         """Public decode: host (T, d) array in, host (T, d) float32 out (copies included).
         routing: optional (T, L, K) activation trace (trace-driven mode)."""
-        import torch
-
         return self._run_host(self.decode_device, h_in, routing)
 
     # -- records / stats --
@@ -363,6 +378,26 @@ class OffloadEngine:
             rb.ctypes.data, ev.ctypes.data, probs.ctypes.data))
         return {"acts": acts, "guessed": guessed, "resident_before": rb, "evicted": ev,
                 "probs": probs}
+
+    def record_gaps(self, t0: int, T: int) -> np.ndarray:
+        """(T, L) f32 near-tie margins of the same steps: the K-th selected route logit minus
+        the best unselected one (toymoe.py:99-115 ordering); +inf when K == E, NaN for
+        trace-driven steps.  A margin below the fp tolerance is a selection an fp64
+        evaluation could order differently (north star: ties within tolerance are stated)."""
+        cfg = self.config
+        gaps = np.zeros((T, cfg.num_layers), np.float32)
+        _native.check(self._lib.moe_engine_record_gaps(self._h, t0, T, gaps.ctypes.data, None))
+        return gaps
+
+    def record_early_guesses(self, t0: int, T: int) -> np.ndarray:
+        """(T, L-1, K) early guesses: at step (t, l) the top-k of gate_{l+1} on h'_l (ascending),
+        the guess the speculative prefetch of layer l+1 acted on; -1 with prefetch off."""
+        cfg = self.config
+        L, K = cfg.num_layers, cfg.top_k
+        early = np.full((T, max(L - 1, 0), K), -1, np.int64)
+        if L > 1:
+            _native.check(self._lib.moe_engine_record_gaps(self._h, t0, T, None, early.ctypes.data))
+        return early
 
     def event_log(self, t0: int, T: int, warmup_tokens: int = 0):
         """The engine's own cache decisions as a CacheEventLog (simulate.py format)."""

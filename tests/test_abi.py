@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_channel():
     lib = _native.load_library()
-    assert lib.moe_abi_version() == 3
+    assert lib.moe_abi_version() == 4
     assert isinstance(lib.moe_last_error(), bytes)
 
 

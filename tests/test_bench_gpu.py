@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
 def test_bench_reduced_run_prints_contract_line():
     cmd = [sys.executable, str(ROOT / "bench.py"), "--layers", "2", "--steps", "3", "--warmup", "3",
            "--variants", "lru,lfu+prefetch,lfu@2", "--e2e-steps", "3", "--cpu-sample-tokens", "2",
+           "--cpu-sample-layers", "1", "--cpu-repeats", "1",
            "--prefill-tokens", "64", "--prefill-decode", "4", "--tiny-tokens", "64",
            "--trace-variants", "zipf:1.0", "--replay-streams", "64", "--replay-tokens", "256"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
@@ -36,12 +37,27 @@ def test_bench_reduced_run_prints_contract_line():
     assert all(v["check_hits_from_records"] for v in d["variants"].values())
     assert d["tiny"]["trace_equals_oracle"] and d["replay"]["decisions_equal_oracle_sample"]
     assert d["prefill"]["prefill_tokens_per_s"] > 0
+    # the line's tail: parity against the oracle, the comparison table, the 8x22B section
+    p = d["parity"]
+    assert p["traces_equal_oracle_replay_all_variants"] and p["prefetch_issued_used_equal_oracle"]
+    assert p["fp64_selections_headline"]["layers"] == 1
+    assert p["fp64_selections_headline"]["mismatches"] == p["fp64_selections_headline"]["mismatches_at_near_ties"]
+    assert set(d["variants_summary"]) == {"lru", "lfu+prefetch", "lfu@2"}
+    assert list(d)[-3:] == ["variants_summary", "parity", "mixtral_8x22b"]
+    assert d["mixtral_8x22b"]["tok_s"] > 0 and d["mixtral_8x22b"]["parity"]["traces_equal_oracle_replay_all_variants"]
+    # both arms print the same workload config (the driver compares them key for key)
+    ref = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "3", "--cpu-sample-layers", "1", "--cpu-sample-tokens", "2",
+                          "--cpu-repeats", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = json.loads([ln for ln in ref.stdout.splitlines() if ln.startswith("{")][-1])
+    assert r["config"] == d["config"]
 
 
 def test_bench_8x22b_shape_reduced():
     """configs[4]'s bench path (Mixtral-8x22B shape, LFU + prefetch default) on 2 layers."""
     cmd = [sys.executable, str(ROOT / "bench.py"), "--model", "mixtral_8x22b", "--layers", "2",
            "--steps", "3", "--warmup", "3", "--e2e-steps", "2", "--cpu-sample-tokens", "2",
+           "--cpu-sample-layers", "1", "--cpu-repeats", "1",
            "--prefill-tokens", "0", "--tiny-tokens", "0", "--trace-variants", "", "--replay-streams", "0"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
