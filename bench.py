@@ -124,6 +124,9 @@ def parse_args():
     p.add_argument("--replay-tokens", type=int, default=8192)
     p.add_argument("--shared-store", action="store_true",
                    help="host experts in a node-shared segment (automatic when WORLD_SIZE > 1)")
+    p.add_argument("--peer-tier", action="store_true",
+                   help="N>1: NVLink peer-HBM miss tier (SURVEY 8f.4): each replica holds 1/N of "
+                        "the raw experts in HBM and serves the others' misses over NVLink")
     p.add_argument("--section-8x22b", type=int, default=1,
                    help="configs[4] section after the configs[1] run: 8x22B engine in a child "
                         "bench (LFU + prefetch, C=4), summarised in the line (0 = skip)")
@@ -413,20 +416,21 @@ def early_precision(rec, early):
     return tp / early.size
 
 
-def variant_parity(rec, gaps, early, s0, s1, policy, csize, nb, n_exp):
+def variant_parity(rec_all, rec, gaps, early, s0, s1, policy, csize, nb, n_exp):
     """Parity of one timed variant, checked here against the oracle (bench's checker role):
-    the live cache trace against the C oracle's replay of the engine's own selections
-    (kernels.py:60-147); with prefetch, the issued / used decisions against
-    oracle.prefetch_oracle; the selections' near-tie margins as the engine recorded them."""
+    the live cache trace of every token since the variant's cold start (rec_all: warm-up +
+    timed) against the C oracle's replay of the engine's own selections (kernels.py:60-147);
+    with prefetch, the timed region's issued / used decisions against oracle.prefetch_oracle;
+    the timed selections' near-tie margins as the engine recorded them."""
     import numpy as np
 
     from oracle.model import prefetch_oracle, replay_layers
 
     code, df, dp = policy.device_params()
-    rb, ev = replay_layers(rec["acts"], n_exp, csize, code, df, dp)
+    rb, ev = replay_layers(rec_all["acts"], n_exp, csize, code, df, dp)
     out = {"trace_equals_oracle_replay": bool(
-               np.array_equal(rec["resident_before"], np.transpose(rb, (1, 0, 2)))
-               and np.array_equal(rec["evicted"], np.transpose(ev, (1, 0, 2)))),
+               np.array_equal(rec_all["resident_before"], np.transpose(rb, (1, 0, 2)))
+               and np.array_equal(rec_all["evicted"], np.transpose(ev, (1, 0, 2)))),
            "near_ties_lt_1e-3": int((gaps < TIE_TOL).sum()),
            "min_topk_gap": float(np.nanmin(gaps)) if gaps.size else None,
            "steps": int(gaps.size)}
@@ -555,6 +559,17 @@ def run_ours(args, world, rank, local):
     else:
         eng = OffloadEngine(cfg)
         eng.init_random(args.seed)
+    peer = None
+    if args.peer_tier and world > 1:
+        import torch.distributed as dist
+
+        def gather(obj):
+            out = [None] * world
+            dist.all_gather_object(out, obj)
+            return out
+
+        peer = replicas.open_peer_tier(eng, rank, world, gather)
+        barrier(world)
     t_setup = time.perf_counter() - t_setup
     st0 = eng.stats()
     compressed_ratio = (st0["compressed_store_bytes"] / (cfg.host_store_layers * cfg.num_experts * EB)
@@ -627,7 +642,9 @@ def run_ours(args, world, rank, local):
         gaps = eng.record_gaps(t0_tok + args.warmup, args.steps)
         early = eng.record_early_guesses(t0_tok + args.warmup, args.steps) if prefetch else None
         nb = csize + ((cfg.prefetch_buffers or cfg.top_k) if prefetch else 0)
-        par = variant_parity(rec, gaps, early, s0, s1, policy, csize, nb, cfg.num_experts)
+        # the trace is replayed from the cold cache set_mode left, warm-up tokens included
+        rec_all = eng.records(t0_tok, args.warmup + args.steps)
+        par = variant_parity(rec_all, rec, gaps, early, s0, s1, policy, csize, nb, cfg.num_experts)
         if headline:
             head_rec, head_gaps = rec, gaps
         results[v] = {
@@ -642,6 +659,7 @@ def run_ours(args, world, rank, local):
             "pcie_bound_tokens_per_s": pcie_peak * 1e9 / max(1.0, misses / args.steps * EB * compressed_ratio),
             "expert_GBps_delivered": (demand + s1["prefetch_bytes"] - s0["prefetch_bytes"]
                                       + s1["prefill_bytes"] - s0["prefill_bytes"]) / (ms / 1e3) / 1e9,
+            "peer_tier_GBps": (s1["peer_bytes"] - s0["peer_bytes"]) / (ms / 1e3) / 1e9,
             "prefetch_issued": s1["prefetch_issued"] - s0["prefetch_issued"],
             "prefetch_used": s1["prefetch_used"] - s0["prefetch_used"],
             "prefetch_wasted_bytes": s1["prefetch_wasted_bytes"] - s0["prefetch_wasted_bytes"],
@@ -675,6 +693,7 @@ def run_ours(args, world, rank, local):
     if args.prefill_tokens > 0:
         prefill = run_prefill(args, eng, inputs, base, stream, world, pcie_peak)
     eng.close()
+    peer = None   # the peer tier's HBM (and mapped peers) after the engine that used it
     if coded is not None:
         barrier(world)
         coded.close()
@@ -685,6 +704,10 @@ def run_ours(args, world, rank, local):
     if store is not None:
         barrier(world)
         store.close()
+    # every replica checked its own live traces against the oracle replay: count them
+    ranks_ok = sum_over_ranks(float(all(r["parity"]["trace_equals_oracle_replay"]
+                                        and r["parity"].get("prefetch_issued_used_equal_oracle", True)
+                                        for r in results.values())), world)
     if rank != 0:
         return
     head = results[variants[0]]
@@ -737,6 +760,9 @@ def run_ours(args, world, rank, local):
                                 + (", coded store only" if cfg.compress == 2 else "")
                                 if cfg.compress else "raw bf16"),
             "prefetch_buffers_per_layer": (cfg.prefetch_buffers or cfg.top_k) if want_prefetch else 0,
+            "peer_tier": (f"NVLink peer-HBM tier: 1/{world} of the raw experts per replica's HBM, "
+                          "misses of peer-homed experts copied device to device"
+                          if args.peer_tier and world > 1 else "off"),
         },
         "hit_rate": head["hit_rate"],
         "variants": results,
@@ -819,6 +845,8 @@ def run_ours(args, world, rank, local):
     line["e2e"] = e2e
     line["clocks"] = clocks
     line["gpu_launches"] = launches_timed
+    if cpu:
+        line["speedup_vs_cpu_port"] = head["tokens_per_s"] / cpu["value"]
     pars = [r["parity"] for r in results.values()]
     parity = {
         "traces_equal_oracle_replay_all_variants": all(p["trace_equals_oracle_replay"] for p in pars),
@@ -830,6 +858,7 @@ def run_ours(args, world, rank, local):
     }
     if cpu_acts is not None:
         parity["fp64_selections_headline"] = fp64_selection_check(head_rec, head_gaps, cpu_acts)
+    parity["replicas_with_oracle_equal_traces"] = f"{int(ranks_ok)}/{world}"
     parity["full_depth_tests"] = ("tests/test_fullscale_gpu.py: configs[1] 32 layers and the "
                                   "configs[4] shape vs the fp64 oracle")
     line["variants_summary"] = {
@@ -842,8 +871,6 @@ def run_ours(args, world, rank, local):
                 "pf_wasted_GB": round(r["prefetch_wasted_bytes"] / 1e9, 2)} if r["prefetch"] else {})}
         for v, r in results.items()}
     line["parity"] = parity
-    if cpu:
-        line["speedup_vs_cpu_port"] = head["tokens_per_s"] / cpu["value"]
     if args.model == "mixtral_8x7b" and args.section_8x22b and world == 1:
         line["mixtral_8x22b"] = run_8x22b_section(args)
     print(json.dumps(line), flush=True)

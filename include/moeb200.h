@@ -175,6 +175,8 @@ typedef struct {
   int64_t demand_link_bytes;   /* bytes the demand copies put on the link (== demand_bytes
                                   uncompressed; h2d_bytes = demand_link + prefetch + prefill) */
   int64_t compressed_store_bytes; /* host bytes of the exponent-coded expert store (0: off) */
+  int64_t peer_bytes;             /* expert bytes copied from the peer-HBM tier (ABI 4; not in
+                                     h2d_bytes, which counts the PCIe link only) */
 } moe_stats;
 
 moe_status moe_engine_create(const moe_engine_config* cfg, moe_engine** out);
@@ -294,13 +296,29 @@ moe_status moe_engine_records(moe_engine* eng, int64_t t0, int64_t T, int64_t* a
  *     logit (toymoe.py:99-115 ranks by logit desc, ties to the lower id; a margin below the fp
  *     tolerance marks a selection the fp64 reference could order differently).  +inf when
  *     K == E, NaN for trace-driven steps.
+ *   guess_gaps (T, L-1) f32: the same margin of the reference-definition guess for layer l
+ *     (gate_l on the output of l-1, toymoe.py:178-180); NaN without speculation records.
+ *   zscales (T, L, 2) f32: the largest |logit| of the route and of the guess at each step,
+ *     for margins relative to the logit scale (fp32 logit error grows with it).
  *   early (T, L-1, K) int64: the early guess for layer l+1 made at step (t, l) (gate_{l+1} on
  *     h'_l, ascending) that drove its speculative prefetch; -1 with prefetch off or in a
  *     prefill. */
 moe_status moe_engine_record_gaps(moe_engine* eng, int64_t t0, int64_t T, float* gaps,
-                                  int64_t* early);
+                                  float* guess_gaps, float* zscales, int64_t* early);
 
 moe_status moe_engine_stats(moe_engine* eng, moe_stats* out);
+
+/* NVLink peer-HBM miss tier (ABI 4), off until attached.  ptrs[l * E + e] is the
+ * device address of the raw expert block (layer l, expert e) -- on a peer GPU of the node
+ * (opened with cudaIpcOpenMemHandle, peer access enabled) or on this GPU -- or NULL for
+ * experts the tier does not hold.  Demand misses and speculative prefetches of held experts
+ * are copied from there by the copy engine (device to device, NVLink for a peer) instead of
+ * from the pinned host store over PCIe; only the transfer source changes: selections, cache
+ * decisions and buffers are the device's as before, so traces and outputs are identical.
+ * The reference models the transfer source as a constant bandwidth (costmodel.py:90-111).
+ * Copy-engine transfer mode only.  n = L * E; ptrs == NULL (n = 0) detaches.  The caller keeps
+ * the blocks alive and unchanged while attached. */
+moe_status moe_engine_attach_peer_tier(moe_engine* eng, const void* const* ptrs, int64_t n);
 
 /* ---- kernel microbenchmark (tuning aid) --------------------------------------------- */
 

@@ -36,6 +36,7 @@ EXPORTED = (
     "moe_text_data", "moe_text_size", "moe_text_free", "moe_format_trace", "moe_format_event_log",
     "moe_sample_zipf", "moe_sample_markov", "moe_engine_decode_routed", "moe_engine_prefill_routed",
     "moe_xc_encode", "moe_xc_decode", "moe_engine_coded_size", "moe_engine_attach_coded",
+    "moe_engine_attach_peer_tier",
 )
 
 
@@ -61,7 +62,7 @@ class StatsC(ctypes.Structure):
         "prefetch_issued", "prefetch_used", "prefetch_wasted_bytes", "expert_bytes")] + [
         ("copy_busy_ms", ctypes.c_double), ("prefill_tokens", ctypes.c_int64),
         ("prefill_bytes", ctypes.c_int64), ("demand_link_bytes", ctypes.c_int64),
-        ("compressed_store_bytes", ctypes.c_int64)]
+        ("compressed_store_bytes", ctypes.c_int64), ("peer_bytes", ctypes.c_int64)]
 
 
 class KernelTimesC(ctypes.Structure):
@@ -103,7 +104,8 @@ _SIGNATURES = {
     "moe_engine_prefill": ([_P, _P, _I64, _P, _P], _I32),
     "moe_engine_sync": ([_P], _I32),
     "moe_engine_records": ([_P, _I64, _I64, _P, _P, _P, _P, _P], _I32),
-    "moe_engine_record_gaps": ([_P, _I64, _I64, _P, _P], _I32),
+    "moe_engine_record_gaps": ([_P, _I64, _I64, _P, _P, _P, _P], _I32),
+    "moe_engine_attach_peer_tier": ([_P, _P, _I64], _I32),
     "moe_engine_stats": ([_P, ctypes.POINTER(StatsC)], _I32),
     "moe_engine_set_mode": ([_P, _I32, _F64, _I64, _I32, _I32], _I32),
     "moe_engine_profile": ([_P, _I32], _I32),

@@ -32,8 +32,14 @@ namespace {
 
 moe_status create_resources(moe_engine* g);
 
+// Raw bytes [off, off + n) of (layer, expert) into buffer `buf`: from the peer-HBM tier when it
+// holds the expert (device to device), else from the pinned host store (PCIe).
 moe_status issue_copy(moe_engine* g, int layer, int buf, int expert, long long off, long long n) {
   char* dst = g->pool + (static_cast<long long>(layer) * g->NB + buf) * g->expert_bytes + off;
+  if (const char* pb = g->peer_block(layer, expert)) {
+    MOE_CUDA(cudaMemcpyAsync(dst, pb + off, n, cudaMemcpyDefault, g->copy_stream));
+    return MOE_OK;
+  }
   const char* src = g->store_block(layer, expert) + off;
   MOE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, g->copy_stream));
   return MOE_OK;
@@ -134,7 +140,7 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
   for (int i = 0; i < m.n_demand; ++i) order[i] = i;
   std::sort(order, order + m.n_demand,
             [&](int x, int y) { return m.demand_expert[x] < m.demand_expert[y]; });
-  long long demand = 0, link = 0;
+  long long demand = 0, link = 0, peer = 0;
   std::pair<cudaEvent_t, cudaEvent_t> tev{nullptr, nullptr};
   if (m.n_demand > 0) {
     tev = take_timing_events(g);
@@ -158,7 +164,8 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
       g->st.prefetch_used += 1;
     }
     plan->comp[k] = false;
-    if (zone >= 0 || (g->cstore && from == 0)) {
+    const bool via_peer = g->peer_block(m.layer, e) != nullptr;
+    if (zone >= 0 || (g->cstore && from == 0 && !via_peer)) {
       // exponent-coded: an adopted prefetch finishes the coded bytes in its zone, a fresh miss
       // lands in slot k (after that slot's previous decode); the compute stream decodes each
       // part into the expert's buffer as it lands
@@ -183,10 +190,11 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
       continue;
     }
     // part A: [from, split), then event; part B: [max(from, split), end), then event
+    long long& over = via_peer ? peer : link;   // bytes over NVLink / over PCIe
     if (from < split) {
       TRY(issue_copy(g, m.layer, b, e, from, split - from));
       demand += split - from;
-      link += split - from;
+      over += split - from;
     }
     plan->ev_a[k] = next_order_event(g);
     MOE_CUDA(cudaEventRecord(plan->ev_a[k], g->copy_stream));
@@ -194,7 +202,7 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
     if (fb < g->expert_bytes) {
       TRY(issue_copy(g, m.layer, b, e, fb, g->expert_bytes - fb));
       demand += g->expert_bytes - fb;
-      link += g->expert_bytes - fb;
+      over += g->expert_bytes - fb;
     }
     plan->ev_b[k] = next_order_event(g);
     MOE_CUDA(cudaEventRecord(plan->ev_b[k], g->copy_stream));
@@ -203,7 +211,8 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
   for (int i = 0; i < m.n_prefetch; ++i) {
     PrefetchJob j{m.layer + 1, m.prefetch_buf[i], m.prefetch_expert[i], 0, nchunks, false, false};
     j.bytes = g->expert_bytes;
-    if (g->pzone) {
+    j.peer = g->peer_block(j.layer, j.expert) != nullptr;
+    if (g->pzone && !j.peer) {
       j.zone = g->pzone_next;
       g->pzone_next = (g->pzone_next + 1) % static_cast<int>(g->pzone_free.size());
       j.bytes = coded_total(g, m.layer + 1, j.expert);
@@ -215,6 +224,7 @@ moe_status handle_mail(moe_engine* g, const MailRecord& m, DemandPlan* plan) {
   g->st.demand_bytes += demand;
   g->st.demand_link_bytes += link;
   g->st.h2d_bytes += link;
+  g->st.peer_bytes += peer;
   g->st.prefetch_issued += m.n_prefetch;
   if (m.n_demand > 0) g->busy_events.push_back(tev);
   return MOE_OK;
@@ -272,7 +282,7 @@ moe_status pump_prefetch(moe_engine* g, bool* did) {
   g->prefetch_inflight.push_back(ev);
   std::lock_guard<std::mutex> lk(g->stats_mu);
   g->st.prefetch_bytes += n;
-  g->st.h2d_bytes += n;
+  (j.peer ? g->st.peer_bytes : g->st.h2d_bytes) += n;
   *did = true;
   return MOE_OK;
 }
@@ -692,6 +702,8 @@ moe_status create_resources(moe_engine* g) {
   TRY(alloc_device(reinterpret_cast<void**>(&g->h_norm), sizeof(float) * D));
   TRY(alloc_device(reinterpret_cast<void**>(&g->gate_part), sizeof(float) * 148 * (3 * kMaxE + 2)));
   TRY(alloc_device(reinterpret_cast<void**>(&g->norm_scale), sizeof(float)));
+  TRY(alloc_device(reinterpret_cast<void**>(&g->mix_ctr), sizeof(unsigned int)));
+  MOE_CUDA(cudaMemset(g->mix_ctr, 0, sizeof(unsigned int)));
   TRY(alloc_device(reinterpret_cast<void**>(&g->y), sizeof(float) * K * D));
   TRY(alloc_device(reinterpret_cast<void**>(&g->act), sizeof(float) * K * g->f));
   TRY(alloc_device(reinterpret_cast<void**>(&g->err), sizeof(int)));
@@ -804,7 +816,8 @@ moe_status moe_engine_destroy(moe_engine* g) {
     cudaFree(g->gate_phase_ns);
   }
   void* dev[] = {g->pool, g->mixing, g->gate_w, g->gate_b, g->states, g->ring, g->h_in,
-                 g->h_mid, g->h_norm, g->gate_part, g->norm_scale, g->y, g->act, g->err, g->dstats, g->x_pad, g->out_pad};
+                 g->h_mid, g->h_norm, g->gate_part, g->norm_scale, g->y, g->act, g->err, g->dstats, g->x_pad, g->out_pad,
+                 g->mix_ctr};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (g->mail_h) cudaFreeHost(g->mail_h);
@@ -1077,6 +1090,8 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
   const int grid_mix = stream_grid(1), grid_ffn = stream_grid(K);
   // SM transfer runs a token as one kernel chain (no copy-event waits): launch it programmatically
   const bool pdl = g->sm_transfer && !g->no_pdl;
+  // bf16 engines take the gate / cache step in the mixing GEMV's last CTA (one launch)
+  const bool fused_gate = g->bf16 && !g->no_fused_gate;
   // one expert-FFN launch group: phase 0 = hits, 1 = misses; only = -1 all, i = i-th miss
   if (g->profiling && !g->prof_bytes_dev)
     MOE_CUDA(cudaMalloc(&g->prof_bytes_dev, 4 * sizeof(long long) * moe_engine::kProfSlots));
@@ -1204,6 +1219,13 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       MixParams mp{l == 0 ? x : nullptr, hm_prev, g->y, l == 0 ? nullptr : trec + (l - 1),
                    static_cast<char*>(g->mixing) + static_cast<size_t>(l) * D * D * msz,
                    c.mixing_scale, D, K, g->h_in, hm};
+      GateParams gp{hm, g->h_in, g->gate_w, g->gate_b, l, L, c.num_experts, K, D, c.cache_size,
+                    c.cache_size + (c.prefetch ? g->S : 0), c.policy, c.decay_factor, c.decay_period, c.record_speculation,
+                    c.prefetch, c.renormalize, seq, g->states, trec + l,
+                    g->sm_transfer ? nullptr : g->mail_d,
+                    g->ctl_d, g->err, g->dstats, c.rms_norm, c.rms_eps, g->h_norm,
+                    g->gate_phase_ns, g->bf16 ? g->gate_part : nullptr, grid_mix, g->norm_scale,
+                    routing_dev ? routing_dev + (static_cast<size_t>(t) * L + l) * K : nullptr};
       std::array<cudaEvent_t, 3> pe{};
       if (g->profiling) {
         for (auto& e : pe) e = take_prof_event(g);
@@ -1229,20 +1251,16 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
         sp.E = c.num_experts;
         sp.do_guess = c.record_speculation && l >= 1;
         sp.part = g->gate_part;
+        sp.fuse_gate = fused_gate ? 1 : 0;
+        sp.done_ctr = g->mix_ctr;
+        sp.gate = gp;
         MOE_CUDA(launch_stream<kModeMix>(gmix, grid_mix, sp, s));
       } else {
         MOE_CUDA(launch_k(pdl, mix_kernel<false>, dim3(mix_grid), dim3(256), mix_smem, s, mp));
       }
       MOE_LAUNCHED();
       if (g->profiling) MOE_CUDA(cudaEventRecord(pe[1], s));
-      GateParams gp{hm, g->h_in, g->gate_w, g->gate_b, l, L, c.num_experts, K, D, c.cache_size,
-                    c.cache_size + (c.prefetch ? g->S : 0), c.policy, c.decay_factor, c.decay_period, c.record_speculation,
-                    c.prefetch, c.renormalize, seq, g->states, trec + l,
-                    g->sm_transfer ? nullptr : g->mail_d,
-                    g->ctl_d, g->err, g->dstats, c.rms_norm, c.rms_eps, g->h_norm,
-                    g->gate_phase_ns, g->bf16 ? g->gate_part : nullptr, grid_mix, g->norm_scale,
-                    routing_dev ? routing_dev + (static_cast<size_t>(t) * L + l) * K : nullptr};
-      {
+      if (!fused_gate) {
         // programmatic launch: the gate's launch and state staging overlap the mixing tail
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(1);
@@ -1257,8 +1275,8 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
           MOE_CUDA(cudaLaunchKernelEx(&lc, gate_cache_kernel<8>, gp));
         else
           MOE_CUDA(cudaLaunchKernelEx(&lc, gate_cache_kernel<kMaxE>, gp));
+        MOE_LAUNCHED();
       }
-      MOE_LAUNCHED();
       if (g->profiling) MOE_CUDA(cudaEventRecord(pe[2], s));
       const bool tl = g->timeline_path && !g->sm_transfer && !fixed;
       moe_engine::TimelineRec trc{};
@@ -1537,7 +1555,7 @@ moe_status moe_engine_records(moe_engine* g, int64_t t0, int64_t T, int64_t* act
 }
 
 moe_status moe_engine_record_gaps(moe_engine* g, int64_t t0, int64_t T, float* gaps,
-                                  int64_t* early) {
+                                  float* guess_gaps, float* zscales, int64_t* early) {
   MOE_REQUIRE(g, "null engine");
   const moe_engine_config& c = g->cfg;
   MOE_REQUIRE(t0 >= 0 && T >= 0 && t0 + T <= g->tokens_done, "tokens [%lld, %lld) not decoded",
@@ -1554,6 +1572,11 @@ moe_status moe_engine_record_gaps(moe_engine* g, int64_t t0, int64_t T, float* g
                         cudaMemcpyDeviceToHost));
     for (int l = 0; l < L; ++l) {
       if (gaps) gaps[t * L + l] = buf[l].gap;
+      if (guess_gaps && l >= 1) guess_gaps[t * (L - 1) + (l - 1)] = buf[l].guess_gap;
+      if (zscales) {
+        zscales[(t * L + l) * 2] = buf[l].zscale[0];
+        zscales[(t * L + l) * 2 + 1] = buf[l].zscale[1];
+      }
       if (early && l + 1 < L)
         for (int j = 0; j < c.top_k; ++j)
           early[(t * (L - 1) + l) * c.top_k + j] = buf[l].early[j];
@@ -1600,6 +1623,40 @@ moe_status moe_engine_kernel_times(moe_engine* g, moe_kernel_times* out) {
   MOE_CUDA(cudaDeviceSynchronize());
   resolve_profile(g);
   *out = g->ktimes;
+  return MOE_OK;
+}
+
+moe_status moe_engine_attach_peer_tier(moe_engine* g, const void* const* ptrs, int64_t n) {
+  MOE_REQUIRE(g, "null engine");
+  const moe_engine_config& c = g->cfg;
+  if (!ptrs) {
+    g->peer.clear();
+    return MOE_OK;
+  }
+  MOE_REQUIRE(n == static_cast<int64_t>(c.num_layers) * c.num_experts,
+              "peer tier table needs L * E = %d entries, got %lld", c.num_layers * c.num_experts,
+              (long long)n);
+  MOE_REQUIRE(!g->sm_transfer, "the peer tier serves the copy-engine transfer mode");
+  MOE_ON_DEVICE(g->device);
+  MOE_CUDA(cudaDeviceSynchronize());   // no copy of the previous source is in flight
+  std::vector<const char*> t(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    t[i] = static_cast<const char*>(ptrs[i]);
+    if (!t[i]) continue;
+    cudaPointerAttributes a{};
+    MOE_CUDA(cudaPointerGetAttributes(&a, t[i]));
+    MOE_REQUIRE(a.type == cudaMemoryTypeDevice, "peer tier entry %lld is not device memory",
+                (long long)i);
+    if (a.device != g->device) {
+      int ok = 0;
+      MOE_CUDA(cudaDeviceCanAccessPeer(&ok, g->device, a.device));
+      MOE_REQUIRE(ok, "GPU %d cannot access peer GPU %d", g->device, a.device);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else MOE_CUDA(e);
+    }
+  }
+  g->peer.swap(t);
   return MOE_OK;
 }
 

@@ -108,6 +108,7 @@ struct PrefetchJob {
   int zone = -1;        // compressed: landing zone of the exponent-coded expert (-1: raw copy
                         // straight into the staging buffer)
   long long bytes = 0;  // bytes this job moves (expert_bytes raw, or the coded size)
+  bool peer = false;    // raw copy from the peer-HBM tier (not over PCIe)
 };
 
 }  // namespace moe
@@ -131,6 +132,7 @@ struct moe_engine {
   StepRecord* ring = nullptr;    // [max_tokens][L]
   float *h_in = nullptr, *h_mid = nullptr, *h_norm = nullptr, *y = nullptr, *act = nullptr;
   float* gate_part = nullptr;   // [148][3E + 2] partial gate logits from the mixing GEMV
+  unsigned int* mix_ctr = nullptr;  // fused mix + gate: CTAs done (zero between launches)
   float* norm_scale = nullptr;  // 1 / rms(h') of the current layer
   float *x_pad = nullptr, *out_pad = nullptr;  // padded token staging when d % 8 != 0
   int* err = nullptr;
@@ -184,6 +186,7 @@ struct moe_engine {
   // token graph (SM transfer): one token captured once, replayed per token
   bool no_graph = getenv("MOE_NO_GRAPH") != nullptr;
   bool no_pdl = getenv("MOE_NO_PDL") != nullptr;
+  bool no_fused_gate = getenv("MOE_NO_FUSED_GATE") != nullptr;  // A/B: separate gate launch
   cudaGraphExec_t graph_exec = nullptr;
   uint64_t graph_kernels = 0;
   cudaStream_t cap_stream = nullptr;
@@ -238,6 +241,12 @@ struct moe_engine {
 
   // batched prefill (prefill.cu), allocated on first use
   moe::PrefillState* pf = nullptr;
+
+  // NVLink peer-HBM tier (moe_engine_attach_peer_tier): raw expert blocks by [l * E + e]
+  std::vector<const char*> peer;
+  const char* peer_block(int layer, int expert) const {
+    return peer.empty() ? nullptr : peer[static_cast<size_t>(layer) * cfg.num_experts + expert];
+  }
 
   // host block of expert e of layer l (store layers alias modulo SL)
   char* store_block(int layer, int expert) const {

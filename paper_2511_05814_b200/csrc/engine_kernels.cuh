@@ -37,6 +37,9 @@ struct StepRecord {
                          // (near-tie margin; +inf when K == E, NaN under forced routing)
   int32_t early[kMaxK];  // early guess for layer l+1 (gate_{l+1} on h'_l, ascending) that
                          // drove this step's speculative prefetch; -1 when prefetch is off
+  float guess_gap;       // the same margin for the reference-definition guess (NaN: none)
+  float zscale[2];       // max |logit| of the route / guess (relative near-tie tests)
+  uint32_t pad2;
 };
 static_assert(sizeof(StepRecord) % 16 == 0, "records are copied with 16-byte stores");
 
@@ -326,24 +329,38 @@ __device__ __forceinline__ bool load_forced(const int32_t* forced, int K, int E,
 
 constexpr int kGateThreads = 512;  // d=4096: two float4 columns per thread, loads all in flight
 
-template <int EM>  // compile-time bound on E (8 for Mixtral) so the accumulators stay in registers
-__global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) {
-  pdl_trigger();  // the FFN pass may launch and wait for the decision meanwhile
-  __shared__ float z[3][kMaxE];
-  __shared__ float red[2][kGateThreads / 32];
-  __shared__ __align__(16) LayerState sS, sS1;   // working copies of this / next layer's state
-  __shared__ __align__(16) MailRecord sM;
-  __shared__ long long s_consumed;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+// Working set of the gate / cache step in shared memory.
+struct GateSmem {
+  float z[3][kMaxE];
+  float red[2][kGateThreads / 32];
+  __align__(16) LayerState sS;    // working copies of this / next layer's state
+  __align__(16) LayerState sS1;
+  __align__(16) MailRecord sM;
+  long long s_consumed;
+};
+
+// The gate + cache step run by `nthreads` threads (tid in [0, nthreads), a multiple of 32):
+// as its own single-CTA kernel (gate_cache_kernel) or by the last CTA of the fused mixing
+// GEMV (stream_gemv_kernel<kModeMix>, fuse_gate).  sync() is a barrier over those threads.
+template <int EM, class Sync>
+__device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& gsm, int tid,
+                                                int nthreads, Sync sync, bool wait_pdl) {
+  float (&z)[3][kMaxE] = gsm.z;
+  float (&red)[2][kGateThreads / 32] = gsm.red;
+  LayerState& sS = gsm.sS;
+  LayerState& sS1 = gsm.sS1;
+  MailRecord& sM = gsm.sM;
+  long long& s_consumed = gsm.s_consumed;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nthreads >> 5;
   const bool do_guess = p.record_spec && p.layer >= 1;
   const bool do_prefetch = p.prefetch == MOE_PREFETCH_EARLY && p.layer + 1 < p.L;
   const unsigned long long t0 = p.phase_ns ? gtimer() : 0;
   // stage the cache state in shared memory (its latency overlaps the logits below)
-  copy16(&sS, &p.states[p.layer], sizeof(LayerState), threadIdx.x, blockDim.x);
-  if (do_prefetch) copy16(&sS1, &p.states[p.layer + 1], sizeof(LayerState), threadIdx.x, blockDim.x);
-  if (threadIdx.x == 0) s_consumed = p.mail ? p.ctl->consumed : 0;
+  copy16(&sS, &p.states[p.layer], sizeof(LayerState), tid, nthreads);
+  if (do_prefetch) copy16(&sS1, &p.states[p.layer + 1], sizeof(LayerState), tid, nthreads);
+  if (tid == 0) s_consumed = p.mail ? p.ctl->consumed : 0;
   // launched programmatically after the mixing kernel: its outputs are read from here on
-  pdl_wait();
+  if (wait_pdl) pdl_wait();
   // RMSNorm scales of h' (route, early guess, experts) and of h_in (reference guess)
   float inv_mid = 1.f, inv_in = 1.f;
   const int njob = 3 * p.E + 2;
@@ -359,22 +376,22 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
         else red[q - 3 * p.E][0] = acc;
       }
     }
-    __syncthreads();
+    sync();
     if (p.rms_norm) {
       inv_mid = rsqrtf(red[0][0] / p.d + p.rms_eps);
       inv_in = rsqrtf(red[1][0] / p.d + p.rms_eps);
     }
-    if (threadIdx.x < 3 * p.E) {
-      const int which = threadIdx.x / p.E, e = threadIdx.x % p.E;
+    if (tid < 3 * p.E) {
+      const int which = tid / p.E, e = tid % p.E;
       const int gl = which == 2 ? p.layer + 1 : p.layer;
       if ((which == 1 && do_guess) || (which == 2 && do_prefetch) || which == 0)
         z[which][e] = z[which][e] * (which == 1 ? inv_in : inv_mid) + p.gate_b[gl * p.E + e];
     }
-    if (threadIdx.x == 0 && p.norm_scale) *p.norm_scale = inv_mid;
+    if (tid == 0 && p.norm_scale) *p.norm_scale = inv_mid;
   } else {
     if (p.rms_norm) {
       float sm = 0.f, si = 0.f;
-      for (int i = threadIdx.x; i < p.d; i += blockDim.x) {
+      for (int i = tid; i < p.d; i += nthreads) {
         const float a = p.h_mid[i];
         sm = fmaf(a, a, sm);
         if (do_guess) {
@@ -388,7 +405,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
         red[0][warp] = sm;
         red[1][warp] = si;
       }
-      __syncthreads();
+      sync();
       float tm = 0.f, ti = 0.f;
       for (int w = 0; w < nwarps; ++w) {
         tm += red[0][w];
@@ -396,9 +413,9 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
       }
       inv_mid = rsqrtf(tm / p.d + p.rms_eps);
       inv_in = rsqrtf(ti / p.d + p.rms_eps);
-      for (int i = threadIdx.x; i < p.d; i += blockDim.x) p.h_norm[i] = p.h_mid[i] * inv_mid;
+      for (int i = tid; i < p.d; i += nthreads) p.h_norm[i] = p.h_mid[i] * inv_mid;
     }
-    if (threadIdx.x == 0 && p.norm_scale) *p.norm_scale = 1.f;
+    if (tid == 0 && p.norm_scale) *p.norm_scale = 1.f;
   }
   const unsigned long long t1 = p.phase_ns ? gtimer() : 0;
   if (!p.part) {
@@ -424,7 +441,7 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
     if (lane == 0) z[which][e] = acc * (which == 1 ? inv_in : inv_mid) + p.gate_b[gl * p.E + e];
   }
   }
-  __syncthreads();
+  sync();
   if (warp != 0) return;
   const unsigned long long t2 = p.phase_ns ? gtimer() : 0;
 
@@ -453,6 +470,8 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
     warp_topk(zr, valid && finite, p.K, sel);
   }
   const float gap = p.forced ? NAN : topk_gap(zr, valid, sel, p.K);
+  const float zs_r = warp_max(valid ? fabsf(zr) : 0.f);
+  const float zs_g = do_guess ? warp_max(valid ? fabsf(zg) : 0.f) : 0.f;
   const bool go = finite && routed_ok;
   float psel[kMaxK];
   float ssel = 0.f;
@@ -488,8 +507,10 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
     S.last_touch[lane] = st.last_touch[0];
   }
   // speculation guesses
+  float ggap = NAN;
   if (do_guess) {
     warp_topk(zg, valid && finite, p.K, gs);
+    ggap = topk_gap(zg, valid, gs, p.K);
     sort_small(gs, p.K);
   }
   int pf[kMaxK];
@@ -514,6 +535,9 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
     rec->ev = ev;
     rec->flags = flags;
     rec->gap = gap;
+    rec->guess_gap = ggap;
+    rec->zscale[0] = zs_r;
+    rec->zscale[1] = zs_g;
     if (flags) atomicOr(p.err, static_cast<int>(flags));
     int nd = 0, nc = 0, np = 0;
     if (go && ok) {
@@ -620,6 +644,13 @@ __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) 
       atomicAdd(&p.phase_ns[5], 1ull);
     }
   }
+}
+
+template <int EM>  // compile-time bound on E (8 for Mixtral) so the accumulators stay in registers
+__global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) {
+  pdl_trigger();  // the FFN pass may launch and wait for the decision meanwhile
+  __shared__ GateSmem gsm;
+  gate_cache_body<EM>(p, gsm, threadIdx.x, blockDim.x, [] { __syncthreads(); }, true);
 }
 
 // ---- K3: expert FFN over the selected slots ---------------------------------------------

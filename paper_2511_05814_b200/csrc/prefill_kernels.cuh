@@ -176,6 +176,8 @@ __global__ void __launch_bounds__(256) pf_gate_kernel(PfGateParams p) {
   else
     warp_topk(zr, valid && finite, p.K, sel);
   const float gap = p.forced ? NAN : topk_gap(zr, valid, sel, p.K);
+  const float zs_r = warp_max(valid ? fabsf(zr) : 0.f);
+  const float zs_g = do_guess ? warp_max(valid ? fabsf(zg) : 0.f) : 0.f;
   float psel[kMaxK], ssel = 0.f;
   for (int j = 0; j < p.K; ++j) {
     psel[j] = __shfl_sync(FULL, prob, sel[j] & 31);
@@ -185,8 +187,10 @@ __global__ void __launch_bounds__(256) pf_gate_kernel(PfGateParams p) {
     for (int j = 0; j < p.K; ++j) psel[j] = psel[j] / ssel;
   for (int j = 0; j < p.K; ++j) acts[j] = sel[j];
   sort_small(acts, p.K);
+  float ggap = NAN;
   if (do_guess) {
     warp_topk(zg, valid && finite, p.K, gs);
+    ggap = topk_gap(zg, valid, gs, p.K);
     sort_small(gs, p.K);
   }
   if (lane == 0) {
@@ -203,6 +207,9 @@ __global__ void __launch_bounds__(256) pf_gate_kernel(PfGateParams p) {
     const uint32_t fl = (finite ? 0u : 1u) | (routed_ok ? 0u : 4u);
     rec->flags = fl;
     rec->gap = gap;
+    rec->guess_gap = ggap;
+    rec->zscale[0] = zs_r;
+    rec->zscale[1] = zs_g;
     if (fl) atomicOr(p.err, static_cast<int>(fl));
     p.inv[t] = inv_mid;
   }

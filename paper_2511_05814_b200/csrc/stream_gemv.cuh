@@ -58,6 +58,11 @@ struct StreamParams {
   // UP: scale applied to xin while staging (1/rms(h') from the gate), or nullptr
   const float* xscale;
   int stream_only;         // microbenchmark: consumers release stages without computing
+  // MIX with fuse_gate: the last CTA to finish (done_ctr, zero between launches) runs the
+  // gate / cache step on the summed partials -- no separate gate launch on the critical path
+  int fuse_gate;
+  unsigned int* done_ctr;
+  GateParams gate;
 };
 
 // Which experts this launch covers: (selection slot j, weight block), in ascending expert
@@ -289,6 +294,27 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
         }
         acc = warp_sum(acc);
         if (lane == 0) p.part[static_cast<size_t>(blockIdx.x) * njob + q] = acc;
+      }
+      if (p.fuse_gate) {
+        // last-CTA-done: the CTA whose ticket completes the grid sums every CTA's partials
+        // (fence: they are visible once their ticket is) and takes the gate / cache step
+        __shared__ int s_last;
+        consumers_sync();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          s_last = atomicAdd(p.done_ctr, 1u) == gridDim.x - 1;
+        }
+        consumers_sync();
+        if (s_last) {
+          __threadfence();
+          // the stage ring is idle (every stage consumed): it holds the gate's working set
+          GateSmem& gsm = *reinterpret_cast<GateSmem*>(stage_base);
+          if (threadIdx.x == 0) *p.done_ctr = 0u;   // ready for the next launch (stream order)
+          if (p.gate.E <= 8)
+            gate_cache_body<8>(p.gate, gsm, threadIdx.x, kStreamWarps * 32, [] { consumers_sync(); }, false);
+          else
+            gate_cache_body<kMaxE>(p.gate, gsm, threadIdx.x, kStreamWarps * 32, [] { consumers_sync(); }, false);
+        }
       }
     }
   }

@@ -175,6 +175,28 @@ class OffloadEngine:
                                                         int(build)))
         self._coded = segment
 
+    def attach_peer_tier(self, blocks) -> None:
+        """NVLink peer-HBM miss tier (include/moeb200.h moe_engine_attach_peer_tier):
+        blocks maps (layer, expert) -> a CUDA uint8 tensor of expert_bytes holding that raw expert
+        block, on a peer GPU (replicas.open_peer_tier) or on this one; None detaches.  Misses and
+        prefetches of those experts are copied device to device instead of over PCIe; the
+        decisions, traces and outputs do not change.  The tensors are kept alive here."""
+        cfg = self.config
+        if blocks is None:
+            _native.check(self._lib.moe_engine_attach_peer_tier(self._h, None, 0))
+            self._peer = None
+            return
+        n = cfg.num_layers * cfg.num_experts
+        table = (ctypes.c_void_p * n)()
+        for (l, e), t in blocks.items():
+            if not (0 <= l < cfg.num_layers and 0 <= e < cfg.num_experts):
+                raise ConfigError(f"peer block ({l}, {e}) out of range")
+            if t.device.type != "cuda" or t.numel() * t.element_size() != cfg.expert_bytes:
+                raise ConfigError("a peer block is a CUDA tensor of expert_bytes")
+            table[l * cfg.num_experts + e] = t.data_ptr()
+        _native.check(self._lib.moe_engine_attach_peer_tier(self._h, table, n))
+        self._peer = dict(blocks)
+
     def load_toy_model(self, model) -> None:
         """Upload a ToyMoeModel's weights (reference layout, rounded to f32)."""
         cfg = self.config
@@ -386,8 +408,25 @@ class OffloadEngine:
         evaluation could order differently (north star: ties within tolerance are stated)."""
         cfg = self.config
         gaps = np.zeros((T, cfg.num_layers), np.float32)
-        _native.check(self._lib.moe_engine_record_gaps(self._h, t0, T, gaps.ctypes.data, None))
+        _native.check(self._lib.moe_engine_record_gaps(self._h, t0, T, gaps.ctypes.data, None, None, None))
         return gaps
+
+    def record_guess_gaps(self, t0: int, T: int) -> np.ndarray:
+        """(T, L-1) margins of the reference-definition guesses (gate_l on the output of l-1,
+        toymoe.py:178-180): NaN when speculation is not recorded."""
+        cfg = self.config
+        gg = np.full((T, max(cfg.num_layers - 1, 0)), np.nan, np.float32)
+        if cfg.num_layers > 1:
+            _native.check(self._lib.moe_engine_record_gaps(self._h, t0, T, None, gg.ctypes.data, None, None))
+        return gg
+
+    def record_logit_scales(self, t0: int, T: int) -> np.ndarray:
+        """(T, L, 2) largest |logit| of the route and of the guess per step (0 without a
+        guess): fp32 logit error grows with this scale, so near-tie tests are relative to it."""
+        cfg = self.config
+        zs = np.zeros((T, cfg.num_layers, 2), np.float32)
+        _native.check(self._lib.moe_engine_record_gaps(self._h, t0, T, None, None, zs.ctypes.data, None))
+        return zs
 
     def record_early_guesses(self, t0: int, T: int) -> np.ndarray:
         """(T, L-1, K) early guesses: at step (t, l) the top-k of gate_{l+1} on h'_l (ascending),
@@ -396,7 +435,7 @@ class OffloadEngine:
         L, K = cfg.num_layers, cfg.top_k
         early = np.full((T, max(L - 1, 0), K), -1, np.int64)
         if L > 1:
-            _native.check(self._lib.moe_engine_record_gaps(self._h, t0, T, None, early.ctypes.data))
+            _native.check(self._lib.moe_engine_record_gaps(self._h, t0, T, None, None, None, early.ctypes.data))
         return early
 
     def event_log(self, t0: int, T: int, warmup_tokens: int = 0):

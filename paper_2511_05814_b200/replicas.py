@@ -182,3 +182,40 @@ def reduce_timing(elapsed_ms: float, tokens: int, world: int):
     dist.all_reduce(n, op=dist.ReduceOp.SUM)
     ms, total = float(t.item()), int(n.item())
     return total / (ms / 1e3), ms, total
+
+
+def peer_home(layer: int, expert: int, num_experts: int, world: int) -> int:
+    """The replica whose HBM holds the home copy of (layer, expert) in the peer tier: round robin
+    over the node's ranks, so each GPU holds 1/world of the raw experts (8x7B on 8 GPUs: 11.3 GB)."""
+    return (layer * num_experts + expert) % world
+
+
+def open_peer_tier(engine, rank: int, world: int, all_gather_object: Callable, include_own: bool = False):
+    """NVLink peer-HBM miss tier: every replica copies its home share of the raw
+    experts from its host store into its own HBM once, publishes the buffer as a CUDA IPC handle,
+    and maps the other replicas' buffers; the engine then serves misses of experts homed on a
+    peer with device-to-device copies over NVLink instead of PCIe (moe_engine_attach_peer_tier).
+    include_own also serves the rank's own home experts from its HBM (the one-GPU stand-in).
+    all_gather_object(obj) -> [obj of rank 0, ..., rank world-1].  Returns (home tensor, blocks):
+    keep both alive while the tier is attached."""
+    import torch
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    cfg = engine.config
+    L, E = cfg.num_layers, cfg.num_experts
+    mine = [(l, e) for l in range(L) for e in range(E) if peer_home(l, e, E, world) == rank]
+    home = torch.empty((max(1, len(mine)), cfg.expert_bytes), dtype=torch.uint8, device=engine._dev)
+    for i, (l, e) in enumerate(mine):
+        home[i].copy_(torch.from_numpy(engine.expert_block(l, e)))
+    torch.cuda.synchronize(engine._dev)
+    handles = all_gather_object(reduce_tensor(home) if world > 1 else None)
+    blocks = {}
+    for r in range(world):
+        if r == rank and not include_own:
+            continue
+        t = home if r == rank else handles[r][0](*handles[r][1])
+        owned = [(l, e) for l in range(L) for e in range(E) if peer_home(l, e, E, world) == r]
+        for i, le in enumerate(owned):
+            blocks[le] = t[i]
+    engine.attach_peer_tier(blocks)
+    return home, blocks

@@ -145,13 +145,39 @@ def forward_token(model: ToyMoeModel, h_in: HiddenState, layer: int):
     return HiddenState(values=out.cpu().numpy(), layer=layer), frozenset(sel.cpu().tolist())
 
 
+# fp32 margins below this fraction of the logit scale are re-decided in fp64 (run_model)
+NEAR_TIE_REL = 1e-4
+
+
+def _fp64_token(model: ToyMoeModel, x, K: int):
+    """One token through every layer on the fp64 device path: (acts (L, K), guesses (L-1, K))
+    sorted ascending -- the reference's run_model loop body (toymoe.py:175-185)."""
+    L = model.config.shape.num_layers
+    h = HiddenState(values=np.asarray(x, dtype=np.float64), layer=-1)
+    acts = np.zeros((L, K), np.int64)
+    guesses = np.zeros((max(L - 1, 0), K), np.int64)
+    for l in range(L):
+        if l >= 1:
+            guesses[l - 1] = sorted(speculate_next(h, model.gates[l], K))
+        h, sel = forward_token(model, h, l)
+        acts[l] = sorted(sel)
+    return acts, guesses
+
+
 def run_model(config: ToyModelConfig, cache_size: Optional[int] = None, policy=None,
               return_engine_stats: bool = False):
     """Decode config.tokens seeded tokens through all layers on the GPU engine.
 
-    Returns (ActivationTrace, SpeculationTrace) exactly as toymoe.run_model does
-    (toymoe.py:159-190).  The engine always runs its per-layer HBM cache; by default it
-    holds every expert (cache_size = E, LRU) so only compulsory misses are transferred.
+    Returns (ActivationTrace, SpeculationTrace) as toymoe.run_model does (toymoe.py:159-190).
+    The engine always runs its per-layer HBM cache; by default it holds every expert
+    (cache_size = E, LRU) so only compulsory misses are transferred.
+
+    The engine computes in fp32, the reference in fp64: a selection (or guess) whose top-k
+    logit margin is within fp32 reach of a tie could be ordered differently.  The engine
+    records every step's margin and logit scale; each token with a margin below
+    NEAR_TIE_REL x max(1, |logit|) anywhere is re-decoded on the fp64 device path
+    (forward_token / speculate_next, the reference's arithmetic), so the returned traces
+    are the fp64 ones wherever fp32 could not decide.
     """
     from .engine import OffloadEngine, EngineConfig
     from .policies import PolicyKind
@@ -174,10 +200,19 @@ def run_model(config: ToyModelConfig, cache_size: Optional[int] = None, policy=N
         eng.load_toy_model(model)
         eng.decode(inputs.astype(np.float32))
         rec = eng.records(0, T)
+        gaps, ggaps = eng.record_gaps(0, T), eng.record_guess_gaps(0, T)
+        zs = eng.record_logit_scales(0, T)
         stats = eng.stats()
-    acts = rec["acts"]
+    acts, guessed = rec["acts"], rec["guessed"]
+    near = (gaps < NEAR_TIE_REL * np.maximum(1.0, zs[:, :, 0])).any(axis=1)
     if L >= 2:
-        guessed, actual = rec["guessed"], acts[:, 1:, :]
+        near |= (ggaps < NEAR_TIE_REL * np.maximum(1.0, zs[:, 1:, 1])).any(axis=1)
+    for t in np.nonzero(near)[0]:
+        acts[t], g = _fp64_token(model, inputs[t], K)
+        if L >= 2:
+            guessed[t] = g
+    if L >= 2:
+        actual = acts[:, 1:, :]
     else:
         guessed = actual = np.zeros((0, 0, K), np.int64)
     act_trace = ActivationTrace(shape, acts)

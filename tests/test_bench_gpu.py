@@ -65,3 +65,36 @@ def test_bench_8x22b_shape_reduced():
     assert d["config"]["workload"].startswith("configs[4]") and d["value"] > 0
     assert list(d["variants"]) == ["lfu+prefetch"]
     assert d["variants"]["lfu+prefetch"]["prefetch_issued"] > 0
+
+
+def test_two_replicas_on_one_gpu_through_bench():
+    """The N>1 replica path end to end on the one GPU gpurun has: torch.distributed.run with 2
+    ranks (gloo, MOEB200_REPLICA_DEVICE=0), a node-shared raw + coded expert store created by
+    local rank 0 and page-locked by both, one engine per rank on disjoint token streams, and the
+    peer-HBM tier (each rank's home half of the raw experts in HBM, the other rank's mapped
+    through CUDA IPC).  Every replica's live cache traces equal the oracle replay of its own
+    selections, and the line aggregates both ranks' tokens over the slowest rank's time."""
+    import os
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, MOEB200_REPLICA_DEVICE="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), "--gpus", "2",
+           "--layers", "4", "--steps", "6", "--warmup", "3", "--variants", "lru,lfu+prefetch",
+           "--prefill-tokens", "0", "--tiny-tokens", "0", "--replay-streams", "0",
+           "--trace-variants", "", "--no-cpu-baseline", "--peer-tier"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 2
+    assert d["engine"]["shared_store"] is True
+    assert d["parity"]["replicas_with_oracle_equal_traces"] == "2/2"
+    assert d["parity"]["traces_equal_oracle_replay_all_variants"]
+    # the peer tier (rank 1's HBM mapped by rank 0 over CUDA IPC) served part of the misses
+    assert d["engine"]["peer_tier"].startswith("NVLink")
+    assert all(v["peer_tier_GBps"] > 0 for v in d["variants"].values())
+    # value = both ranks' tokens / the slowest rank's time
+    assert abs(d["value"] - 2 * d["steps"] / (d["ms_per_step"] * d["steps"] / 1e3)) < 1e-6 * d["value"]

@@ -262,3 +262,23 @@ def test_reference_suite_model_api_calls():
             out, sel = got
             assert sorted(sel) == rec["result"]["selected"] and out.layer == rec["result"]["layer"]
             np.testing.assert_allclose(out.values, rec["result"]["values"], rtol=1e-12, atol=1e-12)
+
+
+def test_run_model_near_tie_fallback_is_the_fp64_path(monkeypatch):
+    """run_model re-decodes tokens with a near-tie margin on the fp64 device path.  Forcing
+    every token through that path (threshold huge) reproduces the reference's traces exactly
+    as the fp32 engine does (T1 and a deep, large-mixing config), and the fp32 engine's own
+    margins on T1 are far above the threshold."""
+    from paper_2511_05814_b200 import toymoe
+
+    cfgs = [ToyModelConfig(ModelShape(4, 8, 2), hidden_dim=256, mixing_scale=0.1, seed=42, tokens=64),
+            ToyModelConfig(ModelShape(6, 8, 2), hidden_dim=64, mixing_scale=3.0, seed=7, tokens=24)]
+    base = [run_model(c) for c in cfgs]
+    monkeypatch.setattr(toymoe, "NEAR_TIE_REL", 1e30)
+    forced = [run_model(c) for c in cfgs]
+    for (a0, s0), (a1, s1) in zip(base, forced):
+        assert np.array_equal(a0.activations, a1.activations)
+        assert np.array_equal(s0.guessed, s1.guessed)
+    ref_acts, ref_guessed, _ = oracle.toy_run_model(4, 8, 2, 256, 0.1, 1.0, 42, 64)
+    assert np.array_equal(forced[0][0].activations, ref_acts)
+    assert np.array_equal(forced[0][1].guessed, ref_guessed)
