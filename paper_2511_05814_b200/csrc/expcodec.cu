@@ -13,7 +13,6 @@ namespace xc {
 namespace {
 
 inline int expo(uint16_t w) { return (w >> 7) & 0xFF; }
-inline uint32_t pad8(uint32_t x) { return (x + 7) & ~7u; }
 
 struct ChunkStats {
   uint8_t base, win;
@@ -68,7 +67,7 @@ Plan make_plan(const uint16_t* in, uint64_t n, int mode_req) {
         if (dl < 256) in2 += hist[dl];
       }
       const uint32_t l2 = cnt - in1, l3 = l2 - in2;
-      const uint64_t cost = 3ull * pad8(l2) + 8ull * l3;
+      const uint64_t cost = 3ull * l2 + 8ull * l3;
       if (cost < best) best = cost, s.win = static_cast<uint8_t>(w), s.l2 = l2, s.l3 = l3;
     }
     p.st[c] = s;
@@ -77,7 +76,7 @@ Plan make_plan(const uint16_t* in, uint64_t n, int mode_req) {
   for (const auto& s : p.st) {
     t3 += s.e3;
     t4 += s.e4;
-    tl2 += pad8(s.l2);
+    tl2 += s.l2;
     tl3 += s.l3;
   }
   const uint64_t head = align16(sizeof(PartHeader)) + align16(sizeof(ChunkEntry) * p.nch) + align16(n);
@@ -97,7 +96,7 @@ Plan make_plan(const uint16_t* in, uint64_t n, int mode_req) {
     p.esc_off[c] = run;
     p.l2_off[c] = run2;
     run += p.mode == 3 ? s.e3 : p.mode == 4 ? s.e4 : s.l3;
-    run2 += p.mode == kMode23 ? pad8(s.l2) : 0;
+    run2 += p.mode == kMode23 ? s.l2 : 0;
   }
   p.low_off = align16(sizeof(PartHeader)) + align16(sizeof(ChunkEntry) * p.nch);
   p.code_off = p.low_off + align16(n);
@@ -151,9 +150,15 @@ uint64_t encode(const uint16_t* in, uint64_t n, int mode_req, uint8_t* out) {
     uint32_t ei = p.esc_off[c];
     uint64_t l2i = p.l2_off[c];
     const int base = p.st[c].base, win = e.win;
-    // chunks start on whole bytes of every plane (kChunk * k bits, 24-bit level-2 runs)
+    // chunks start on whole bytes of the low and level-1 planes (kChunk * k bits); mode 23's
+    // level-2 codes run on across chunks, each warp's start recorded in the chunk entry
     for (uint64_t i = a; i < b; ++i) {
       const uint16_t w = in[i];
+      if (p.mode == kMode23 && i > a && (i - a) % kWarpWeights == 0) {
+        const int wq = static_cast<int>((i - a) / kWarpWeights) - 1;
+        ce[c].l2_rel[wq] = static_cast<uint16_t>(l2i - p.l2_off[c]);
+        ce[c].esc_rel[wq] = static_cast<uint16_t>(ei - p.esc_off[c]);
+      }
       low[i] = static_cast<uint8_t>(((w >> 8) & 0x80) | (w & 0x7F));
       const int dl = base - expo(w);
       if (p.mode == kMode23) {
@@ -228,9 +233,8 @@ __device__ __forceinline__ uint32_t spread2(uint32_t cb) {
   return (s | (s << 6)) & 0x03030303u;
 }
 
-// One CTA per chunk, 32 consecutive weights per thread; escapes ranked by block scans.
-// Mode 23 decodes four weights per step in byte lanes (the exponents of a code byte by one
-// subtraction, the bf16 words by byte permutes) and patches the level-1 escapes in place.
+// Modes 3 / 4: one CTA per chunk, 32 consecutive weights per thread; escapes ranked by a
+// block scan.
 template <int K>
 __global__ void __launch_bounds__(kThreads) decode_kernel(const PartBatch pb,
                                                           long long* __restrict__ prof) {
@@ -259,20 +263,14 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const PartBatch pb,
   const bool active = first < h.n;
   const int cnt = active ? static_cast<int>(h.n - first < 32 ? h.n - first : 32) : 0;
   uint32_t lo[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  uint64_t c0 = 0, c1 = 0;  // K-bit codes 0..15 / 16..31 (mode 23: all 32 2-bit codes in c0)
-  uint32_t escm = 0;        // modes 3 / 4: bit j = weight j escapes to a byte
-  uint64_t zm = 0;          // mode 23: bit 2j = weight j escapes to level 2
+  uint64_t c0 = 0, c1 = 0;  // K-bit codes 0..15 / 16..31
+  uint32_t escm = 0;        // bit j = weight j escapes to a byte
   if (active) {
     const uint4* lp = reinterpret_cast<const uint4*>(part + h.low_off + first);
     const uint4 l0 = lp[0], l1 = lp[1];
     lo[0] = l0.x; lo[1] = l0.y; lo[2] = l0.z; lo[3] = l0.w;
     lo[4] = l1.x; lo[5] = l1.y; lo[6] = l1.z; lo[7] = l1.w;
-    if constexpr (K == kMode23) {
-      const uint2 q = *reinterpret_cast<const uint2*>(part + h.code_off + first / 4);
-      c0 = (static_cast<uint64_t>(q.y) << 32) | q.x;
-      zm = ~(c0 | (c0 >> 1)) & 0x5555555555555555ull;
-      if (cnt < 32) zm &= (1ull << (2 * cnt)) - 1ull;
-    } else if constexpr (K == 4) {
+    if constexpr (K == 4) {
       const uint4 q = *reinterpret_cast<const uint4*>(part + h.code_off + first / 2);
       c0 = (static_cast<uint64_t>(q.y) << 32) | q.x;
       c1 = (static_cast<uint64_t>(q.w) << 32) | q.z;
@@ -282,100 +280,204 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const PartBatch pb,
       c0 = (static_cast<uint64_t>(w1) << 32) | w0;                    // stream bits 0..63
       c1 = (static_cast<uint64_t>(w2) << 16) | (w1 >> 16);            // stream bits 48..95
     }
-    if constexpr (K != kMode23) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const uint32_t code = static_cast<uint32_t>((j < 16 ? c0 >> (K * j) : c1 >> (K * (j - 16))) & ((1u << K) - 1));
-        if (j < cnt && !code) escm |= 1u << j;
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t code = static_cast<uint32_t>((j < 16 ? c0 >> (K * j) : c1 >> (K * (j - 16))) & ((1u << K) - 1));
+      if (j < cnt && !code) escm |= 1u << j;
+    }
+  }
+  const int before1 = block_exclusive_scan(__popc(escm), warp_tot);
+  if (!active) return;
+  uint32_t o[16];
+  const uint8_t* esc = part + h.esc_off + ce.esc_off + before1;
+  int e = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const uint32_t b8 = (lo[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+    const uint32_t code = static_cast<uint32_t>((j < 16 ? c0 >> (K * j) : c1 >> (K * (j - 16))) & ((1u << K) - 1));
+    uint32_t ex = static_cast<uint32_t>(ce.base) + 1u - code;
+    if ((escm >> j) & 1u) {  // rare: exponent from the side list
+      ex = esc[e];
+      ++e;
+    }
+    const uint32_t w = bf16_word(b8, ex);
+    if (j & 1) o[j >> 1] |= w << 16;
+    else o[j >> 1] = w;
+  }
+  store_out(out, first, cnt, o);
+  if (prof && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&prof[1], static_cast<long long>(t));
+  }
+}
+
+// ---- mode 23: warp-independent, table-driven -------------------------------------------
+// Expansion selectors for one group of four weights, indexed by its code byte (four 2-bit
+// level-1 codes, weight i at bits 2i): nibble i selects byte `rank` of the group's level-2
+// value word (operand a of the byte permute) for a zero code, byte 4 + c of the level-1
+// table word (operand b: byte c = exponent of code c) otherwise; bits 16.. hold 8 x the
+// number of zero codes (how far the value stream advances past the group).
+struct ExpandTable {
+  uint32_t v[256];
+  constexpr ExpandTable() : v() {
+    for (int i = 0; i < 256; ++i) {
+      uint32_t sel = 0, rank = 0;
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t code = (static_cast<uint32_t>(i) >> (2 * k)) & 3u;
+        sel |= (code ? 4u + code : rank++) << (4 * k);
+      }
+      v[i] = sel | ((8u * rank) << 16);
+    }
+  }
+};
+__device__ constexpr ExpandTable kExpand{};
+
+// twelve bits = four 3-bit codes -> the low bits of four nibbles (a byte-permute selector)
+__device__ __forceinline__ uint32_t nib3(uint32_t x) {
+  const uint32_t a = (x & 0x3Fu) | ((x << 2) & 0x3F00u);      // codes 0,1 | codes 2,3
+  return (a & 0x0707u) | ((a << 1) & 0x7070u);
+}
+
+__device__ __forceinline__ int warp_exclusive_sum(int v, int lane) {
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  return incl - v;
+}
+
+// One CTA per 4096-weight chunk, four independent warps of 1024 weights, 32 per lane.
+// Per lane: (1) its level-1 escapes (zero 2-bit codes) ranked by a warp scan; (2) their
+// level-2 codes read as one bit run and turned into exponent bytes by byte permutes through
+// an 8-entry table (the rare zero level-2 codes take an escape byte); (3) each group of four
+// weights resolved by one byte permute -- level-1 exponents from a 3-entry table, level-2
+// values from the head of the lane's value stream -- with the selector from kExpand;
+// (4) bf16 words from the exponent and sign|mantissa bytes by byte permutes.
+__global__ void __launch_bounds__(kThreads) decode23_kernel(const PartBatch pb,
+                                                            long long* __restrict__ prof) {
+  __shared__ uint32_t stab[256];
+  stab[threadIdx.x] = kExpand.v[threadIdx.x];
+  stab[threadIdx.x + kThreads] = kExpand.v[threadIdx.x + kThreads];
+  const uint8_t* part = pb.part[0];
+  uint16_t* out = pb.out[0];
+  uint32_t pstart = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxBatch; ++q)
+    if (q < pb.n && blockIdx.x >= pb.start[q]) {
+      part = pb.part[q];
+      out = pb.out[q];
+      pstart = pb.start[q];
+    }
+  if (prof && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&prof[0], 0x7fffffffffffffffll - static_cast<long long>(t));
+  }
+  const PartHeader& h = *reinterpret_cast<const PartHeader*>(part);
+  const uint32_t c = blockIdx.x - pstart;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the chunk entry as three 8-byte words (ChunkEntry: esc_off, l2_off | base, win,
+  // l2_rel[0] | l2_rel[1..2] | esc_rel[0..1] | esc_rel[2], pad); this warp's offsets picked
+  // by shifts (no indexed local copy)
+  const uint2* ep = reinterpret_cast<const uint2*>(part + align16(sizeof(PartHeader))) + 3 * c;
+  const uint2 e0 = ep[0], e1 = ep[1], e2 = ep[2];
+  const uint32_t l2_rel = warp == 0 ? 0u : warp == 1 ? e1.x >> 16 : warp == 2 ? e1.y & 0xFFFFu : e1.y >> 16;
+  const uint32_t esc_rel = warp == 0 ? 0u : warp == 1 ? e2.x & 0xFFFFu : warp == 2 ? e2.x >> 16 : e2.y & 0xFFFFu;
+  const uint64_t first = static_cast<uint64_t>(c) * kChunk + threadIdx.x * 32ull;
+  const bool active = first < h.n;
+  const int cnt = active ? static_cast<int>(h.n - first < 32 ? h.n - first : 32) : 0;
+  uint32_t lo[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint64_t c0 = 0;   // the lane's 32 level-1 codes, weight j at bits 2j
+  if (active) {
+    const uint4* lp = reinterpret_cast<const uint4*>(part + h.low_off + first);
+    const uint4 l0 = lp[0], l1 = lp[1];
+    lo[0] = l0.x; lo[1] = l0.y; lo[2] = l0.z; lo[3] = l0.w;
+    lo[4] = l1.x; lo[5] = l1.y; lo[6] = l1.z; lo[7] = l1.w;
+    const uint2 q = *reinterpret_cast<const uint2*>(part + h.code_off + first / 4);
+    c0 = (static_cast<uint64_t>(q.y) << 32) | q.x;
+  }
+  uint64_t zm = ~(c0 | (c0 >> 1)) & 0x5555555555555555ull;   // bit 2j: weight j escapes
+  if (cnt < 32) zm &= (1ull << (2 * cnt)) - 1ull;               // (cnt = 0: no escapes)
+  const int nh0 = __popc(static_cast<uint32_t>(zm)), n1 = nh0 + __popc(static_cast<uint32_t>(zm >> 32));
+  const int before1 = warp_exclusive_sum(n1, lane);
+  // chunk tables: level 1 (byte c = exponent of 2-bit code c = base - (win + c - 1)) and
+  // level 2 (byte c = exponent of 3-bit code c: r = w2 + c - 1, dl = r < win ? r : r + 3).
+  // Bytes of codes a chunk cannot hold (dl > base) may borrow from higher bytes, which are
+  // unused codes too; byte 0 (the escape code) is never read.
+  const uint32_t base = e1.x & 0xFFu, win = (e1.x >> 8) & 0xFFu, w2 = win > 2u ? win - 2u : 0u, d = win - w2;
+  const uint32_t lut1 = (base - win) * 0x01010100u - 0x02010000u;
+  const uint32_t b4 = base * 0x01010101u;
+  const uint32_t lut2lo = b4 - (w2 * 0x01010100u + 0x02010000u + (d == 0 ? 0x03030300u : d == 1 ? 0x03030000u : 0x03000000u));
+  const uint32_t lut2hi = b4 - (w2 * 0x01010101u + 0x06050403u + 0x03030303u);
+  // level-2 values of each half (16 weights: at most 16 escapes), as a byte stream in 4 words
+  const uint32_t* l2w = reinterpret_cast<const uint32_t*>(part + h.l2_off);
+  const uint64_t l2base = static_cast<uint64_t>(e0.y) + l2_rel + before1;
+  uint32_t v[2][4];
+  uint32_t zq[2][4];   // zero level-2 codes: bit 4i of quartet q = code 4q + i of the half
+  int n2 = 0;
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+    const int nh = hf ? n1 - nh0 : nh0;
+    uint64_t x = 0;
+    if (nh) {
+      const uint64_t bit = (l2base + (hf ? nh0 : 0)) * 3ull;
+      const uint32_t* wp = l2w + (bit >> 5);
+      const uint32_t s = static_cast<uint32_t>(bit & 31);
+      const uint32_t w0 = wp[0], w1 = wp[1], w2w = wp[2];
+      x = (static_cast<uint64_t>(__funnelshift_r(w1, w2w, s)) << 32) | __funnelshift_r(w0, w1, s);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      v[hf][q] = 0;
+      zq[hf][q] = 0;
+      // quartets 2, 3 only when some lane of the warp needs them (rare past 8 escapes)
+      if (q < 2 || __any_sync(0xffffffffu, nh > 4 * q)) {
+        const uint32_t sel = nib3(static_cast<uint32_t>(x >> (12 * q)) & 0xFFFu);
+        v[hf][q] = __byte_perm(lut2lo, lut2hi, sel);
+        uint32_t z = ~(sel | (sel >> 1) | (sel >> 2)) & 0x1111u;
+        const int valid = nh - 4 * q;   // codes of this quartet that belong to the lane
+        z &= valid >= 4 ? 0x1111u : valid <= 0 ? 0u : (0x1111u >> (4 * (4 - valid)));
+        zq[hf][q] = z;
+        n2 += __popc(z);
       }
     }
   }
-  const int n1 = K == kMode23 ? __popcll(zm) : __popc(escm);
-  const int before1 = block_exclusive_scan(n1, warp_tot);
+  // rare: zero level-2 codes take the next escape bytes (weight order across the warp)
+  if (__any_sync(0xffffffffu, n2)) {
+    const int before2 = warp_exclusive_sum(n2, lane);
+    const uint8_t* esc = part + h.esc_off + e0.x + esc_rel + before2;
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        for (uint32_t z = zq[hf][q]; z; z &= z - 1u) {
+          const int i = (__ffs(z) - 1) >> 2;
+          const uint32_t sh = 8u * i;
+          v[hf][q] = (v[hf][q] & ~(0xFFu << sh)) | (static_cast<uint32_t>(*esc++) << sh);
+        }
+  }
+  __syncthreads();   // stab
+  if (!active) return;
   uint32_t o[16];
-  if constexpr (K == kMode23) {
-    // level-2 codes of this thread: n1 consecutive 3-bit codes from index l2_off + before1,
-    // held in a 128-bit shift register (r0 low)
-    const uint64_t bit = (static_cast<uint64_t>(ce.l2_off) + before1) * 3;
-    const uint32_t* wp = reinterpret_cast<const uint32_t*>(part + h.l2_off) + (bit >> 5);
-    uint64_t r0 = 0, r1 = 0;
-    if (n1) {
-      const uint64_t wlo = (static_cast<uint64_t>(wp[1]) << 32) | wp[0];
-      const uint64_t whi = (static_cast<uint64_t>(wp[3]) << 32) | wp[2];
-      const int sh = static_cast<int>(bit & 31);
-      r0 = sh ? (wlo >> sh) | (whi << (64 - sh)) : wlo;
-      r1 = whi >> sh;
-    }
-    // byte escapes = zero 3-bit fields among the first n1 (fields 0..20 in r0, 21.. after it)
-    int n2 = 0;
-    if (n1) {
-      constexpr uint64_t kField = 0x1249249249249249ull;  // bit 3i, i = 0..20
-      const int f0 = n1 < 21 ? n1 : 21, f1 = n1 - f0;
-      const uint64_t a = r0, b = (r0 >> 63) | (r1 << 1);
-      const uint64_t m0 = f0 == 21 ? kField : kField & ((1ull << (3 * f0)) - 1ull);
-      const uint64_t m1 = f1 <= 0 ? 0ull : kField & ((1ull << (3 * f1)) - 1ull);
-      n2 = __popcll(~(a | (a >> 1) | (a >> 2)) & m0) + __popcll(~(b | (b >> 1) | (b >> 2)) & m1);
-    }
-    const int before2 = block_exclusive_scan(n2, warp_tot);
-    if (!active) return;
-    const uint8_t* esc = part + h.esc_off + ce.esc_off + before2;
-    const uint32_t win = ce.win, base = ce.base, w2 = win > 2u ? win - 2u : 0u;
-    // level-1 exponents four at a time, carry-free: ex = (base - win) - (c - 1) per byte, a zero
-    // (escape) code first raised to 1 (base - win <= 255 even when base + 1 - win = 256)
-    const uint32_t Em1x4 = (base - win) * 0x01010101u;
-    // exponent bytes of the thread's 32 weights in shared memory ([group][thread] words, so
-    // the word accesses are conflict-free), escapes patched byte-wise, then the bf16 words
-    __shared__ uint32_t xs[8 * kThreads];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      const uint32_t s1 = spread2(static_cast<uint32_t>(c0 >> (8 * g)) & 0xFFu);
-      const uint32_t z1 = (~(s1 + 0x7F7F7F7Fu) & 0x80808080u) >> 7;  // 0x01 where the code is 0
-      xs[g * kThreads + threadIdx.x] = Em1x4 - ((s1 | z1) - 0x01010101u);
-    }
-    uint8_t* xb = reinterpret_cast<uint8_t*>(xs) + threadIdx.x * 4;
-    // escape positions as a 32-bit mask (even bits of zm gathered)
-    uint64_t x = zm;
-    x = (x | (x >> 1)) & 0x3333333333333333ull;
-    x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0Full;
-    x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
-    x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
-    uint32_t em = static_cast<uint32_t>(x | (x >> 16));
-    uint32_t q0 = static_cast<uint32_t>(r0), q1 = static_cast<uint32_t>(r0 >> 32),
-             q2 = static_cast<uint32_t>(r1), q3 = static_cast<uint32_t>(r1 >> 32);
-    for (; em; em &= em - 1u) {
-      const int j = __ffs(em) - 1;
-      const uint32_t c2 = q0 & 7u;
-      q0 = __funnelshift_r(q0, q1, 3);
-      q1 = __funnelshift_r(q1, q2, 3);
-      q2 = __funnelshift_r(q2, q3, 3);
-      q3 >>= 3;
-      uint32_t ex;
-      if (c2) {
-        const uint32_t r = c2 - 1u + w2;
-        ex = base - (r < win ? r : r + 3u);
-      } else {
-        ex = *esc++;
+  for (int hf = 0; hf < 2; ++hf) {
+    uint32_t v0 = v[hf][0], v1 = v[hf][1], v2 = v[hf][2], v3 = v[hf][3];
+#pragma unroll
+    for (int gq = 0; gq < 4; ++gq) {
+      const int g = 4 * hf + gq;
+      const uint32_t e = stab[static_cast<uint32_t>(c0 >> (8 * g)) & 0xFFu];
+      const uint32_t X = __byte_perm(v0, lut1, e);
+      if (gq < 3) {   // advance the value stream past this group's escapes
+        const uint32_t sh = e >> 16;
+        v0 = __funnelshift_rc(v0, v1, sh);
+        v1 = __funnelshift_rc(v1, v2, sh);
+        v2 = __funnelshift_rc(v2, v3, sh);
+        v3 = __funnelshift_rc(v3, 0u, sh);
       }
-      xb[(j >> 2) * kThreads * 4 + (j & 3)] = static_cast<uint8_t>(ex);
-    }
-#pragma unroll
-    for (int g = 0; g < 8; ++g) bf16x4(lo[g], xs[g * kThreads + threadIdx.x], o[2 * g], o[2 * g + 1]);
-  } else {
-    if (!active) return;
-    const uint8_t* esc = part + h.esc_off + ce.esc_off + before1;
-    int e = 0;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const uint32_t b8 = (lo[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-      const uint32_t code = static_cast<uint32_t>((j < 16 ? c0 >> (K * j) : c1 >> (K * (j - 16))) & ((1u << K) - 1));
-      uint32_t ex = static_cast<uint32_t>(ce.base) + 1u - code;
-      if ((escm >> j) & 1u) {  // rare: exponent from the side list
-        ex = esc[e];
-        ++e;
-      }
-      const uint32_t w = bf16_word(b8, ex);
-      if (j & 1) o[j >> 1] |= w << 16;
-      else o[j >> 1] = w;
+      bf16x4(lo[g], X, o[2 * g], o[2 * g + 1]);
     }
   }
   store_out(out, first, cnt, o);
@@ -412,7 +514,7 @@ moe_status decode_batch(const void* const* parts_dev, const PartHeader* hs, uint
   else if (kb == 4)
     decode_kernel<4><<<grid, kThreads, 0, s>>>(pb, prof);
   else
-    decode_kernel<kMode23><<<grid, kThreads, 0, s>>>(pb, prof);
+    decode23_kernel<<<grid, kThreads, 0, s>>>(pb, prof);
   MOE_LAUNCHED();
   return MOE_OK;
 }

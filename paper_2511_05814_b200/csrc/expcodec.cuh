@@ -15,7 +15,9 @@
 //
 // Part layout (every section 16-byte aligned):
 //   PartHeader | ChunkEntry[nch] | low[n] | codes (k * n bits, or 2 * n bits in mode 23)
-//   | level-2 codes (mode 23: 3 bits each, each chunk's run padded to 8 codes) | escape bytes
+//   | level-2 codes (mode 23: 3 bits each, contiguous over the part) | escape bytes
+// Mode 23 decodes warp by warp (1024 weights, 32 per lane) with no block-level scan: each
+// chunk entry stores where its warps 1..3 start in the level-2 and escape-byte streams.
 #pragma once
 #include <cstdint>
 
@@ -37,13 +39,17 @@ struct __align__(16) PartHeader {
   uint64_t low_off, code_off, l2_off, esc_off, total;  // byte offsets from the header; size
 };
 
-struct ChunkEntry {
+struct ChunkEntry {      // 24 bytes
   uint32_t esc_off;     // index of the chunk's first escape byte
-  uint32_t l2_off;      // mode 23: index of the chunk's first level-2 code (multiple of 8)
+  uint32_t l2_off;      // mode 23: index of the chunk's first level-2 code
   uint8_t base;         // largest exponent in the chunk
   uint8_t win;          // mode 23: first dl of the level-1 window (w)
-  uint8_t pad[6];
+  uint16_t l2_rel[3];   // mode 23: first level-2 code of warps 1..3, relative to l2_off
+  uint16_t esc_rel[3];  // mode 23: first escape byte of warps 1..3, relative to esc_off
+  uint16_t pad;
 };
+static_assert(sizeof(ChunkEntry) == 24, "chunk entries are read as three 8-byte words");
+constexpr int kWarpWeights = 1024;  // mode 23: weights per decoding warp
 
 inline __host__ __device__ uint64_t align16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
 

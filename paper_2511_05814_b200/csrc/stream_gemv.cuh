@@ -298,14 +298,16 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
       if (p.fuse_gate) {
         // last-CTA-done: the CTA whose ticket completes the grid sums every CTA's partials
         // (fence: they are visible once their ticket is) and takes the gate / cache step
-        __shared__ int s_last;
+        // the flag lives in the dynamic region (xch[63]; the partial exchange uses <= 16):
+        // a static __shared__ would push static + 227 KB dynamic past the per-CTA limit
+        volatile int* s_last = reinterpret_cast<volatile int*>(xch + 63);
         consumers_sync();
         if (threadIdx.x == 0) {
           __threadfence();
-          s_last = atomicAdd(p.done_ctr, 1u) == gridDim.x - 1;
+          *s_last = atomicAdd(p.done_ctr, 1u) == gridDim.x - 1;
         }
         consumers_sync();
-        if (s_last) {
+        if (*s_last) {
           __threadfence();
           // the stage ring is idle (every stage consumed): it holds the gate's working set
           GateSmem& gsm = *reinterpret_cast<GateSmem*>(stage_base);
@@ -403,11 +405,22 @@ template <int MODE>
 inline cudaError_t launch_stream(const StreamGeom& g, int grid, const StreamParams& sp,
                                  cudaStream_t s) {
   static std::atomic<uint64_t> attrs{0};
-  once_per_device(attrs, [] {
-    cudaFuncSetAttribute(stream_gemv_kernel<MODE, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(stream_gemv_kernel<MODE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(stream_gemv_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaError_t set = cudaSuccess;
+  once_per_device(attrs, [&set] {
+    // the opt-in limit covers static + dynamic shared memory (227 KB per CTA)
+    auto opt_in = [&set](auto* fn) {
+      cudaFuncAttributes fa{};
+      cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024 - static_cast<int>(fa.sharedSizeBytes));
+      if (e != cudaSuccess && set == cudaSuccess) set = e;
+    };
+    opt_in(stream_gemv_kernel<MODE, 8>);
+    opt_in(stream_gemv_kernel<MODE, 4>);
+    opt_in(stream_gemv_kernel<MODE, 2>);
   });
+  if (set != cudaSuccess) return set;
   StreamParams p = sp;
   p.cb = g.cb;
   p.ncb = g.ncb;

@@ -46,6 +46,25 @@ def install_aliases():
 
     kernels.replay_policy_layers = replay_layers_host
 
+    # Out of scope: the expert-imbalance histogram (metrics.py:253-300) and the
+    # memory-calibration fit (costmodel.py:59-74, 135-171) are not restated in the package.
+    # The reference's test modules import them at module level, so they are bound to stubs
+    # that raise; their test classes are deselected in main().
+    def _out_of_scope(*_a, **_k):
+        raise NotImplementedError("out of scope for the B200 hot path (SURVEY §2)")
+
+    metrics = sys.modules["moesim.metrics"]
+    costmodel = sys.modules["moesim.costmodel"]
+    for mod, names in ((metrics, ("expert_histograms", "gini_coefficient", "ExpertHistogram")),
+                       (costmodel, ("estimate_peak_memory", "fit_memory_model",
+                                    "parse_memory_points", "MemoryModel"))):
+        for n in names:
+            if not hasattr(mod, n):
+                setattr(mod, n, _out_of_scope)
+
+
+OUT_OF_SCOPE = "not TestHistograms and not TestMemoryModel"
+
 
 def main(argv):
     if not REF.exists():
@@ -61,6 +80,11 @@ def main(argv):
     install_aliases()   # before the reference's conftest imports moesim
     args = [str(REF / "tests" / f) for f in files] + ["-q", "-p", "no:cacheprovider",
                                                       "--rootdir", tempfile.mkdtemp(prefix="refpkg_")]
+    if "-k" in rest:
+        i = rest.index("-k")
+        rest[i + 1] = f"({rest[i + 1]}) and {OUT_OF_SCOPE}"
+    else:
+        rest += ["-k", OUT_OF_SCOPE]
     return pytest.main(args + rest)
 
 

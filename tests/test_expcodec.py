@@ -41,7 +41,7 @@ def test_ratio_on_synthetic_weights():
 
 def _chunk_windows(enc):
     nch = int.from_bytes(enc[16:20].tobytes(), "little")
-    return [int(enc[64 + 16 * c + 9]) for c in range(nch)]
+    return [int(enc[64 + 24 * c + 9]) for c in range(nch)]   # ChunkEntry: 24 bytes, win at 9
 
 
 def _exponent_entropy_bound(w):
