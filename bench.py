@@ -724,18 +724,19 @@ def run_ours(args, world, rank, local):
     roofline_decode = None
     if xb and xms > 0:
         roofline_decode = {
-            "kernel": "xc::decode_kernel<23>: exponent-coded expert parts -> bf16 in the cache buffer",
+            "kernel": "xc::decode23p_kernel: exponent-coded expert parts -> bf16 in the cache buffer",
             "bound": "hbm", "achieved": xb / (xms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
             "frac": xb / (xms / 1e3) / 1e9 / hbm_peak,
             "achieved_in_kernel": xb / (xkms / 1e3) / 1e9 if xkms > 0 else None,
             "frac_in_kernel": xb / (xkms / 1e3) / 1e9 / hbm_peak if xkms > 0 else None,
             "launches": ktimes["xdec_launches"], "bytes_per_launch": xb / max(1, ktimes["xdec_launches"]),
             "algorithmic_bytes": "coded part read + bf16 weights written (~3.35 B / weight)",
-            "traffic": 338.8e6, "traffic_unit": "DRAM bytes of one w1|w3-part launch (ncu --set full: "
-                                                "157.95 MB read + 180.8 MB written; algorithmic 392.8 MB; "
-                                                "profiles/ncu_xc_decode_r1.md)",
-            "note": "ALU-bound in practice (ncu: ALU pipe 73 %, DRAM 34 %); overlapped with the H2D "
-                    "copies except for the step's last w2 piece",
+            "traffic": 339.4e6, "traffic_unit": "DRAM bytes of one w1|w3-part launch (ncu --set full: "
+                                                "160.6 MB read + 178.9 MB written; algorithmic 393.0 MB; "
+                                                "profiles/ncu_xc_decode_r2.md)",
+            "note": "persistent, bulk-copy fed; issue-bound in practice (ncu: issue slots 59 %, "
+                    "DRAM 42 %, 98.3 us per 117 M-weight part); overlapped with the H2D copies except "
+                    "for the step's last w2 piece",
             "peak_source": peaks.get("source", "MEASURED_PEAKS.json hbm_gbs"),
         }
     line = {

@@ -149,7 +149,8 @@ def load_library() -> ctypes.CDLL:
             f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
             " (tools/build_native.sh). There is no CPU fallback."
         )
-    lib = ctypes.CDLL(str(LIB_PATH))
+    # MOEB200_LIB: a variant build of the same library (tuning probes only)
+    lib = ctypes.CDLL(os.environ.get("MOEB200_LIB", str(LIB_PATH)))
     for name, (args, res) in _SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = args

@@ -1,8 +1,11 @@
 // Exponent codec for expert transfers (expcodec.cuh): multi-threaded host encoder, GPU decoder.
 #include "common.cuh"
 #include "expcodec.cuh"
+#include "sm100.cuh"
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -349,115 +352,128 @@ __device__ __forceinline__ int warp_exclusive_sum(int v, int lane) {
   return incl - v;
 }
 
+// per-byte rotate right by one: exponent byte e -> (e >> 1) | (e & 1) << 7, the two halves
+// of its bf16 word in place (bits 0..6 -> the high byte, bit 7 -> the low byte)
+__device__ __forceinline__ uint32_t ror8x4(uint32_t x) {
+  return ((x >> 1) & 0x7F7F7F7Fu) | ((x << 7) & 0x80808080u);
+}
+
 // One CTA per 4096-weight chunk, four independent warps of 1024 weights, 32 per lane.
 // Per lane: (1) its level-1 escapes (zero 2-bit codes) ranked by a warp scan; (2) their
 // level-2 codes read as one bit run and turned into exponent bytes by byte permutes through
-// an 8-entry table (the rare zero level-2 codes take an escape byte); (3) each group of four
+// an 8-entry table (zero level-2 codes take the next escape byte); (3) each group of four
 // weights resolved by one byte permute -- level-1 exponents from a 3-entry table, level-2
 // values from the head of the lane's value stream -- with the selector from kExpand;
-// (4) bf16 words from the exponent and sign|mantissa bytes by byte permutes.
-__global__ void __launch_bounds__(kThreads) decode23_kernel(const PartBatch pb,
+// (4) bf16 words from the exponent and sign|mantissa bytes: every table holds its exponents
+// rotated (ror8x4), so each half-word is one 3-input logic op, then two byte permutes.
+// The part descriptors come from the host copy of the headers (kernel parameters), so the
+// chunk's loads issue at once.
+__global__ void __launch_bounds__(kThreads) decode23_kernel(const __grid_constant__ Batch23 pb,
                                                             long long* __restrict__ prof) {
   __shared__ uint32_t stab[256];
+  __shared__ uint32_t vsm[kThreads * 8];   // escape-byte patching: [warp][word][lane]
   stab[threadIdx.x] = kExpand.v[threadIdx.x];
   stab[threadIdx.x + kThreads] = kExpand.v[threadIdx.x + kThreads];
-  const uint8_t* part = pb.part[0];
-  uint16_t* out = pb.out[0];
-  uint32_t pstart = 0;
-#pragma unroll
-  for (int q = 1; q < kMaxBatch; ++q)
-    if (q < pb.n && blockIdx.x >= pb.start[q]) {
-      part = pb.part[q];
-      out = pb.out[q];
-      pstart = pb.start[q];
-    }
+  const uint32_t bx = blockIdx.x;
+  const int pi = (bx >= pb.start[1]) + (bx >= pb.start[2]) + (bx >= pb.start[3]);
+  const Part23& P = pb.p[pi];
+  const uint8_t* part = P.part;
   if (prof && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMax(&prof[0], 0x7fffffffffffffffll - static_cast<long long>(t));
   }
-  const PartHeader& h = *reinterpret_cast<const PartHeader*>(part);
-  const uint32_t c = blockIdx.x - pstart;
+  const uint32_t c = bx - pb.start[pi];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // 32-bit weight and code indices (decode_batch: n < 2^30)
+  const uint32_t n = static_cast<uint32_t>(P.n);
+  const uint32_t first = c * kChunk + threadIdx.x * 32u;
+  const bool active = first < n;
+  const int cnt = active ? static_cast<int>(min(n - first, 32u)) : 0;
   // the chunk entry as three 8-byte words (ChunkEntry: esc_off, l2_off | base, win,
   // l2_rel[0] | l2_rel[1..2] | esc_rel[0..1] | esc_rel[2], pad); this warp's offsets picked
   // by shifts (no indexed local copy)
   const uint2* ep = reinterpret_cast<const uint2*>(part + align16(sizeof(PartHeader))) + 3 * c;
   const uint2 e0 = ep[0], e1 = ep[1], e2 = ep[2];
-  const uint32_t l2_rel = warp == 0 ? 0u : warp == 1 ? e1.x >> 16 : warp == 2 ? e1.y & 0xFFFFu : e1.y >> 16;
-  const uint32_t esc_rel = warp == 0 ? 0u : warp == 1 ? e2.x & 0xFFFFu : warp == 2 ? e2.x >> 16 : e2.y & 0xFFFFu;
-  const uint64_t first = static_cast<uint64_t>(c) * kChunk + threadIdx.x * 32ull;
-  const bool active = first < h.n;
-  const int cnt = active ? static_cast<int>(h.n - first < 32 ? h.n - first : 32) : 0;
   uint32_t lo[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  uint64_t c0 = 0;   // the lane's 32 level-1 codes, weight j at bits 2j
+  uint2 cw = make_uint2(0u, 0u);   // the lane's 32 level-1 codes, weight j at bits 2j
   if (active) {
-    const uint4* lp = reinterpret_cast<const uint4*>(part + h.low_off + first);
+    const uint4* lp = reinterpret_cast<const uint4*>(part + P.low_off + first);
     const uint4 l0 = lp[0], l1 = lp[1];
     lo[0] = l0.x; lo[1] = l0.y; lo[2] = l0.z; lo[3] = l0.w;
     lo[4] = l1.x; lo[5] = l1.y; lo[6] = l1.z; lo[7] = l1.w;
-    const uint2 q = *reinterpret_cast<const uint2*>(part + h.code_off + first / 4);
-    c0 = (static_cast<uint64_t>(q.y) << 32) | q.x;
+    cw = *reinterpret_cast<const uint2*>(part + P.code_off + first / 4);
   }
+  const uint64_t c0 = (static_cast<uint64_t>(cw.y) << 32) | cw.x;
   uint64_t zm = ~(c0 | (c0 >> 1)) & 0x5555555555555555ull;   // bit 2j: weight j escapes
   if (cnt < 32) zm &= (1ull << (2 * cnt)) - 1ull;               // (cnt = 0: no escapes)
   const int nh0 = __popc(static_cast<uint32_t>(zm)), n1 = nh0 + __popc(static_cast<uint32_t>(zm >> 32));
   const int before1 = warp_exclusive_sum(n1, lane);
+  const uint32_t l2_rel = warp == 0 ? 0u : warp == 1 ? e1.x >> 16 : warp == 2 ? e1.y & 0xFFFFu : e1.y >> 16;
   // chunk tables: level 1 (byte c = exponent of 2-bit code c = base - (win + c - 1)) and
   // level 2 (byte c = exponent of 3-bit code c: r = w2 + c - 1, dl = r < win ? r : r + 3).
   // Bytes of codes a chunk cannot hold (dl > base) may borrow from higher bytes, which are
   // unused codes too; byte 0 (the escape code) is never read.
   const uint32_t base = e1.x & 0xFFu, win = (e1.x >> 8) & 0xFFu, w2 = win > 2u ? win - 2u : 0u, d = win - w2;
-  const uint32_t lut1 = (base - win) * 0x01010100u - 0x02010000u;
+  const uint32_t lut1 = ror8x4((base - win) * 0x01010100u - 0x02010000u);
   const uint32_t b4 = base * 0x01010101u;
-  const uint32_t lut2lo = b4 - (w2 * 0x01010100u + 0x02010000u + (d == 0 ? 0x03030300u : d == 1 ? 0x03030000u : 0x03000000u));
-  const uint32_t lut2hi = b4 - (w2 * 0x01010101u + 0x06050403u + 0x03030303u);
+  const uint32_t lut2lo = ror8x4(b4 - (w2 * 0x01010100u + 0x02010000u + (d == 0 ? 0x03030300u : d == 1 ? 0x03030000u : 0x03000000u)));
+  const uint32_t lut2hi = ror8x4(b4 - (w2 * 0x01010101u + 0x06050403u + 0x03030303u));
   // level-2 values of each half (16 weights: at most 16 escapes), as a byte stream in 4 words
-  const uint32_t* l2w = reinterpret_cast<const uint32_t*>(part + h.l2_off);
-  const uint64_t l2base = static_cast<uint64_t>(e0.y) + l2_rel + before1;
+  const uint32_t* l2w = reinterpret_cast<const uint32_t*>(part + P.l2_off);
+  const uint32_t l2base = e0.y + l2_rel + before1;
   uint32_t v[2][4];
-  uint32_t zq[2][4];   // zero level-2 codes: bit 4i of quartet q = code 4q + i of the half
+  uint64_t zt[2];   // zero level-2 codes of each half: bit 3k = code k
   int n2 = 0;
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf) {
     const int nh = hf ? n1 - nh0 : nh0;
     uint64_t x = 0;
     if (nh) {
-      const uint64_t bit = (l2base + (hf ? nh0 : 0)) * 3ull;
+      const uint32_t bit = (l2base + (hf ? nh0 : 0)) * 3u;
       const uint32_t* wp = l2w + (bit >> 5);
-      const uint32_t s = static_cast<uint32_t>(bit & 31);
+      const uint32_t s = bit & 31u;
       const uint32_t w0 = wp[0], w1 = wp[1], w2w = wp[2];
       x = (static_cast<uint64_t>(__funnelshift_r(w1, w2w, s)) << 32) | __funnelshift_r(w0, w1, s);
     }
+    zt[hf] = ~(x | (x >> 1) | (x >> 2)) & 0x0000249249249249ull & ((1ull << (3 * nh)) - 1ull);
+    n2 += __popcll(zt[hf]);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       v[hf][q] = 0;
-      zq[hf][q] = 0;
-      // quartets 2, 3 only when some lane of the warp needs them (rare past 8 escapes)
-      if (q < 2 || __any_sync(0xffffffffu, nh > 4 * q)) {
-        const uint32_t sel = nib3(static_cast<uint32_t>(x >> (12 * q)) & 0xFFFu);
-        v[hf][q] = __byte_perm(lut2lo, lut2hi, sel);
-        uint32_t z = ~(sel | (sel >> 1) | (sel >> 2)) & 0x1111u;
-        const int valid = nh - 4 * q;   // codes of this quartet that belong to the lane
-        z &= valid >= 4 ? 0x1111u : valid <= 0 ? 0u : (0x1111u >> (4 * (4 - valid)));
-        zq[hf][q] = z;
-        n2 += __popc(z);
-      }
+      // quartets 2, 3 only when some lane of the warp needs them (past 8 escapes)
+      if (q < 2 || __any_sync(0xffffffffu, nh > 4 * q))
+        v[hf][q] = __byte_perm(lut2lo, lut2hi, nib3(static_cast<uint32_t>(x >> (12 * q)) & 0xFFFu));
     }
   }
-  // rare: zero level-2 codes take the next escape bytes (weight order across the warp)
+  // zero level-2 codes (~3 per warp on bell-shaped weights) take the next escape bytes, in
+  // weight order across the warp
   if (__any_sync(0xffffffffu, n2)) {
-    const int before2 = warp_exclusive_sum(n2, lane);
-    const uint8_t* esc = part + h.esc_off + e0.x + esc_rel + before2;
+    const uint32_t esc_rel = warp == 0 ? 0u : warp == 1 ? e2.x & 0xFFFFu : warp == 2 ? e2.x >> 16 : e2.y & 0xFFFFu;
+    int before2;
+    if (__all_sync(0xffffffffu, n2 <= 1)) {
+      unsigned lt;
+      asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+      before2 = __popc(__ballot_sync(0xffffffffu, n2) & lt);
+    } else {
+      before2 = warp_exclusive_sum(n2, lane);
+    }
+    const uint8_t* esc = part + P.esc_off + e0.x + esc_rel + before2;
+    // patch in shared memory: the lane's 8 value words out ([word][lane], conflict-free),
+    // each escape byte stored at its stream position, the words back
+    uint32_t* vw = vsm + warp * 256 + lane;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) vw[32 * k] = v[k >> 2][k & 3];
+    uint8_t* vb = reinterpret_cast<uint8_t*>(vsm + warp * 256);
 #pragma unroll
     for (int hf = 0; hf < 2; ++hf)
+      for (uint64_t t = zt[hf]; t; t &= t - 1ull) {
+        const uint32_t k = ((__ffsll(static_cast<long long>(t)) - 1) * 43u) >> 7;   // bit 3k -> k
+        const uint32_t b = *esc++;
+        vb[((4 * hf + (k >> 2)) * 32 + lane) * 4 + (k & 3u)] = static_cast<uint8_t>((b >> 1) | (b << 7));
+      }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        for (uint32_t z = zq[hf][q]; z; z &= z - 1u) {
-          const int i = (__ffs(z) - 1) >> 2;
-          const uint32_t sh = 8u * i;
-          v[hf][q] = (v[hf][q] & ~(0xFFu << sh)) | (static_cast<uint32_t>(*esc++) << sh);
-        }
+    for (int k = 0; k < 8; ++k) v[k >> 2][k & 3] = vw[32 * k];
   }
   __syncthreads();   // stab
   if (!active) return;
@@ -465,11 +481,12 @@ __global__ void __launch_bounds__(kThreads) decode23_kernel(const PartBatch pb,
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf) {
     uint32_t v0 = v[hf][0], v1 = v[hf][1], v2 = v[hf][2], v3 = v[hf][3];
+    const uint32_t cwh = hf ? cw.y : cw.x;
 #pragma unroll
     for (int gq = 0; gq < 4; ++gq) {
       const int g = 4 * hf + gq;
-      const uint32_t e = stab[static_cast<uint32_t>(c0 >> (8 * g)) & 0xFFu];
-      const uint32_t X = __byte_perm(v0, lut1, e);
+      const uint32_t e = stab[__byte_perm(cwh, 0u, 0x4440u | gq)];
+      const uint32_t R = __byte_perm(v0, lut1, e);   // rotated exponent bytes of the group
       if (gq < 3) {   // advance the value stream past this group's escapes
         const uint32_t sh = e >> 16;
         v0 = __funnelshift_rc(v0, v1, sh);
@@ -477,10 +494,321 @@ __global__ void __launch_bounds__(kThreads) decode23_kernel(const PartBatch pb,
         v2 = __funnelshift_rc(v2, v3, sh);
         v3 = __funnelshift_rc(v3, 0u, sh);
       }
-      bf16x4(lo[g], X, o[2 * g], o[2 * g + 1]);
+      // high bytes sign | e >> 1, low bytes e & 1 | mantissa, interleaved into bf16 words
+      const uint32_t H = (lo[g] & 0x80808080u) | (R & 0x7F7F7F7Fu);
+      const uint32_t L = (lo[g] & 0x7F7F7F7Fu) | (R & 0x80808080u);
+      o[2 * g] = __byte_perm(L, H, 0x5140);
+      o[2 * g + 1] = __byte_perm(L, H, 0x7362);
     }
   }
-  store_out(out, first, cnt, o);
+  store_out(P.out, first, cnt, o);
+  if (prof && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&prof[1], static_cast<long long>(t));
+  }
+}
+
+// ---- mode 23, persistent and bulk-copy fed ---------------------------------------------
+// The decode of a chunk needs its sign|mantissa bytes, level-1 codes, level-2 codes and escape
+// bytes; issued as dependent global loads (entry -> codes -> warp scan -> level-2 words ->
+// escape bytes) they leave the kernel latency-bound.  Here a producer warp per CTA streams
+// each chunk's four byte ranges into a ring of shared-memory stages with cp.async.bulk (the
+// TMA engine; completion on an mbarrier, the entry words alongside), several chunks ahead,
+// while four consumer warps decode the previous stages from shared memory and release them.
+// CTAs are persistent: CTA b takes chunks b, b + G, b + 2G, ... of the launch.
+#ifndef XC_STAGES
+#define XC_STAGES 3
+#endif
+#ifndef XC_LO_GLOBAL
+#define XC_LO_GLOBAL 0
+#endif
+#ifndef XC_MINB
+#define XC_MINB 8
+#endif
+constexpr int kStages23 = XC_STAGES;
+constexpr int kL2Win = 1600;   // level-2 window: 4096 codes * 3 bits + alignment and read slack
+constexpr int kEscWin = 64;    // escape-byte window (larger runs are read from global memory)
+// Per-chunk metadata the producer derives from the chunk entry (lane-uniform work done once):
+enum : int {
+  kMLut1 = 0, kMLut2lo, kMLut2hi,   // rotated exponent tables (levels 1 and 2)
+  kMRem,                            // weights of the chunk (4096 but for a part's last chunk)
+  kML2Bit,                          // [4]: each warp's first level-2 code, as a bit of the window
+  kMEsc = kML2Bit + 4,              // [4]: each warp's first escape byte (index in the part)
+  kMEscWin = kMEsc + 4,             // escape window's first index (0xFFFFFFFF: global memory)
+  kMPart,                           // part of the launch
+  kMeta = 16
+};
+struct __align__(16) Stage23 {
+#if !XC_LO_GLOBAL
+  uint8_t lo[kChunk];
+#endif
+  uint8_t codes[kChunk / 4];
+  uint8_t l2[kL2Win];
+  uint8_t esc[kEscWin];
+  uint32_t meta[kMeta];
+};
+constexpr int kThreads23 = kThreads + 32;   // four consumer warps + the producer warp
+
+__device__ __forceinline__ int part_of(const Batch23& pb, uint32_t k) {
+  return (k >= pb.start[1]) + (k >= pb.start[2]) + (k >= pb.start[3]);
+}
+
+// (a & m) | (b & ~m) as one 3-input logic op
+__device__ __forceinline__ uint32_t bitsel(uint32_t m, uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(d) : "r"(m), "r"(a), "r"(b));   // m ? a : b (0xF0 ? 0xCC : 0xAA)
+  return d;
+}
+
+__global__ void __launch_bounds__(kThreads23, XC_MINB) decode23p_kernel(const __grid_constant__ Batch23 pb,
+                                                               long long* __restrict__ prof) {
+  __shared__ Stage23 stages[kStages23];
+  __shared__ uint64_t full[kStages23], empty[kStages23];
+  __shared__ uint32_t stab[256];
+  __shared__ uint32_t vsm[kThreads * 8];   // escape-byte patching: [warp][word][lane]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 256; i += kThreads23) stab[i] = kExpand.v[i];
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kStages23; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], kThreads / 32);
+    }
+    mbar_fence_init();
+  }
+  if (prof && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&prof[0], 0x7fffffffffffffffll - static_cast<long long>(t));
+  }
+  __syncthreads();
+  const uint32_t G = gridDim.x;
+  if (warp == kThreads / 32) {
+    // ---------------- producer warp ----------------
+    const uint64_t pol = evict_first_policy();   // coded bytes are read once
+    uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};    // lane j: entry words + next chunk's offsets
+    int i = 0;
+    for (uint32_t k = blockIdx.x; k < pb.chunks; k += G, ++i) {
+      if ((i & 31) == 0) {   // the entries of the next 32 chunks, one per lane
+        const uint32_t kj = k + lane * G;
+        if (kj < pb.chunks) {
+          const int pj = part_of(pb, kj);
+          const Part23& P = pb.p[pj];
+          const uint32_t c = kj - pb.start[pj];
+          const uint2* ep = reinterpret_cast<const uint2*>(P.part + align16(sizeof(PartHeader))) + 3 * c;
+          const uint2 a = ep[0], b = ep[1], d = ep[2];
+          m[0] = a.x; m[1] = a.y; m[2] = b.x; m[3] = b.y; m[4] = d.x; m[5] = d.y;
+          if (c + 1 < P.nch) {
+            const uint2 f = ep[3];
+            m[6] = f.x;   // next chunk's first escape byte
+            m[7] = f.y;   // next chunk's first level-2 code
+          } else {
+            m[6] = m[7] = 0xFFFFFFFFu;   // last chunk: its runs end with their sections
+          }
+        }
+      }
+      uint32_t e[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) e[q] = __shfl_sync(0xffffffffu, m[q], i & 31);
+      if (lane == 0) {
+        const int s = i % kStages23;
+        // the producer mostly waits here (the consumers set the pace): back off instead of
+        // spinning, so the wait takes no issue slots from the consumer warps
+        if (i >= kStages23)
+          while (!mbar_try_wait(&empty[s], ((i / kStages23) - 1) & 1)) __nanosleep(64);
+        Stage23& st = stages[s];
+        const int pi = part_of(pb, k);
+        const Part23& P = pb.p[pi];
+        const uint32_t c = k - pb.start[pi];
+        const uint32_t rem = min(static_cast<uint32_t>(P.n) - c * kChunk, static_cast<uint32_t>(kChunk));
+        const uint32_t lo_b = (rem + 15u) & ~15u;
+        const uint32_t cd_b = ((rem + 3u) / 4u + 15u) & ~15u;
+        // level-2 window [wb, we): whole 16-byte units around the chunk's codes + 16 bytes of
+        // read slack, within the section (esc_off - l2_off bytes, a multiple of 16)
+        const uint32_t l2sec = static_cast<uint32_t>(P.esc_off - P.l2_off);
+        const uint32_t wb = ((3u * e[1]) >> 3) & ~15u;
+        uint32_t we = e[7] == 0xFFFFFFFFu ? l2sec : ((((3u * e[7]) + 7u) >> 3) + 15u & ~15u) + 16u;
+        if (we > l2sec) we = l2sec;
+        // escape window: the chunk's escape bytes if they fit kEscWin from a 16-byte boundary
+        const uint32_t escsec = static_cast<uint32_t>(P.total - P.esc_off);
+        const uint32_t eb = e[0] & ~15u;
+        const uint32_t eend = e[6] == 0xFFFFFFFFu ? escsec : e[6];
+        uint32_t esc_b = 0, escw = 0xFFFFFFFFu;
+        if (eend <= e[0]) {
+          escw = eb;   // no escapes: nothing to read
+        } else if (eend - eb <= kEscWin) {
+          esc_b = (eend - eb + 15u) & ~15u;
+          if (eb + esc_b > escsec) esc_b = escsec - eb;
+          escw = eb;
+        }
+        // tables (chunk-uniform): level 1 byte c = exponent of code c = base - (win + c - 1);
+        // level 2 byte c: r = w2 + c - 1, dl = r < win ? r : r + 3.  Bytes of codes a chunk
+        // cannot hold (dl > base) may borrow from higher bytes, unused codes too; byte 0 (the
+        // escape code) is never read.  Stored rotated (ror8x4).
+        const uint32_t base = e[2] & 0xFFu, win = (e[2] >> 8) & 0xFFu, w2 = win > 2u ? win - 2u : 0u, dd = win - w2;
+        const uint32_t b4 = base * 0x01010101u;
+        uint32_t* mt = st.meta;
+        mt[kMLut1] = ror8x4((base - win) * 0x01010100u - 0x02010000u);
+        mt[kMLut2lo] = ror8x4(b4 - (w2 * 0x01010100u + 0x02010000u + (dd == 0 ? 0x03030300u : dd == 1 ? 0x03030000u : 0x03000000u)));
+        mt[kMLut2hi] = ror8x4(b4 - (w2 * 0x01010101u + 0x06050403u + 0x03030303u));
+        mt[kMRem] = rem;
+        const uint32_t l2rel[4] = {0u, e[2] >> 16, e[3] & 0xFFFFu, e[3] >> 16};
+        const uint32_t escrel[4] = {0u, e[4] & 0xFFFFu, e[4] >> 16, e[5] & 0xFFFFu};
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          mt[kML2Bit + w] = 3u * (e[1] + l2rel[w]) - 8u * wb;
+          mt[kMEsc + w] = e[0] + escrel[w];
+        }
+        mt[kMEscWin] = escw;
+        mt[kMPart] = static_cast<uint32_t>(pi);
+        const uint32_t l2_b = we > wb ? we - wb : 0u;
+#if XC_LO_GLOBAL
+        mbar_expect_tx(&full[s], cd_b + l2_b + esc_b);
+        (void)lo_b;
+#else
+        mbar_expect_tx(&full[s], lo_b + cd_b + l2_b + esc_b);
+        bulk_g2s(st.lo, P.part + P.low_off + static_cast<uint64_t>(c) * kChunk, lo_b, &full[s], pol);
+#endif
+        bulk_g2s(st.codes, P.part + P.code_off + static_cast<uint64_t>(c) * (kChunk / 4), cd_b, &full[s], pol);
+        if (l2_b) bulk_g2s(st.l2, P.part + P.l2_off + wb, l2_b, &full[s], pol);
+        if (esc_b) bulk_g2s(st.esc, P.part + P.esc_off + eb, esc_b, &full[s], pol);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  // ---------------- consumer warps ----------------
+  int i = 0;
+  for (uint32_t k = blockIdx.x; k < pb.chunks; k += G, ++i) {
+    const int s = i % kStages23;
+#if XC_LO_GLOBAL
+    // sign|mantissa bytes straight from global memory, issued before the stage wait
+    uint4 lg0 = make_uint4(0, 0, 0, 0), lg1 = lg0;
+    {
+      const int pk = part_of(pb, k);
+      const Part23& P = pb.p[pk];
+      const uint32_t lf = (k - pb.start[pk]) * kChunk + threadIdx.x * 32u;
+      if (lf < static_cast<uint32_t>(P.n)) {
+        const uint4* lp = reinterpret_cast<const uint4*>(P.part + P.low_off + lf);
+        lg0 = __ldcs(lp);
+        lg1 = __ldcs(lp + 1);
+      }
+    }
+#endif
+    mbar_wait(&full[s], (i / kStages23) & 1);
+    const Stage23& st = stages[s];
+    const uint4 mq = *reinterpret_cast<const uint4*>(st.meta);   // luts, rem
+    const uint32_t lut1 = mq.x, lut2lo = mq.y, lut2hi = mq.z, rem = mq.w;
+    const uint32_t l2bit = st.meta[kML2Bit + warp];
+    const uint32_t lfirst = threadIdx.x * 32u;   // the lane's first weight in the chunk
+    const int cnt = lfirst < rem ? static_cast<int>(min(rem - lfirst, 32u)) : 0;
+    uint32_t lo[8];
+    {
+#if XC_LO_GLOBAL
+      const uint4 l0 = lg0, l1 = lg1;
+#else
+      const uint4* lp = reinterpret_cast<const uint4*>(st.lo + lfirst);
+      const uint4 l0 = lp[0], l1 = lp[1];   // (stale bytes past rem: never stored)
+#endif
+      lo[0] = l0.x; lo[1] = l0.y; lo[2] = l0.z; lo[3] = l0.w;
+      lo[4] = l1.x; lo[5] = l1.y; lo[6] = l1.z; lo[7] = l1.w;
+    }
+    const uint2 cw = *reinterpret_cast<const uint2*>(st.codes + threadIdx.x * 8);
+    const uint64_t c0 = (static_cast<uint64_t>(cw.y) << 32) | cw.x;
+    uint64_t zm = ~(c0 | (c0 >> 1)) & 0x5555555555555555ull;   // bit 2j: weight j escapes
+    if (cnt < 32) zm &= (1ull << (2 * cnt)) - 1ull;
+    const int nh0 = __popc(static_cast<uint32_t>(zm)), n1 = nh0 + __popc(static_cast<uint32_t>(zm >> 32));
+    const int before1 = warp_exclusive_sum(n1, lane);
+    const uint32_t* l2w = reinterpret_cast<const uint32_t*>(st.l2);
+    uint32_t v[2][4];
+    uint64_t zt[2];   // zero level-2 codes of each half: bit 3k = code k
+    int n2 = 0;
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int nh = hf ? n1 - nh0 : nh0;
+      uint64_t x = 0;
+      if (nh) {
+        const uint32_t bit = l2bit + 3u * static_cast<uint32_t>(before1 + (hf ? nh0 : 0));
+        const uint32_t* wp = l2w + (bit >> 5);
+        const uint32_t sft = bit & 31u;
+        const uint32_t w0 = wp[0], w1 = wp[1], w2w = wp[2];
+        x = (static_cast<uint64_t>(__funnelshift_r(w1, w2w, sft)) << 32) | __funnelshift_r(w0, w1, sft);
+      }
+      zt[hf] = ~(x | (x >> 1) | (x >> 2)) & 0x0000249249249249ull & ((1ull << (3 * nh)) - 1ull);
+      n2 += __popcll(zt[hf]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        v[hf][q] = 0;
+        if (q < 2 || __any_sync(0xffffffffu, nh > 4 * q))
+          v[hf][q] = __byte_perm(lut2lo, lut2hi, nib3(static_cast<uint32_t>(x >> (12 * q)) & 0xFFFu));
+      }
+    }
+    // zero level-2 codes (~3 per warp on bell-shaped weights) take the next escape bytes, in
+    // weight order across the warp; patched in shared memory ([word][lane], conflict-free)
+    if (__any_sync(0xffffffffu, n2)) {
+      int before2;
+      if (__all_sync(0xffffffffu, n2 <= 1)) {
+        unsigned lt;
+        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+        before2 = __popc(__ballot_sync(0xffffffffu, n2) & lt);
+      } else {
+        before2 = warp_exclusive_sum(n2, lane);
+      }
+      const uint32_t escw = st.meta[kMEscWin];
+      const uint32_t ei = st.meta[kMEsc + warp] + before2;   // the lane's first escape byte
+      const uint8_t* esc;
+      if (escw != 0xFFFFFFFFu) {
+        esc = st.esc + (ei - escw);
+      } else {
+        const Part23& P = pb.p[st.meta[kMPart]];
+        esc = P.part + P.esc_off + ei;
+      }
+      uint32_t* vw = vsm + warp * 256 + lane;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) vw[32 * q] = v[q >> 2][q & 3];
+      uint8_t* vb = reinterpret_cast<uint8_t*>(vsm + warp * 256);
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf)
+        for (uint64_t t = zt[hf]; t; t &= t - 1ull) {
+          const uint32_t kk = ((__ffsll(static_cast<long long>(t)) - 1) * 43u) >> 7;   // bit 3k -> k
+          const uint32_t b = *esc++;
+          vb[((4 * hf + (kk >> 2)) * 32 + lane) * 4 + (kk & 3u)] = static_cast<uint8_t>((b >> 1) | (b << 7));
+        }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q >> 2][q & 3] = vw[32 * q];
+    }
+    const int pi = static_cast<int>(st.meta[kMPart]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done with the stage
+    if (cnt > 0) {
+      uint32_t o[16];
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t v0 = v[hf][0], v1 = v[hf][1], v2 = v[hf][2], v3 = v[hf][3];
+        const uint32_t cwh = hf ? cw.y : cw.x;
+#pragma unroll
+        for (int gq = 0; gq < 4; ++gq) {
+          const int g = 4 * hf + gq;
+          const uint32_t e = stab[__byte_perm(cwh, 0u, 0x4440u | gq)];
+          const uint32_t R = __byte_perm(v0, lut1, e);   // rotated exponent bytes of the group
+          if (gq < 3) {   // advance the value stream past this group's escapes
+            const uint32_t sh = e >> 16;
+            v0 = __funnelshift_rc(v0, v1, sh);
+            v1 = __funnelshift_rc(v1, v2, sh);
+            v2 = __funnelshift_rc(v2, v3, sh);
+            v3 = __funnelshift_rc(v3, 0u, sh);
+          }
+          // high bytes sign | e >> 1, low bytes e & 1 | mantissa, interleaved into bf16 words
+          const uint32_t H = bitsel(0x80808080u, lo[g], R);
+          const uint32_t L = bitsel(0x80808080u, R, lo[g]);
+          o[2 * g] = __byte_perm(L, H, 0x5140);
+          o[2 * g + 1] = __byte_perm(L, H, 0x7362);
+        }
+      }
+      const Part23& P = pb.p[pi];
+      store_out(P.out, static_cast<uint64_t>(k - pb.start[pi]) * kChunk + lfirst, cnt, o);
+    }
+  }
   if (prof && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -509,12 +837,45 @@ moe_status decode_batch(const void* const* parts_dev, const PartHeader* hs, uint
   }
   if (m == 0) return MOE_OK;
   pb.n = m;
+  if (kb == kMode23) {
+    // mode 23 takes each part's section offsets as parameters (from the host header copy)
+    Batch23 b{};
+    for (int q = 0; q < kMaxBatch; ++q) b.start[q] = 0xFFFFFFFFu;
+    for (int i = 0, j = 0; i < n; ++i) {
+      if (hs[i].n == 0) continue;
+      MOE_REQUIRE(hs[i].n < (1ull << 30), "a mode-23 part holds < 2^30 weights, got %llu",
+                  (unsigned long long)hs[i].n);
+      b.p[j] = Part23{pb.part[j], pb.out[j], hs[i].n, hs[i].low_off, hs[i].code_off, hs[i].l2_off,
+                      hs[i].esc_off, hs[i].total, hs[i].nch};
+      b.start[j] = pb.start[j];
+      ++j;
+    }
+    b.chunks = grid;
+    static const bool simple = getenv("MOE_XC_SIMPLE") != nullptr;   // A/B: one CTA per chunk
+    if (simple) {
+      decode23_kernel<<<grid, kThreads, 0, s>>>(b, prof);
+    } else {
+      // persistent: every CTA slot of the device, capped by the chunk count
+      static std::atomic<uint64_t> occ_done{0};
+      static int occ[64] = {};
+      int dev = 0;
+      MOE_CUDA(cudaGetDevice(&dev));
+      once_per_device(occ_done, [&] {
+        int per_sm = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode23p_kernel, kThreads23, 0);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        occ[dev & 63] = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+      });
+      const uint32_t g = std::min<uint32_t>(grid, static_cast<uint32_t>(occ[dev & 63]));
+      decode23p_kernel<<<g, kThreads23, 0, s>>>(b, prof);
+    }
+    MOE_LAUNCHED();
+    return MOE_OK;
+  }
   if (kb == 3)
     decode_kernel<3><<<grid, kThreads, 0, s>>>(pb, prof);
-  else if (kb == 4)
-    decode_kernel<4><<<grid, kThreads, 0, s>>>(pb, prof);
   else
-    decode23_kernel<<<grid, kThreads, 0, s>>>(pb, prof);
+    decode_kernel<4><<<grid, kThreads, 0, s>>>(pb, prof);
   MOE_LAUNCHED();
   return MOE_OK;
 }

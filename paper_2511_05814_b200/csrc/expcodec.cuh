@@ -69,6 +69,17 @@ struct PartBatch {
   uint32_t start[kMaxBatch];  // first CTA of each part
   int n;
 };
+struct Part23 {   // mode-23 part descriptor (the header's fields the decoder needs)
+  const uint8_t* part;
+  uint16_t* out;
+  uint64_t n, low_off, code_off, l2_off, esc_off, total;
+  uint32_t nch;
+};
+struct Batch23 {
+  Part23 p[kMaxBatch];
+  uint32_t start[kMaxBatch];  // first chunk of each part in the launch (unused: 0xFFFFFFFF)
+  uint32_t chunks;            // chunks of all parts
+};
 moe_status decode_batch(const void* const* parts_dev, const PartHeader* hs, uint16_t* const* outs_dev,
                         int n, cudaStream_t s, long long* prof = nullptr);
 
