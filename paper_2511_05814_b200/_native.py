@@ -150,7 +150,7 @@ def load_library() -> ctypes.CDLL:
             " (tools/build_native.sh). There is no CPU fallback."
         )
     # MOEB200_LIB: a variant build of the same library (tuning probes only)
-    lib = ctypes.CDLL(os.environ.get("MOEB200_LIB", str(LIB_PATH)))
+    lib = ctypes.CDLL(os.environ.get("MOEB200_LIB") or str(LIB_PATH))
     for name, (args, res) in _SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = args

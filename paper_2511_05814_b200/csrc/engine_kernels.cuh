@@ -522,6 +522,9 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
   }
   MailRecord& mr = sM;
   const unsigned long long t3 = p.phase_ns ? gtimer() : 0;
+  // every lane has read S.resident / S.step above; lane 0 rewrites them below (racecheck:
+  // warp-level WAR without this barrier)
+  __syncwarp();
   if (lane == 0) {
     // -- record --
     for (int j = 0; j < p.K; ++j) {

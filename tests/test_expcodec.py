@@ -97,6 +97,12 @@ def _cases():
     hi |= (rng.integers(0, 2, 4096 * 3).astype(np.uint16) << 15)
     hi[::5] = (hi[::5] & 0x807F) | (rng.integers(0, 250, hi[::5].size).astype(np.uint16) << 7)  # escapes
     yield "top_exponents", hi
+    # escapes clustered in one lane (10 in lane 5 of chunk 1, 6 in lane 31 of chunk 2) with few
+    # elsewhere: the chunk's escape window is used and a lane holds more than four escape bytes
+    c = synthetic_expert_rows(4096 * 3).copy()
+    c[4096 + 5 * 32 + np.arange(10) * 3] = 0x0100 | 0x8005                 # exponent 2
+    c[2 * 4096 + 31 * 32 + np.arange(6) * 5] = 0x0180 | 0x0011              # exponent 3
+    yield "clustered_escapes", c
 
 
 @pytest.mark.gpu
