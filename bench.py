@@ -785,10 +785,10 @@ def run_ours(args, world, rank, local):
                                if ktimes.get("ffn_kernel_ms") else None),
             "in_kernel_note": "globaltimer span first CTA start -> last CTA end per launch. The "
                               "CUDA-event span of a single launch is inflated while the copy "
-                              "engine runs: tools/dma_event_probe.py times a 235 MB D2D copy "
-                              "kernel at 80 us with or without H2D traffic under one event pair "
-                              "over 20 launches, but at 105 us with an event pair per launch "
-                              "under H2D traffic (80 us without). The events are recorded on an "
+                              "engine runs: tools/event_chunk_probe.py times a 235 MB elementwise "
+                              "SM kernel at 78 us alone and at ~103 us with an event pair per "
+                              "launch while >= 16 MB host->device copies are in flight "
+                              "(profiles/box_probe_r2.md). The events are recorded on an "
                               "identical replay of the timed tokens, not in the headline run "
                               "(they slow it by 1-3 %: tools/profile_overhead_probe.py)",
             "traffic": traffic.get("dram_bytes_per_expert") if traffic else None,

@@ -566,7 +566,6 @@ __global__ void __launch_bounds__(kThreads23, XC_MINB) decode23p_kernel(const __
   __shared__ Stage23 stages[kStages23];
   __shared__ uint64_t full[kStages23], empty[kStages23];
   __shared__ uint32_t stab[256];
-  __shared__ uint32_t vsm[kThreads * 8];   // escape-byte patching: [warp][word][lane]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 256; i += kThreads23) stab[i] = kExpand.v[i];
   if (threadIdx.x == 0) {
@@ -744,7 +743,7 @@ __global__ void __launch_bounds__(kThreads23, XC_MINB) decode23p_kernel(const __
       }
     }
     // zero level-2 codes (~3 per warp on bell-shaped weights) take the next escape bytes, in
-    // weight order across the warp; patched in shared memory ([word][lane], conflict-free)
+    // weight order across the warp
     if (__any_sync(0xffffffffu, n2)) {
       int before2;
       if (__all_sync(0xffffffffu, n2 <= 1)) {
@@ -763,19 +762,18 @@ __global__ void __launch_bounds__(kThreads23, XC_MINB) decode23p_kernel(const __
         const Part23& P = pb.p[st.meta[kMPart]];
         esc = P.part + P.esc_off + ei;
       }
-      uint32_t* vw = vsm + warp * 256 + lane;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) vw[32 * q] = v[q >> 2][q & 3];
-      uint8_t* vb = reinterpret_cast<uint8_t*>(vsm + warp * 256);
+      // patched in registers: each escape byte is merged into the one value word (of the
+      // half's four) that holds its stream position, by a masked select per word
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf)
         for (uint64_t t = zt[hf]; t; t &= t - 1ull) {
           const uint32_t kk = ((__ffsll(static_cast<long long>(t)) - 1) * 43u) >> 7;   // bit 3k -> k
           const uint32_t b = *esc++;
-          vb[((4 * hf + (kk >> 2)) * 32 + lane) * 4 + (kk & 3u)] = static_cast<uint8_t>((b >> 1) | (b << 7));
-        }
+          const uint32_t sh = 8u * (kk & 3u), wq = kk >> 2;
+          const uint32_t m = 0xFFu << sh, val = (((b >> 1) | (b << 7)) & 0xFFu) << sh;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q >> 2][q & 3] = vw[32 * q];
+          for (int q = 0; q < 4; ++q) v[hf][q] = bitsel(wq == static_cast<uint32_t>(q) ? m : 0u, val, v[hf][q]);
+        }
     }
     const int pi = static_cast<int>(st.meta[kMPart]);
     __syncwarp();
