@@ -127,6 +127,10 @@ __device__ __forceinline__ uint32_t ordered_bits(float f) {
   uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+// inverse of ordered_bits(float) (-0 comes back as +0)
+__device__ __forceinline__ float key_float(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
 __device__ __forceinline__ uint64_t ordered_bits(double f) {
   if (f == 0.0) f = 0.0;
   uint64_t u = static_cast<uint64_t>(__double_as_longlong(f));

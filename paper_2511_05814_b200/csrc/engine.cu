@@ -1088,10 +1088,14 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
                 "bf16 engine needs hidden_dim and ffn_dim multiples of 256");
   }
   const int grid_mix = stream_grid(1), grid_ffn = stream_grid(K);
+  static_assert(148 <= kMaxParts, "the gate sums one partial per mixing CTA");
   // SM transfer runs a token as one kernel chain (no copy-event waits): launch it programmatically
   const bool pdl = g->sm_transfer && !g->no_pdl;
   // bf16 engines take the gate / cache step in the mixing GEMV's last CTA (one launch)
   const bool fused_gate = g->bf16 && !g->no_fused_gate;
+  // copy-engine decode: the stream GEMVs launch programmatically (each overlaps its launch and
+  // prologue with its predecessor's tail; MIX also streams its weights meanwhile)
+  const bool pdl_stream = !g->sm_transfer && !g->no_pdl && fused_gate;
   // one expert-FFN launch group: phase 0 = hits, 1 = misses; only = -1 all, i = i-th miss
   if (g->profiling && !g->prof_bytes_dev)
     MOE_CUDA(cudaMalloc(&g->prof_bytes_dev, 4 * sizeof(long long) * moe_engine::kProfSlots));
@@ -1170,7 +1174,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       sp.yout = fp.y;
       sp.prof_bytes = prof_slot();
       const int grid = only >= 0 ? stream_grid(1) : grid_ffn;
-      MOE_CUDA(launch_stream<kModeUp>(gup, grid, sp, s));
+      MOE_CUDA(launch_stream<kModeUp>(gup, grid, sp, s, pdl_stream));
       MOE_LAUNCHED();
       return MOE_OK;
     }
@@ -1194,7 +1198,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
       sp.yout = fp.y;
       sp.prof_bytes = prof_slot();
       const int grid = only >= 0 ? stream_grid(1) : grid_ffn;
-      MOE_CUDA(launch_stream<kModeDown>(gdown, grid, sp, s));
+      MOE_CUDA(launch_stream<kModeDown>(gdown, grid, sp, s, pdl_stream));
       MOE_LAUNCHED();
       return MOE_OK;
     }
@@ -1241,6 +1245,9 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
         sp.y = mp.y;
         sp.prev = mp.prev;
         sp.M = static_cast<const uint16_t*>(mp.M);
+        if (!g->no_l2_prefetch)   // layer l+1 (after the last layer: the next token's layer 0)
+          sp.M_next = reinterpret_cast<const uint16_t*>(static_cast<char*>(g->mixing) +
+                                                        static_cast<size_t>((l + 1) % L) * D * D * msz);
         sp.alpha = mp.alpha;
         sp.h_in = mp.h_in;
         sp.h_mid = mp.h_mid;
@@ -1254,7 +1261,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
         sp.fuse_gate = fused_gate ? 1 : 0;
         sp.done_ctr = g->mix_ctr;
         sp.gate = gp;
-        MOE_CUDA(launch_stream<kModeMix>(gmix, grid_mix, sp, s));
+        MOE_CUDA(launch_stream<kModeMix>(gmix, grid_mix, sp, s, pdl_stream));
       } else {
         MOE_CUDA(launch_k(pdl, mix_kernel<false>, dim3(mix_grid), dim3(256), mix_smem, s, mp));
       }

@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(256) mix_kernel(MixParams p) {
 }
 
 // ---- K1 + K2: gate, softmax, top-k, speculation, cache policy, buffer table, mailbox ----
+constexpr int kMaxParts = 152;   // mixing-GEMV CTAs whose gate partials the gate sums (>= 148)
 struct GateParams {
   const float* h_mid;      // h' of this layer
   const float* h_in;       // layer input (reference guess point for this layer)
@@ -304,6 +305,76 @@ __device__ __forceinline__ void sort_small(int* v, int n) {
   }
 }
 
+// Register forms of warp_topk / topk_gap / load_forced: `out` / `sel` are indexed by unrolled
+// constants only, so the K-long id lists stay in registers.
+__device__ __forceinline__ void warp_topk_k(float z, bool valid, int K, int (&out)[kMaxK]) {
+  const int lane = threadIdx.x & 31;
+  bool taken = false;
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) {
+    if (j >= K) break;
+    uint64_t key = 0;
+    if (valid && !taken) key = (static_cast<uint64_t>(ordered_bits(z)) << 32) | (0xffffffffu - lane);
+    key = warp_max_u64(key);   // key 0: no candidate left (-1)
+    const int e = static_cast<int>(0xffffffffu - static_cast<uint32_t>(key & 0xffffffffu));
+    out[j] = e;
+    if (lane == e) taken = true;
+  }
+}
+__device__ __forceinline__ float topk_gap_k(float z, bool valid, const int (&sel)[kMaxK], int K) {
+  const int lane = threadIdx.x & 31;
+  bool taken = false;
+  int last = 0;
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j)
+    if (j < K) {
+      taken = taken || sel[j] == lane;
+      last = sel[j] & 31;
+    }
+  const float zk = __shfl_sync(FULL, z, last);
+  const float next = key_float(__reduce_max_sync(FULL, valid && !taken ? ordered_bits(z)
+                                                                         : ordered_bits(-INFINITY)));
+  return zk - next;
+}
+__device__ __forceinline__ bool load_forced_k(const int32_t* forced, int K, int E, int (&sel)[kMaxK]) {
+  uint32_t seen = 0;
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j)
+    if (j < K) {
+      const int e = forced[j];
+      const bool in = e >= 0 && e < E && e < 32;
+      ok = ok && in && !((seen >> (in ? e : 0)) & 1u);
+      if (in) seen |= 1u << e;
+      sel[j] = in ? e : 0;
+    }
+  return ok;
+}
+// ascending sort of the first n (<= kMaxK) entries, fully unrolled (registers, no stack)
+__device__ __forceinline__ void sort_k(int (&v)[kMaxK], int n) {
+#pragma unroll
+  for (int i = 0; i < kMaxK - 1; ++i)
+#pragma unroll
+    for (int j = 0; j < kMaxK - 1 - i; ++j)
+      if (j + 1 < n && v[j] > v[j + 1]) {
+        const int x = v[j];
+        v[j] = v[j + 1];
+        v[j + 1] = x;
+      }
+}
+
+// The same from global to shared memory without a register round trip (cp.async, 16 bytes
+// per copy); the caller cp_async_wait_all()s before the barrier that publishes it.
+__device__ __forceinline__ void copy16_async(void* dst, const void* src, int n, int tid, int nthreads) {
+  const char* s = static_cast<const char*>(src);
+  for (int i = tid; i < n / 16; i += nthreads)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(static_cast<char*>(dst) + 16 * i))),
+                 "l"(s + 16 * i)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Copy `n` bytes (multiple of 16) with the calling threads (tid in [0, nthreads)).
 __device__ __forceinline__ void copy16(void* dst, const void* src, int n, int tid, int nthreads) {
   int4* d = static_cast<int4*>(dst);
@@ -336,7 +407,6 @@ struct GateSmem {
   __align__(16) LayerState sS;    // working copies of this / next layer's state
   __align__(16) LayerState sS1;
   __align__(16) MailRecord sM;
-  long long s_consumed;
 };
 
 // The gate + cache step run by `nthreads` threads (tid in [0, nthreads), a multiple of 32):
@@ -350,15 +420,17 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
   LayerState& sS = gsm.sS;
   LayerState& sS1 = gsm.sS1;
   MailRecord& sM = gsm.sM;
-  long long& s_consumed = gsm.s_consumed;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nthreads >> 5;
   const bool do_guess = p.record_spec && p.layer >= 1;
   const bool do_prefetch = p.prefetch == MOE_PREFETCH_EARLY && p.layer + 1 < p.L;
   const unsigned long long t0 = p.phase_ns ? gtimer() : 0;
-  // stage the cache state in shared memory (its latency overlaps the logits below)
-  copy16(&sS, &p.states[p.layer], sizeof(LayerState), tid, nthreads);
-  if (do_prefetch) copy16(&sS1, &p.states[p.layer + 1], sizeof(LayerState), tid, nthreads);
-  if (tid == 0) s_consumed = p.mail ? p.ctl->consumed : 0;
+  // stage the cache state in shared memory asynchronously (cp.async: its latency overlaps the
+  // partial sums / logits below; waited for before the barrier that ends them)
+  copy16_async(&sS, &p.states[p.layer], sizeof(LayerState), tid, nthreads);
+  if (do_prefetch) copy16_async(&sS1, &p.states[p.layer + 1], sizeof(LayerState), tid, nthreads);
+  // the host's acknowledgement counter lives in mapped host memory: a PCIe round trip, so
+  // thread 0 (lane 0 of warp 0, which writes the mail) issues the load now and uses it last
+  const long long consumed0 = (tid == 0 && p.mail) ? p.ctl->consumed : 0;
   // launched programmatically after the mixing kernel: its outputs are read from here on
   if (wait_pdl) pdl_wait();
   // RMSNorm scales of h' (route, early guess, experts) and of h_in (reference guess)
@@ -367,11 +439,26 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
   if (p.part) {
     // fused: sum the per-CTA partials, one warp per job, lanes over CTAs, then a fixed
     // shuffle tree (the same order every call: deterministic)
-    for (int q = warp; q < njob; q += nwarps) {
+    // Eight threads per job, each summing every 8th CTA's partial in CTA order with its loads
+    // all in flight (one L2 round trip instead of one per job), then a fixed xor tree over
+    // the eight: the same order every call (deterministic).
+    for (int q0 = 0; q0 < njob; q0 += nthreads / 8) {
+      const int q = q0 + tid / 8, sub = tid & 7;
       float acc = 0.f;
-      for (int c = lane; c < p.nparts; c += 32) acc += p.part[c * njob + q];
-      acc = warp_sum(acc);
-      if (lane == 0) {
+      if (q < njob) {
+        float v[kMaxParts / 8];
+#pragma unroll
+        for (int i = 0; i < kMaxParts / 8; ++i) {
+          const int c = sub + 8 * i;
+          v[i] = c < p.nparts ? p.part[c * njob + q] : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < kMaxParts / 8; ++i) acc += v[i];
+      }
+      acc += __shfl_xor_sync(FULL, acc, 4);
+      acc += __shfl_xor_sync(FULL, acc, 2);
+      acc += __shfl_xor_sync(FULL, acc, 1);
+      if (q < njob && sub == 0) {
         if (q < 3 * p.E) z[q / p.E][q % p.E] = acc;
         else red[q - 3 * p.E][0] = acc;
       }
@@ -441,6 +528,7 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
     if (lane == 0) z[which][e] = acc * (which == 1 ? inv_in : inv_mid) + p.gate_b[gl * p.E + e];
   }
   }
+  cp_async_wait_all();
   sync();
   if (warp != 0) return;
   const unsigned long long t2 = p.phase_ns ? gtimer() : 0;
@@ -448,77 +536,112 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
   const bool valid = lane < p.E;
   LayerState& S = sS;
   StepRecord* rec = p.rec;
+  const long long t = S.step;
+  const uint32_t emask = p.E >= 32 ? 0xffffffffu : ((1u << p.E) - 1u);
+  int sel[kMaxK], acts[kMaxK], gs[kMaxK], pf[kMaxK];
+  float psel[kMaxK];
+  uint32_t flags = 0u, rb = 0u, ev = 0u, res_after = S.resident & emask;
+  float gap = NAN, ggap = NAN, zs_r = 0.f, zs_g = 0.f;
+  bool go = false, ok = true;
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) sel[j] = acts[j] = gs[j] = pf[j] = -1, psel[j] = 0.f;
+  // One expert per lane, everything in registers (the K-long id lists are indexed by unrolled
+  // constants only), extremes by redux.sync on order-preserving keys: the decision is a short
+  // chain of warp reductions -- this tail runs on one SM while the others wait for it.
   // -- route: finiteness (toymoe.py:109-110), softmax over all E (toymoe.py:93-96) --
   const float zr = valid ? z[0][lane] : 0.f;
+  const float zg = valid && do_guess ? z[1][lane] : 0.f;
+  const float ze = valid && do_prefetch ? z[2][lane] : 0.f;
   bool finite = __all_sync(FULL, !valid || isfinite(zr));
-  float zg = 0.f;
-  if (do_guess) {
-    zg = valid ? z[1][lane] : 0.f;
-    finite = finite && __all_sync(FULL, !valid || isfinite(zg));
-  }
-  int sel[kMaxK], acts[kMaxK], gs[kMaxK];
-  uint32_t flags = finite ? 0u : 1u;
-  const float m = warp_max(valid ? zr : -INFINITY);
+  if (do_guess) finite = finite && __all_sync(FULL, !valid || isfinite(zg));
+  flags = finite ? 0u : 1u;
+  // max over the valid lanes (-inf elsewhere): the ordered-key maximum is fmaxf's result for
+  // finite values (non-finite rows are flagged and their numbers unused)
+  const float m = key_float(__reduce_max_sync(FULL, valid ? ordered_bits(zr) : ordered_bits(-INFINITY)));
   const float ez = valid ? expf(zr - m) : 0.f;
-  const float sum = warp_sum(ez);
+  const float sum = warp_sum(ez);   // butterfly order, as before
   const float prob = ez / sum;
   bool routed_ok = true;
   if (p.forced) {
-    routed_ok = load_forced(p.forced, p.K, p.E, sel);
+    routed_ok = load_forced_k(p.forced, p.K, p.E, sel);
     if (!routed_ok) flags |= 4u;
   } else {
-    warp_topk(zr, valid && finite, p.K, sel);
+    warp_topk_k(zr, valid && finite, p.K, sel);
+    gap = topk_gap_k(zr, valid, sel, p.K);
   }
-  const float gap = p.forced ? NAN : topk_gap(zr, valid, sel, p.K);
-  const float zs_r = warp_max(valid ? fabsf(zr) : 0.f);
-  const float zs_g = do_guess ? warp_max(valid ? fabsf(zg) : 0.f) : 0.f;
-  const bool go = finite && routed_ok;
-  float psel[kMaxK];
+  zs_r = __uint_as_float(__reduce_max_sync(FULL, valid ? __float_as_uint(fabsf(zr)) : 0u));
+  zs_g = do_guess ? __uint_as_float(__reduce_max_sync(FULL, valid ? __float_as_uint(fabsf(zg)) : 0u)) : 0.f;
+  go = finite && routed_ok;
   float ssel = 0.f;
-  for (int j = 0; j < p.K; ++j) {
-    psel[j] = __shfl_sync(FULL, prob, sel[j] & 31);
-    ssel += psel[j];
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j)
+    if (j < p.K) {
+      psel[j] = __shfl_sync(FULL, prob, sel[j] & 31);
+      ssel += psel[j];
+    }
+  if (p.renorm) {
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j)
+      if (j < p.K) psel[j] = psel[j] / ssel;
   }
-  if (p.renorm)
-    for (int j = 0; j < p.K; ++j) psel[j] = psel[j] / ssel;
-  for (int j = 0; j < p.K; ++j) acts[j] = sel[j];
-  sort_small(acts, p.K);
-
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) acts[j] = sel[j];
+  sort_k(acts, p.K);
   // -- cache policy step (kernels.py:89-145), state held one expert per lane --
-  WarpCacheState<1> st;
-  st.resident = valid ? ((S.resident >> lane) & 1u) : 0u;
-  st.freq[0] = valid ? S.freq[lane] : 0.0;
-  st.last_touch[0] = valid ? S.last_touch[lane] : -1;
-  const long long t = S.step;
-  uint32_t rbb = 0, evb = 0;
-  bool ok = true;
   if (go) {
-    ok = warp_policy_step<1>(st, p.E, p.C, p.policy, p.decay_factor, p.decay_period, t,
-                             [&](int j) { return static_cast<long long>(acts[j]); }, p.K,
-                             [&](int) { return 0ll; }, rbb, evb);
+    uint32_t in_act = 0;   // the K activated ids are distinct (top-k, or checked forced ids)
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j)
+      if (j < p.K) in_act |= 1u << acts[j];
+    const uint32_t res0 = S.resident & emask;
+    double fq = valid ? S.freq[lane] : 0.0;
+    long long lt = valid ? S.last_touch[lane] : -1;
+    if (p.policy == MOE_P_LFU_AGED && t > 0 && (t % p.decay_period) == 0) fq *= p.decay_factor;
+    uint32_t res = res0;
+    rb = res0;
+    const bool lfu = p.policy == MOE_P_LFU || p.policy == MOE_P_LFU_AGED;
+    const int need = __popc(res0) + __popc(in_act & ~res0) - p.C;
+    for (int r = 0; r < need; ++r) {
+      // argmin over resident & not activated: LRU (last_touch, id), LFU (freq, last_touch, id)
+      const bool cand = ((res >> lane) & 1u) && !((in_act >> lane) & 1u);
+      uint64_t best = ~0ull;
+      if (lfu) {
+        const uint64_t fb = cand ? static_cast<uint64_t>(__double_as_longlong(fq)) : ~0ull;
+        const uint64_t fmin = warp_min_u64(fb);
+        if (cand && fb == fmin) best = lru_key(lt, lane);
+      } else if (cand) {
+        best = lru_key(lt, lane);
+      }
+      best = warp_min_u64(best);
+      if (best == ~0ull) {   // K > C: the reference's latent out-of-range eviction
+        ok = false;
+        break;
+      }
+      const int victim = static_cast<int>(best & 1023u);
+      res &= ~(1u << victim);
+      ev |= 1u << victim;
+    }
+    if ((in_act >> lane) & 1u) {
+      fq += 1.0;
+      lt = t;
+    }
+    res_after = (res | in_act) & emask;
+    if (valid) {
+      S.freq[lane] = fq;
+      S.last_touch[lane] = lt;
+    }
   }
   if (!ok) flags |= 2u;
-  const uint32_t emask = p.E >= 32 ? 0xffffffffu : ((1u << p.E) - 1u);
-  const uint32_t rb = __ballot_sync(FULL, rbb & 1u) & emask;
-  const uint32_t ev = __ballot_sync(FULL, evb & 1u) & emask;
-  const uint32_t res_after = __ballot_sync(FULL, st.resident & 1u) & emask;
-  if (valid && go) {
-    S.freq[lane] = st.freq[0];
-    S.last_touch[lane] = st.last_touch[0];
-  }
   // speculation guesses
-  float ggap = NAN;
   if (do_guess) {
-    warp_topk(zg, valid && finite, p.K, gs);
-    ggap = topk_gap(zg, valid, gs, p.K);
-    sort_small(gs, p.K);
+    warp_topk_k(zg, valid && finite, p.K, gs);
+    ggap = topk_gap_k(zg, valid, gs, p.K);
+    sort_k(gs, p.K);
   }
-  int pf[kMaxK];
   if (do_prefetch) {
-    const float ze = valid ? z[2][lane] : 0.f;
     const bool fe = __all_sync(FULL, !valid || isfinite(ze));
-    warp_topk(ze, valid && fe, p.K, pf);
-    sort_small(pf, p.K);
+    warp_topk_k(ze, valid && fe, p.K, pf);
+    sort_k(pf, p.K);
   }
   MailRecord& mr = sM;
   const unsigned long long t3 = p.phase_ns ? gtimer() : 0;
@@ -527,7 +650,9 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
   __syncwarp();
   if (lane == 0) {
     // -- record --
-    for (int j = 0; j < p.K; ++j) {
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+      if (j >= p.K) break;
       rec->sel[j] = sel[j];
       rec->prob[j] = psel[j];
       rec->acts[j] = acts[j];
@@ -547,7 +672,9 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
       S.resident = res_after;
       S.step = t + 1;
       int hits = 0;
-      for (int j = 0; j < p.K; ++j) hits += (rb >> acts[j]) & 1u;
+#pragma unroll
+      for (int j = 0; j < kMaxK; ++j)
+        if (j < p.K) hits += (rb >> acts[j]) & 1u;
       atomicAdd(&p.stats->hits, static_cast<unsigned long long>(hits));
       atomicAdd(&p.stats->misses, static_cast<unsigned long long>(p.K - hits));
       // release buffers of evicted experts (their bytes stay until overwritten)
@@ -558,7 +685,9 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
           S.buf_of[e] = -1;
         }
       // misses whose expert was prefetched for exactly this step adopt the staging buffer
-      for (int j = 0; j < p.K; ++j) {
+#pragma unroll
+      for (int j = 0; j < kMaxK; ++j) {
+        if (j >= p.K) break;
         const int e = acts[j];
         if ((rb >> e) & 1u) continue;
         for (int b = 0; b < p.NB; ++b)
@@ -580,7 +709,9 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
           mr.cancel_buf[nc++] = b;
         }
       // fresh demand misses take the lowest free buffer
-      for (int j = 0; j < p.K; ++j) {
+#pragma unroll
+      for (int j = 0; j < kMaxK; ++j) {
+        if (j >= p.K) break;
         const int e = acts[j];
         if (((rb >> e) & 1u) || S.buf_of[e] >= 0) continue;
         int pick = -1;
@@ -597,7 +728,9 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
       // speculative prefetch of layer l+1's guesses that are not resident there
       if (do_prefetch) {
         LayerState& S1 = sS1;
-        for (int j = 0; j < p.K; ++j) {
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j) {
+          if (j >= p.K) break;
           const int g = pf[j];
           if (g < 0 || g >= p.E || S1.buf_of[g] >= 0) continue;
           int pick = -1;
@@ -618,7 +751,7 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
     mr.n_demand = nd;
     mr.n_cancel = nc;
     mr.n_prefetch = np;
-    mr.need_ack = (p.seq - s_consumed) >= (kMailRing / 2) ? 1 : 0;
+    mr.need_ack = (p.seq - consumed0) >= (kMailRing / 2) ? 1 : 0;
   }
   __syncwarp();
   const unsigned long long t4 = p.phase_ns ? gtimer() : 0;

@@ -35,6 +35,9 @@ struct StreamParams {
   const float* y;          // previous layer's expert outputs [K][d] (MIX) / output (DOWN)
   const StepRecord* prev;
   const uint16_t* M;       // mixing [d][d]
+  const uint16_t* M_next;  // the next layer's mixing matrix: each CTA prefetches its band into
+                           // L2 once its own copies are issued (read by the next MIX launch,
+                           // same grid, same bands), or nullptr
   float alpha;
   float* h_in;
   float* h_mid;
@@ -93,7 +96,15 @@ __device__ __forceinline__ int stream_active(const StreamParams& p, int* slot, c
 // pairs/quads combine through shared memory in a fixed order).
 template <int MODE, int RPB>
 __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamParams p) {
-  if constexpr (MODE == kModeMix) pdl_trigger();  // the gate may launch meanwhile
+  // Programmatic launch (copy-engine decode): MIX lets the next kernel launch at once and only
+  // its consumers wait for the previous layer (its producer streams M meanwhile); UP / DOWN
+  // read the gate's record and their predecessor's outputs, so every thread waits first.
+  if constexpr (MODE == kModeMix) {
+    pdl_trigger();
+  } else {
+    pdl_wait();
+    pdl_trigger();
+  }
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NM = MODE == kModeUp ? 2 : 1;  // matrices streamed per row block
   constexpr int WPR = kStreamWarps / RPB;
@@ -179,12 +190,23 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
           }
         }
       }
+      if constexpr (MODE == kModeMix) {
+        // the next layer's band of M into L2 while this layer's experts stream (their weights
+        // are evict-first, so the prefetched band survives until the next mixing launch)
+        if (p.M_next) {
+          const char* b0 = reinterpret_cast<const char*>(p.M_next + static_cast<size_t>(rb0) * RPB * C);
+          const long long nb = static_cast<long long>(rb1 - rb0) * RPB * C * 2;
+          for (long long o = 0; o < nb; o += 32768)
+            bulk_prefetch_l2(b0 + o, static_cast<uint32_t>(nb - o < 32768 ? nb - o : 32768));
+        }
+      }
     }
     return;
   }
 
   // ---------------- consumers: stage the activation vector ----------------
   if constexpr (MODE == kModeMix) {
+    pdl_wait();   // the previous layer's outputs (a no-op unless launched programmatically)
 #pragma unroll 4
     for (int i4 = threadIdx.x; i4 < p.d / 4; i4 += kStreamWarps * 32) {
       const float4 v = p.x ? reinterpret_cast<const float4*>(p.x)[i4]
@@ -403,7 +425,7 @@ inline void set_stream_carveout(int carveout) {
 // Launch one stream GEMV with the template instantiation matching the geometry.
 template <int MODE>
 inline cudaError_t launch_stream(const StreamGeom& g, int grid, const StreamParams& sp,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, bool pdl = false) {
   static std::atomic<uint64_t> attrs{0};
   cudaError_t set = cudaSuccess;
   once_per_device(attrs, [&set] {
@@ -425,13 +447,19 @@ inline cudaError_t launch_stream(const StreamGeom& g, int grid, const StreamPara
   p.cb = g.cb;
   p.ncb = g.ncb;
   p.stages = g.stages;
-  if (g.rpb == 8)
-    stream_gemv_kernel<MODE, 8><<<grid, kStreamThreads, g.smem, s>>>(p);
-  else if (g.rpb == 4)
-    stream_gemv_kernel<MODE, 4><<<grid, kStreamThreads, g.smem, s>>>(p);
-  else
-    stream_gemv_kernel<MODE, 2><<<grid, kStreamThreads, g.smem, s>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(kStreamThreads);
+  lc.dynamicSmemBytes = g.smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  if (g.rpb == 8) return cudaLaunchKernelEx(&lc, stream_gemv_kernel<MODE, 8>, p);
+  if (g.rpb == 4) return cudaLaunchKernelEx(&lc, stream_gemv_kernel<MODE, 4>, p);
+  return cudaLaunchKernelEx(&lc, stream_gemv_kernel<MODE, 2>, p);
 }
 
 }  // namespace moe
