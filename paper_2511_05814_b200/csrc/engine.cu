@@ -1182,9 +1182,11 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
     MOE_LAUNCHED();
     return MOE_OK;
   };
-  auto launch_down = [&](FfnParams fp, int only) -> moe_status {
+  auto launch_down = [&](FfnParams fp, int only, int row_lo = 0, int row_hi = 0) -> moe_status {
     if (g->bf16) {
       StreamParams sp{};
+      sp.row_lo = row_lo;
+      sp.row_hi = row_hi;
       sp.d = D;
       sp.f = g->f;
       sp.K = K;
@@ -1379,6 +1381,10 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
             char* dst[xc::kMaxBatch];
             xc::PartHeader hh[xc::kMaxBatch];
             int nb = 0;
+            // the step's last miss reduces the rows of pieces 1..3 before the last piece
+            // lands, so only the short piece's decode + rows trail the step's last byte
+            const bool split = i == plan.n - 1 && !g->no_split_down;
+            const int head = g->coded_piece_row0(NP - 1);
             for (int q = 1; q < NP; ++q) {
               MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_part[i][q], 0));
               src[nb] = plan.land[i] + coff;
@@ -1390,11 +1396,22 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
                 TRY(xdecode_n(src, hh, dst, nb));
                 nb = 0;
               }
+              if (split && q == NP - 2) {
+                TRY(prof_begin(fev));
+                TRY(launch_down(fp, i, 0, head));
+                TRY(prof_end(fev));
+              }
             }
             MOE_CUDA(cudaEventRecord(plan.free_ev[i], s));
-          } else {
-            MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_b[i], 0));
+            TRY(prof_begin(fev));
+            if (split)
+              TRY(launch_down(fp, i, head, D));
+            else
+              TRY(launch_down(fp, i));
+            TRY(prof_end(fev));
+            continue;
           }
+          MOE_CUDA(cudaStreamWaitEvent(s, plan.ev_b[i], 0));
           TRY(prof_begin(fev));
           TRY(launch_down(fp, i));
           TRY(prof_end(fev));

@@ -187,6 +187,7 @@ struct moe_engine {
   bool no_graph = getenv("MOE_NO_GRAPH") != nullptr;
   bool no_pdl = getenv("MOE_NO_PDL") != nullptr;
   bool no_l2_prefetch = getenv("MOE_NO_L2_PREFETCH") != nullptr;   // A/B: mixing-matrix prefetch off
+  bool no_split_down = getenv("MOE_NO_SPLIT_DOWN") != nullptr;     // A/B: last miss's down in one launch
   bool no_fused_gate = getenv("MOE_NO_FUSED_GATE") != nullptr;  // A/B: separate gate launch
   cudaGraphExec_t graph_exec = nullptr;
   uint64_t graph_kernels = 0;

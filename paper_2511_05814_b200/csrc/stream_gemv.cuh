@@ -51,6 +51,8 @@ struct StreamParams {
   int only;                // -1: every expert of the phase; i: just the i-th (ascending id)
   float* act;              // [K][f]
   float* yout;             // [K][d]
+  int row_lo, row_hi;      // DOWN: only output rows [row_lo, row_hi) (multiples of the row
+                           // block), e.g. the w2 pieces already decoded; row_hi = 0: all rows
   long long* prof_bytes;   // optional profiling slot [4]: weight bytes this launch streams,
                            // max(LLONG_MAX - CTA start ns), max(consumer end ns) (globaltimer)
   // MIX: per-CTA partial gate logits over the CTA's rows (see GateParams::part)
@@ -112,6 +114,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = MODE == kModeDown ? p.f : p.d;  // row length
   const int R = MODE == kModeUp ? p.f : p.d;    // rows per matrix
+  const bool ranged = MODE == kModeDown && p.row_hi > p.row_lo;
+  const int RS = ranged ? p.row_hi - p.row_lo : R;   // rows this launch covers
+  const int rbase = ranged ? p.row_lo / RPB : 0;
   const int cb = p.cb, ncb = p.ncb, S = p.stages;
   const uint32_t slice = static_cast<uint32_t>(cb) * 2;   // bytes per row slice
   const uint32_t stage_bytes = slice * RPB * NM;
@@ -125,17 +130,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMax(&p.prof_bytes[1], 0x7fffffffffffffffll - static_cast<long long>(t));
-    if (blockIdx.x == 0) p.prof_bytes[0] = static_cast<long long>(n_active) * NM * R * C * 2;
+    if (blockIdx.x == 0) p.prof_bytes[0] = static_cast<long long>(n_active) * NM * RS * C * 2;
     if (n_active == 0) atomicMax(&p.prof_bytes[2], static_cast<long long>(t));
   }
   if (n_active == 0) return;
   const int a = static_cast<int>((static_cast<long long>(blockIdx.x) * n_active) / gridDim.x);
   const int c0 = static_cast<int>((static_cast<long long>(a) * gridDim.x + n_active - 1) / n_active);
   const int c1 = static_cast<int>((static_cast<long long>(a + 1) * gridDim.x + n_active - 1) / n_active);
-  const int nrb = R / RPB;
+  const int nrb = RS / RPB;
   const int my = blockIdx.x - c0, ncta = c1 - c0;
-  const int rb0 = static_cast<int>((static_cast<long long>(my) * nrb) / ncta);
-  const int rb1 = static_cast<int>((static_cast<long long>(my + 1) * nrb) / ncta);
+  const int rb0 = rbase + static_cast<int>((static_cast<long long>(my) * nrb) / ncta);
+  const int rb1 = rbase + static_cast<int>((static_cast<long long>(my + 1) * nrb) / ncta);
   const int n_work = (rb1 - rb0) * ncb;
 
   const uint16_t* W[NM];
