@@ -740,7 +740,7 @@ moe_status create_resources(moe_engine* g) {
     g->free_events.push_back({a, b});
   }
   if (getenv("MOE_GATE_TIMING"))
-    TRY(alloc_device(reinterpret_cast<void**>(&g->gate_phase_ns), 8 * sizeof(unsigned long long)));
+    TRY(alloc_device(reinterpret_cast<void**>(&g->gate_phase_ns), 16 * sizeof(unsigned long long)));
   // coded-only engines keep one raw layer as the encoder's staging buffer
   const size_t store_bytes = static_cast<size_t>(g->coded_only ? 1 : g->SL) * E * g->expert_bytes;
   if (g->ext_store) {
@@ -807,11 +807,16 @@ moe_status moe_engine_destroy(moe_engine* g) {
                   static_cast<void*>(g->out_cur), static_cast<void*>(g->x_stage), static_cast<void*>(g->out_stage)})
     if (p) cudaFree(p);
   if (g->gate_phase_ns) {
-    unsigned long long h[8] = {};
+    unsigned long long h[16] = {};
     cudaMemcpy(h, g->gate_phase_ns, sizeof(h), cudaMemcpyDeviceToHost);
+    if (h[5] && h[6])
+      fprintf(stderr, "[moe] fused mixing kernel (avg ns from its first CTA start): last CTA start "
+              "%llu, last staging done %llu, last main loop done %llu, last partials done %llu\n",
+              h[11] / h[5], h[12] / h[5], h[13] / h[5], h[14] / h[5]);
     if (h[5])
-      fprintf(stderr, "[moe] gate kernel phases (avg ns over %llu): state+rms %llu, logits %llu, "
-              "route+policy %llu, bookkeeping %llu, writeback+mail %llu\n", h[5], h[0] / h[5],
+      fprintf(stderr, "[moe] gate kernel phases (avg ns over %llu): mix stream+partials (fused: "
+              "first CTA start -> gate start) %llu, state+rms %llu, logits %llu, route+policy %llu, "
+              "bookkeeping %llu, writeback+mail %llu\n", h[5], h[6] / h[5], h[0] / h[5],
               h[1] / h[5], h[2] / h[5], h[3] / h[5], h[4] / h[5]);
     cudaFree(g->gate_phase_ns);
   }

@@ -778,6 +778,19 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
       atomicAdd(&p.phase_ns[3], t4 - t3);
       atomicAdd(&p.phase_ns[4], t5 - t4);
       atomicAdd(&p.phase_ns[5], 1ull);
+      // fused: first mixing CTA start -> gate start (the GEMV stream, partials, ticket)
+      const unsigned long long mix0 = p.phase_ns[7];
+      if (mix0) {
+        const unsigned long long st0 = ~0ull - mix0;
+        atomicAdd(&p.phase_ns[6], t0 - st0);
+        // milestones of the slowest CTA (slots 8-10: last start, staging, main loop; 15:
+        // partials), relative to the first CTA's start
+        atomicAdd(&p.phase_ns[11], p.phase_ns[8] - st0);
+        atomicAdd(&p.phase_ns[12], p.phase_ns[9] - st0);
+        atomicAdd(&p.phase_ns[13], p.phase_ns[10] - st0);
+        atomicAdd(&p.phase_ns[14], p.phase_ns[15] - st0);
+        p.phase_ns[7] = p.phase_ns[8] = p.phase_ns[9] = p.phase_ns[10] = p.phase_ns[15] = 0ull;
+      }
     }
   }
 }

@@ -19,6 +19,7 @@ constexpr int kStreamWarps = 8;                       // consumer warps = rows p
 constexpr int kStreamThreads = (kStreamWarps + 1) * 32; // + one producer warp
 constexpr int kStreamStageBytes = 32 * 1024;
 constexpr int kStreamSmemBudget = 200 * 1024;
+constexpr int kMixBandRows = 64;   // MIX: gate partials from registers / smem up to this band
 
 __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kStreamWarps * 32) : "memory");
@@ -103,6 +104,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
   // read the gate's record and their predecessor's outputs, so every thread waits first.
   if constexpr (MODE == kModeMix) {
     pdl_trigger();
+    if (p.gate.phase_ns && threadIdx.x == 0) {   // diagnostics: this launch's first CTA start
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(&p.gate.phase_ns[7], ~0ull - t);
+      atomicMax(&p.gate.phase_ns[8], t);
+    }
   } else {
     pdl_wait();
     pdl_trigger();
@@ -143,6 +150,27 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
   const int rb1 = rbase + static_cast<int>((static_cast<long long>(my + 1) * nrb) / ncta);
   const int n_work = (rb1 - rb0) * ncb;
 
+  // MIX: this thread's gate-weight operands for the epilogue's partial logits, loaded now so
+  // their latency hides behind the stream (job q = tid / 8 of the first 32, rows sub + 8k of
+  // the band, sub = tid % 8; they do not depend on the previous kernel)
+  float wpre[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) wpre[k] = 0.f;
+  if constexpr (MODE == kModeMix) {
+    const int r0 = rb0 * RPB, nr = (rb1 - rb0) * RPB;
+    const int q = threadIdx.x >> 3, sub = threadIdx.x & 7;
+    if (p.part && nr <= kMixBandRows && threadIdx.x < kStreamWarps * 32 && q < 3 * p.E) {
+      const int which = q / p.E, e = q % p.E;
+      const float* w = which == 2 ? p.gate_w_next : (which == 1 && !p.do_guess ? nullptr : p.gate_w);
+      if (w) {
+        w += static_cast<size_t>(e) * p.d + r0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (sub + 8 * k < nr) wpre[k] = w[sub + 8 * k];
+      }
+    }
+  }
+
   const uint16_t* W[NM];
   if constexpr (MODE == kModeMix) {
     W[0] = p.M;
@@ -158,7 +186,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
   float4* pb = pa + C / 8;
   float* hs = reinterpret_cast<float*>(pb + C / 8);                 // MIX: layer input
   float* xch = hs + (MODE == kModeMix ? p.d : 0);                   // [RPB][WPR][NM] partials
-  uint64_t* full = reinterpret_cast<uint64_t*>(xch + 64);
+  float* hb = xch + 64;                                              // MIX: this CTA's h' rows
+  uint64_t* full = reinterpret_cast<uint64_t*>(xch + (MODE == kModeMix ? 64 + kMixBandRows : 64));
   uint64_t* empty = full + S;
 
   if (threadIdx.x == 0) {
@@ -221,6 +250,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
     }
     consumers_sync();
     stage_planes_n(hs, p.d, pa, pb, kStreamWarps * 32);
+    if (p.gate.phase_ns && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(&p.gate.phase_ns[9], t);
+    }
   } else if constexpr (MODE == kModeUp) {
     stage_planes_n(p.xin, p.d, pa, pb, kStreamWarps * 32);
     if (p.xscale) {  // RMSNorm applied on the fly: x = h' * (1 / rms(h'))
@@ -293,7 +327,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
       }
       if (part_id == 0 && lane == 0) {
         if constexpr (MODE == kModeMix) {
-          p.h_mid[r] = __fadd_rn(hs[r], __fmul_rn(p.alpha, v[0]));
+          const float hm = __fadd_rn(hs[r], __fmul_rn(p.alpha, v[0]));
+          p.h_mid[r] = hm;
+          if (r - rb0 * RPB < kMixBandRows) hb[r - rb0 * RPB] = hm;
         } else if constexpr (MODE == kModeUp) {
           p.act[static_cast<size_t>(slot[a]) * p.f + r] = v[0] / (1.f + expf(-v[0])) * v[NM - 1];
         } else {
@@ -307,7 +343,40 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
       // gate logits fused into the mixing epilogue: this CTA's rows [r0, r1) of
       //   route  W_l h',  guess  W_l h_in,  early  W_{l+1} h',  and sum h'^2, sum h_in^2
       consumers_sync();
+      if (p.gate.phase_ns && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(&p.gate.phase_ns[10], t);
+      }
       const int r0 = rb0 * RPB, r1 = rb1 * RPB, E = p.E, njob = 3 * E + 2;
+      if (r1 - r0 <= kMixBandRows) {
+        // eight threads per job, each over every 8th row of the band with its operands in
+        // registers (weights) and shared memory (h', h_in), then a fixed xor tree: no global
+        // round trip on this serial path
+        const int nr = r1 - r0, sub = threadIdx.x & 7;
+        for (int q0 = 0; q0 < njob; q0 += kStreamWarps * 4) {
+          const int q = q0 + (threadIdx.x >> 3);
+          float acc = 0.f;
+          if (q < njob) {
+            const int which = q < 3 * E ? q / E : 3, e = q < 3 * E ? q % E : q - 3 * E;
+            const bool on = !(which == 1 && !p.do_guess) && !(which == 2 && !p.gate_w_next);
+            const float* wg = which == 2 ? p.gate_w_next : p.gate_w;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int r = sub + 8 * k;
+              if (r < nr && on) {
+                const float vh = which == 1 || (which == 3 && e == 1) ? hs[r0 + r] : hb[r];
+                const float w = which == 3 ? vh : (q0 == 0 ? wpre[k] : wg[static_cast<size_t>(e) * p.d + r0 + r]);
+                acc = fmaf(w, vh, acc);
+              }
+            }
+          }
+          acc += __shfl_xor_sync(FULL, acc, 4);
+          acc += __shfl_xor_sync(FULL, acc, 2);
+          acc += __shfl_xor_sync(FULL, acc, 1);
+          if (q < njob && sub == 0) p.part[static_cast<size_t>(blockIdx.x) * njob + q] = acc;
+        }
+      } else
       for (int q = warp; q < njob; q += kStreamWarps) {
         const int which = q < 3 * E ? q / E : 3, e = q < 3 * E ? q % E : q - 3 * E;
         float acc = 0.f;
@@ -329,6 +398,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
         // a static __shared__ would push static + 227 KB dynamic past the per-CTA limit
         volatile int* s_last = reinterpret_cast<volatile int*>(xch + 63);
         consumers_sync();
+        if (p.gate.phase_ns && threadIdx.x == 0) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          atomicMax(&p.gate.phase_ns[15], t);
+        }
         if (threadIdx.x == 0) {
           __threadfence();
           *s_last = atomicAdd(p.done_ctr, 1u) == gridDim.x - 1;
@@ -396,7 +470,8 @@ inline StreamGeom stream_geometry_rpb(int mode, int d, int f, int stage_budget, 
   }
   if (g.ncb == 0) return g;
   const size_t stage = static_cast<size_t>(g.cb) * 2 * rpb * NM;
-  const size_t fixed = static_cast<size_t>(C) * 4 + (mode == kModeMix ? static_cast<size_t>(d) * 4 : 0) + 64 * 4;
+  const size_t fixed = static_cast<size_t>(C) * 4 +
+                       (mode == kModeMix ? static_cast<size_t>(d) * 4 + kMixBandRows * 4 : 0) + 64 * 4;
   if (fixed + 2 * stage + 256 > 227 * 1024) {
     g.ncb = 0;
     return g;
