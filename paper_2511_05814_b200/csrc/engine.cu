@@ -1086,7 +1086,11 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
   // bf16 path: bulk-copy streaming GEMVs (stream_gemv.cuh)
   StreamGeom gmix{}, gup{}, gdown{};
   if (g->bf16) {
-    gmix = stream_geometry(kModeMix, D, g->f);
+    // MIX rows per block: MOE_MIX_RPB (A/B; 0 = the default geometry)
+    static const int mix_rpb = getenv("MOE_MIX_RPB") ? atoi(getenv("MOE_MIX_RPB")) : 0;
+    static const int mix_kb = getenv("MOE_MIX_STAGE_KB") ? atoi(getenv("MOE_MIX_STAGE_KB")) : 0;
+    gmix = stream_geometry(kModeMix, D, g->f, mix_kb * 1024, 6, mix_rpb);
+    if (gmix.ncb == 0) gmix = stream_geometry(kModeMix, D, g->f);
     gup = stream_geometry(kModeUp, D, g->f);
     gdown = stream_geometry(kModeDown, D, g->f);
     MOE_REQUIRE(gmix.ncb && gup.ncb && gdown.ncb,

@@ -241,12 +241,52 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
   // ---------------- consumers: stage the activation vector ----------------
   if constexpr (MODE == kModeMix) {
     pdl_wait();   // the previous layer's outputs (a no-op unless launched programmatically)
+    constexpr int kI4 = 8;   // float4s per thread staged with every load in flight (d <= 8192)
+    if (!p.x && p.K <= 2 && p.d <= kI4 * 4 * kStreamWarps * 32) {
+      // h_in = h'_{l-1} + p_0 y_0 + p_1 y_1 (selection order, as combine4): all of this
+      // thread's loads issued before the first use -- one L2 round trip, not one per expert
+      const int K = p.K;
+      const float p0 = p.prev->prob[0], p1 = K > 1 ? p.prev->prob[1] : 0.f;
+      const float4* hm = reinterpret_cast<const float4*>(p.prev_mid);
+      const float4* y0 = reinterpret_cast<const float4*>(p.y);
+      const float4* y1 = reinterpret_cast<const float4*>(p.y + p.d);
+      float4 a[kI4], b[kI4], c[kI4];
+#pragma unroll
+      for (int u = 0; u < kI4; ++u) {
+        const int i4 = threadIdx.x + u * kStreamWarps * 32;
+        if (i4 < p.d / 4) {
+          a[u] = hm[i4];
+          b[u] = y0[i4];
+          if (K > 1) c[u] = y1[i4];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kI4; ++u) {
+        const int i4 = threadIdx.x + u * kStreamWarps * 32;
+        if (i4 < p.d / 4) {
+          float4 v = a[u];
+          v.x = __fadd_rn(v.x, __fmul_rn(p0, b[u].x));
+          v.y = __fadd_rn(v.y, __fmul_rn(p0, b[u].y));
+          v.z = __fadd_rn(v.z, __fmul_rn(p0, b[u].z));
+          v.w = __fadd_rn(v.w, __fmul_rn(p0, b[u].w));
+          if (K > 1) {
+            v.x = __fadd_rn(v.x, __fmul_rn(p1, c[u].x));
+            v.y = __fadd_rn(v.y, __fmul_rn(p1, c[u].y));
+            v.z = __fadd_rn(v.z, __fmul_rn(p1, c[u].z));
+            v.w = __fadd_rn(v.w, __fmul_rn(p1, c[u].w));
+          }
+          reinterpret_cast<float4*>(hs)[i4] = v;
+          if (blockIdx.x == 0) reinterpret_cast<float4*>(p.h_in)[i4] = v;
+        }
+      }
+    } else {
 #pragma unroll 4
-    for (int i4 = threadIdx.x; i4 < p.d / 4; i4 += kStreamWarps * 32) {
-      const float4 v = p.x ? reinterpret_cast<const float4*>(p.x)[i4]
-                           : combine4(p.prev_mid, p.y, p.prev, p.K, p.d, i4);
-      reinterpret_cast<float4*>(hs)[i4] = v;
-      if (blockIdx.x == 0) reinterpret_cast<float4*>(p.h_in)[i4] = v;
+      for (int i4 = threadIdx.x; i4 < p.d / 4; i4 += kStreamWarps * 32) {
+        const float4 v = p.x ? reinterpret_cast<const float4*>(p.x)[i4]
+                             : combine4(p.prev_mid, p.y, p.prev, p.K, p.d, i4);
+        reinterpret_cast<float4*>(hs)[i4] = v;
+        if (blockIdx.x == 0) reinterpret_cast<float4*>(p.h_in)[i4] = v;
+      }
     }
     consumers_sync();
     stage_planes_n(hs, p.d, pa, pb, kStreamWarps * 32);
