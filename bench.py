@@ -89,7 +89,8 @@ def parse_args():
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--variants", default=None,
                    help="headline = the first; policy[+prefetch][@cache_size]. Default: configs[1] "
-                        "and [2] (LRU, LFU, LFU+prefetch at C=4; LFU, LFU+prefetch at C=2 and 6) "
+                        "and [2] (LRU, LFU, LFU+prefetch, LRU+prefetch at C=4; LFU, LFU+prefetch "
+                        "at C=2; LRU, LFU, LFU+prefetch at C=6) "
                         "for 8x7B, configs[4] (LFU+prefetch at C=4) for 8x22B")
     p.add_argument("--e2e-steps", type=int, default=-1,
                    help="tokens replayed through the public API (-1 = all --steps timed tokens, "
@@ -479,7 +480,7 @@ def run_ours(args, world, rank, local):
     factory = EngineConfig.mixtral_8x22b if args.model == "mixtral_8x22b" else EngineConfig.mixtral_8x7b
     if args.variants is None:
         args.variants = ("lfu+prefetch" if args.model == "mixtral_8x22b" else
-                         "lru,lfu,lfu+prefetch,lfu@2,lfu+prefetch@2,lfu@6,lfu+prefetch@6")
+                         "lru,lfu,lfu+prefetch,lru+prefetch,lfu@2,lfu+prefetch@2,lru@6,lfu@6,lfu+prefetch@6")
     variants = [v for v in args.variants.split(",") if v]
     if args.sweep_cache:
         variants = [f"{p}@{c}" for c in args.sweep_cache.split(",") for p in ("lfu", "lfu+prefetch")]
