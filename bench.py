@@ -698,6 +698,7 @@ def run_ours(args, world, rank, local):
     if coded is not None:
         barrier(world)
         coded.close()
+    ffn_iso = isolated_ffn(D, F) if rank == 0 and world == 1 else None
     gemm_iso = isolated_gemm(D, F) if rank == 0 and args.prefill_tokens > 0 else None
     gemm_iso_t = isolated_gemm(D, F, 1024) if rank == 0 and args.prefill_tokens > 0 else None
     tiny = run_tiny(args) if rank == 0 and world == 1 and args.tiny_tokens > 0 else None
@@ -798,6 +799,7 @@ def run_ours(args, world, rank, local):
             "peak_source": peaks.get("source", "MEASURED_PEAKS.json hbm_gbs"),
         },
         "roofline_decode": roofline_decode,
+        "ffn_isolated_events": ffn_iso,
         "kernel_timing": ("per-launch CUDA events + in-kernel spans on an identical replay of the "
                           "timed tokens (same starting cache state); that replay ran at "
                           f"{profiled_tps:.3f} tokens/s, the headline without the events"),
@@ -1192,6 +1194,32 @@ def cpu_prefill_sample(seed, P, X, layers=1, layout="ref"):
     return {"value": P / per_batch, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"{P} tokens x {layers} of {L} layers ({what}), scaled by {L}/{layers}; "
                       f"{dt:.1f} s timed, {t_gen:.1f} s untimed weight materialisation"}
+
+
+def isolated_ffn(Dd, Ff):
+    """The decode FFN GEMVs alone (moe_microbench_gemv): resident experts, no copies in flight,
+    20 back-to-back launches under one CUDA-event pair (launch gaps included) over rotating
+    weight sets larger than L2 -- the event-timed counterpart of `roofline_ffn`'s in-kernel
+    figure without the per-launch inflation concurrent DMA adds (profiles/box_probe_r2.md)."""
+    import ctypes
+
+    import torch
+
+    from paper_2511_05814_b200 import _native
+
+    lib = _native.lib()
+    peak = float(measured_peaks().get("hbm_gbs", 6650.0))
+    out = {}
+    for name, kernel, experts in (("up_1_expert", 1, 1), ("up_2_experts", 1, 2),
+                                  ("down_1_expert", 2, 1), ("down_2_experts", 2, 2)):
+        ms, nb = ctypes.c_float(), ctypes.c_int64()
+        _native.check(lib.moe_microbench_gemv(kernel, Dd, Ff, experts, 0, 6, 0, 0, 20,
+                                              ctypes.byref(ms), ctypes.byref(nb)))
+        gbs = nb.value / (ms.value / 1e3) / 1e9
+        out[name] = {"us": round(ms.value * 1e3, 1), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3)}
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
 
 
 def isolated_gemm(Dd, Ff, m=128):
