@@ -1066,8 +1066,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
     // between consecutive kernels drains the SMs (seen as ~20 us gaps around the FFN launches)
     if (!getenv("MOE_NO_CARVEOUT")) {
       const int mx = cudaSharedmemCarveoutMaxShared;
-      cudaFuncSetAttribute(gate_cache_kernel<8>, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
-      cudaFuncSetAttribute(gate_cache_kernel<kMaxE>, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
+      cudaFuncSetAttribute(gate_cache_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
       cudaFuncSetAttribute(fetch_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
       cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
       cudaFuncSetAttribute(token_begin_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, mx);
@@ -1289,10 +1288,7 @@ moe_status moe_engine_decode_routed(moe_engine* g, const float* h_in_dev, int64_
         at[0].val.programmaticStreamSerializationAllowed = g->no_pdl ? 0 : 1;
         lc.attrs = at;
         lc.numAttrs = 1;
-        if (c.num_experts <= 8)
-          MOE_CUDA(cudaLaunchKernelEx(&lc, gate_cache_kernel<8>, gp));
-        else
-          MOE_CUDA(cudaLaunchKernelEx(&lc, gate_cache_kernel<kMaxE>, gp));
+        MOE_CUDA(cudaLaunchKernelEx(&lc, gate_cache_kernel, gp));
         MOE_LAUNCHED();
       }
       if (g->profiling) MOE_CUDA(cudaEventRecord(pe[2], s));

@@ -412,7 +412,7 @@ struct GateSmem {
 // The gate + cache step run by `nthreads` threads (tid in [0, nthreads), a multiple of 32):
 // as its own single-CTA kernel (gate_cache_kernel) or by the last CTA of the fused mixing
 // GEMV (stream_gemv_kernel<kModeMix>, fuse_gate).  sync() is a barrier over those threads.
-template <int EM, class Sync>
+template <class Sync>
 __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& gsm, int tid,
                                                 int nthreads, Sync sync, bool wait_pdl) {
   float (&z)[3][kMaxE] = gsm.z;
@@ -795,11 +795,11 @@ __device__ __forceinline__ void gate_cache_body(const GateParams& p, GateSmem& g
   }
 }
 
-template <int EM>  // compile-time bound on E (8 for Mixtral) so the accumulators stay in registers
-__global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) {
+// (internal linkage: this header is included by several translation units)
+static __global__ void __launch_bounds__(kGateThreads) gate_cache_kernel(GateParams p) {
   pdl_trigger();  // the FFN pass may launch and wait for the decision meanwhile
   __shared__ GateSmem gsm;
-  gate_cache_body<EM>(p, gsm, threadIdx.x, blockDim.x, [] { __syncthreads(); }, true);
+  gate_cache_body(p, gsm, threadIdx.x, blockDim.x, [] { __syncthreads(); }, true);
 }
 
 // ---- K3: expert FFN over the selected slots ---------------------------------------------

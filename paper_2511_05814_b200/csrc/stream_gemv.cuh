@@ -453,10 +453,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_gemv_kernel(StreamPa
           // the stage ring is idle (every stage consumed): it holds the gate's working set
           GateSmem& gsm = *reinterpret_cast<GateSmem*>(stage_base);
           if (threadIdx.x == 0) *p.done_ctr = 0u;   // ready for the next launch (stream order)
-          if (p.gate.E <= 8)
-            gate_cache_body<8>(p.gate, gsm, threadIdx.x, kStreamWarps * 32, [] { consumers_sync(); }, false);
-          else
-            gate_cache_body<kMaxE>(p.gate, gsm, threadIdx.x, kStreamWarps * 32, [] { consumers_sync(); }, false);
+          gate_cache_body(p.gate, gsm, threadIdx.x, kStreamWarps * 32, [] { consumers_sync(); }, false);
         }
       }
     }
