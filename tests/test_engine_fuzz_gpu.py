@@ -83,3 +83,60 @@ def test_random_config_matches_oracle(i):
         assert st["demand_bytes"] == st["misses"] * cfg.expert_bytes, kw
     if cfg.transfer == "copy_engine":
         assert st["h2d_bytes"] == st["demand_link_bytes"] + st["prefetch_bytes"], kw
+
+
+def draw_prefill(i):
+    rng = np.random.default_rng(2000 + i)
+    E = int(rng.choice([2, 4, 8, 16]))
+    K = int(rng.integers(1, min(E, 4) + 1))
+    C = int(rng.integers(K, E + 1))
+    d = int(rng.choice([256, 512]))
+    return dict(
+        num_layers=int(rng.integers(2, 5)), num_experts=E, top_k=K, hidden_dim=d,
+        ffn_dim=int(rng.choice([512, 768, 1792])), expert_kind="swiglu", cache_size=C,
+        policy=PolicyKind.parse(str(rng.choice(POLICIES))),
+        mixing_scale=0.1 * math.sqrt(16 / d), rms_norm=True,
+        renormalize=bool(rng.integers(0, 2)), compress=int(rng.integers(0, 2)),
+        transfer="copy_engine", max_tokens=512,
+    ), int(rng.choice([1, 33, 128, 257]))
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_random_prefill_matches_oracle(i):
+    """The batched prefill (tcgen05 grouped GEMMs, the policy replayed over the batch in token
+    order) on random shapes / policies / batch sizes: selections vs the oracle's prefill
+    restatement (disagreements only at stated near-ties), outputs, trace == replay, and one
+    load per needed, uncached expert per layer."""
+    kw, T = draw_prefill(i)
+    cfg = EngineConfig(**kw)
+    seed = 70 + i
+    X = oracle.MixtralRef.inputs(seed, T, cfg.hidden_dim)
+    with OffloadEngine(cfg) as eng:
+        eng.init_random(seed)
+        out = eng.prefill(X)
+        rec = eng.records(0, T)
+        st = eng.stats()
+    ref = oracle.MixtralRef(cfg.num_layers, cfg.num_experts, cfg.top_k, cfg.hidden_dim,
+                            cfg.ffn_dim, cfg.mixing_scale, seed=seed, layout="ref",
+                            renormalize=cfg.renormalize, rms_norm=cfg.rms_norm,
+                            rms_eps=cfg.rms_eps)
+    ref_out, ref_acts, _, gaps = oracle.mixtral_prefill(ref, X, return_gaps=True)
+    diff = np.any(rec["acts"] != ref_acts, axis=2)
+    assert not np.any(diff & (gaps > 1e-3)), (kw, T, np.argwhere(diff))
+    ok = ~diff.any(axis=1)
+    if ok.any():
+        rel = np.abs(out[ok] - ref_out[ok]).max() / np.abs(ref_out[ok]).max()
+        assert rel < 1e-2, (kw, T, rel)
+    code, df, dp = cfg.policy.device_params()
+    rb, ev = replay_layers(rec["acts"], cfg.num_experts, cfg.cache_size, code, df, dp)
+    assert np.array_equal(rec["resident_before"], np.transpose(rb, (1, 0, 2))), (kw, T)
+    assert np.array_equal(rec["evicted"], np.transpose(ev, (1, 0, 2))), (kw, T)
+    loads = 0
+    for l in range(cfg.num_layers):
+        needed = np.zeros(cfg.num_experts, bool)
+        needed[np.unique(rec["acts"][:, l])] = True
+        loads += int(np.sum(needed & (rec["resident_before"][0, l] == 0)))
+    if cfg.compress:   # the link carries the exponent-coded parts of the same loads
+        assert 0.5 * loads * cfg.expert_bytes < st["prefill_bytes"] < 0.8 * loads * cfg.expert_bytes, (kw, T)
+    else:
+        assert st["prefill_bytes"] == loads * cfg.expert_bytes, (kw, T)
