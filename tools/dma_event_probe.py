@@ -1,6 +1,8 @@
 """Do busy H2D copies (another stream) inflate a kernel's CUDA-event span?  Times a D2D copy
-kernel (~235 MB, HBM-bound) with events on stream A, with and without a pinned H2D copy loop
-on stream B, and the same kernels back to back (event pairs around each)."""
+(~235 MB, HBM-bound) with events on stream A, with and without a pinned H2D copy loop on stream
+B, and the same copies back to back (event pairs around each).  Caveat (round 2): a contiguous
+D2D `copy_` may run on a copy engine rather than the SMs; tools/event_chunk_probe.py repeats the
+measurement with an SM kernel and per H2D chunk size (profiles/box_probe_r2.md)."""
 import torch
 
 n = 235 * 2**20
