@@ -698,11 +698,12 @@ def run_ours(args, world, rank, local):
     if coded is not None:
         barrier(world)
         coded.close()
-    ffn_iso = isolated_ffn(D, F) if rank == 0 and world == 1 else None
     gemm_iso = isolated_gemm(D, F) if rank == 0 and args.prefill_tokens > 0 else None
     gemm_iso_t = isolated_gemm(D, F, 1024) if rank == 0 and args.prefill_tokens > 0 else None
     tiny = run_tiny(args) if rank == 0 and world == 1 and args.tiny_tokens > 0 else None
     replay = run_replay(args) if rank == 0 and world == 1 and args.replay_streams > 0 else None
+    # last of the GPU sections: its allocations and frees cannot disturb the timed ones above
+    ffn_iso = isolated_ffn(D, F) if rank == 0 and world == 1 else None
     if store is not None:
         barrier(world)
         store.close()
@@ -933,26 +934,32 @@ def run_tiny(args):
     cfg = ToyModelConfig(ModelShape(Lt, Et, Kt), hidden_dim=dt, mixing_scale=0.1, seed=42, tokens=T)
     model, rng = ToyMoeModel.build(cfg)
     inputs = rng.standard_normal((T, dt))
+    reps = 3
     ecfg = EngineConfig(num_layers=Lt, num_experts=Et, top_k=Kt, hidden_dim=dt, expert_kind="toy_tanh",
-                        cache_size=2, policy=PolicyKind.lru(), mixing_scale=0.1, max_tokens=T + 64)
+                        cache_size=2, policy=PolicyKind.lru(), mixing_scale=0.1,
+                        max_tokens=(reps + 1) * T + 64)
     stream = torch.cuda.current_stream()
     with OffloadEngine(ecfg) as eng:
         eng.load_toy_model(model)
         x = torch.from_numpy(inputs.astype(np.float32)).cuda()
-        eng.decode_device(x[:16])            # warm-up
-        eng.sync()
-        eng.reset()
-        n0 = _native.kernel_launches()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        a.record(stream)
+        # warm-up: the whole stream once (a ~0.1 s latency-bound section follows CPU-only work,
+        # so the GPU must be back at full clock), then the best of `reps` cold-cache passes
         eng.decode_device(x)
-        b.record(stream)
-        torch.cuda.synchronize()
         eng.sync()
-        ms = a.elapsed_time(b)
-        launches = _native.kernel_launches() - n0
-        rec = eng.records(16, T)
+        ms, launches = float("inf"), 0
+        for r in range(reps):
+            eng.reset()
+            n0 = _native.kernel_launches()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            eng.decode_device(x)
+            b.record(stream)
+            torch.cuda.synchronize()
+            eng.sync()
+            ms = min(ms, a.elapsed_time(b))
+            launches = _native.kernel_launches() - n0
+        rec = eng.records(reps * T, T)
         eng.reset()
         t0 = time.perf_counter()
         eng.decode(inputs[:64].astype(np.float32))   # public API, host arrays, synced
@@ -964,7 +971,8 @@ def run_tiny(args):
     cpu_s = time.perf_counter() - t0
     return {"workload": "configs[0]: tiny MoE (4 layers, 8 experts top-2, d=256) decode, LRU cache "
                         "2/layer (toy tanh experts, f32 on the GPU)",
-            "tokens": T, "tokens_per_s": T / (ms / 1e3), "us_per_token": ms * 1e3 / T,
+            "tokens": T, "timing": f"best of {reps} cold-cache passes after a full warm-up pass",
+            "tokens_per_s": T / (ms / 1e3), "us_per_token": ms * 1e3 / T,
             "launches_per_token": launches / T, "e2e_tokens_per_s": e2e_tps,
             "trace_equals_oracle": bool(np.array_equal(rec["acts"], acts)),
             "cpu_baseline": {"value": T / cpu_s, "unit": "tokens/s", "cores": os.cpu_count(),
